@@ -1,0 +1,601 @@
+// =============================================================================
+// egfem_oracle.cpp — plain, slow, obviously-correct CPU oracle for the EGFEM hot
+// path (arXiv 2005.06193).  TEST INFRASTRUCTURE ONLY: it may be loaded solely by
+// tests/, __graft_entry__.smoke() and bench.py's cpu_baseline / --impl reference
+// legs.  It shares no code, header, table or constant generator with the CUDA
+// path (paper_2005_06193_b200/csrc) and neither side includes the other.
+//
+// Everything is fp64, single-threaded, sequential, in the paper's order:
+//   * T_ijk = ∫ (slot_a φ_i)(slot_b φ_j)(slot_c η_k) dx assembled element by
+//     element with a quadrature rule (eq. (egfem_terms);
+//     L253 K_a; L327 M; L400 N), duplicates summed in emission order, stored as
+//     SPEC's lexicographically sorted COO.
+//   * w = f(Π_u u, Π_∇u ·₂ u) pointwise at the W-DOFs (PAPER.md L96–99 eq.
+//     (egfem_coeffs), L153–169 §3.2).
+//   * r = T:(u⊗w), r_i = Σ_jk T_ijk u_j w_k.
+//   * A = T·w and the Newton Jacobian
+//     J = T·w + (T·₂u)·D_u w, the Schur complement of the block Jacobian of
+//     PAPER.md L290 (reading C10 in DESIGN.md), formed as a literal sparse
+//     block product.
+//
+// Pinned by tests/test_oracle_*.py (closed forms, brute force, partition of unity,
+// symmetry, Euler homogeneity, finite differences, Case-1 exactness).
+// =============================================================================
+#include <algorithm>
+#include <cmath>
+#include <cstdint>
+#include <cstring>
+#include <map>
+#include <numeric>
+#include <vector>
+
+namespace {
+
+enum { OF_P0 = 0, OF_P1 = 1, OF_P2 = 2 };
+enum { OFORM_CONV_K = 0, OFORM_CONV_J = 1, OFORM_PLAP = 2, OFORM_MASS3 = 3, OFORM_CONV_I = 4 };
+enum { OK_IDENTITY = 0, OK_SQUARE = 1, OK_GRADPOW_P0 = 2, OK_P1_TO_P2_SQUARE = 3 };
+enum { OJ_PICARD = 0, OJ_NEWTON = 1 };
+
+// Slot operators: which functional of a basis function enters a slot.
+enum { OP_VALUE = 0, OP_DX = 1, OP_DXDY = 2, OP_GRAD = 3 };
+
+struct Space {
+  int family;
+  int64_t n_dofs;
+  int n_loc;
+  std::vector<int32_t> cell_dofs;  // n_cells * n_loc
+};
+
+struct OTensor {
+  // mesh
+  int dim;
+  int64_t n_vertices, n_cells;
+  std::vector<double> coords;
+  std::vector<int32_t> cells;
+  Space V, W;
+  int form;
+  int64_t row_begin, row_end;
+  // canonical tensor (rows outside [row_begin,row_end) are empty)
+  std::vector<int64_t> t_row_ptr;
+  std::vector<int32_t> t_j, t_k;
+  std::vector<double> t_val;
+  // CSR pattern (union of element cliques over V-DOFs)
+  std::vector<int64_t> csr_row_ptr;
+  std::vector<int32_t> csr_col;
+};
+
+// ---------------------------------------------------------------- geometry
+// Affine map x = x0 + B ξ with B = [x1-x0, ..., xd-x0]; ∇λ_{1..d} are the rows of
+// B^{-1} and ∇λ_0 = -Σ_{a≥1} ∇λ_a; |K| = |det B| / d!.
+struct Geo {
+  double grad[4][3];  // grad[a][x]
+  double vol;
+};
+
+static double det3(const double m[3][3]) {
+  return m[0][0] * (m[1][1] * m[2][2] - m[1][2] * m[2][1])
+       - m[0][1] * (m[1][0] * m[2][2] - m[1][2] * m[2][0])
+       + m[0][2] * (m[1][0] * m[2][1] - m[1][1] * m[2][0]);
+}
+
+static Geo geometry(const OTensor& T, int64_t cell) {
+  Geo g;
+  std::memset(&g, 0, sizeof(g));
+  const int d = T.dim;
+  const int32_t* cv = &T.cells[cell * (d + 1)];
+  double B[3][3] = {{0}};
+  for (int r = 0; r < d; ++r)
+    for (int c = 0; c < d; ++c)
+      B[r][c] = T.coords[(int64_t)cv[c + 1] * d + r] - T.coords[(int64_t)cv[0] * d + r];
+  double Binv[3][3] = {{0}};
+  double det = 0;
+  if (d == 1) {
+    det = B[0][0];
+    Binv[0][0] = 1.0 / det;
+  } else if (d == 2) {
+    det = B[0][0] * B[1][1] - B[0][1] * B[1][0];
+    Binv[0][0] = B[1][1] / det;
+    Binv[0][1] = -B[0][1] / det;
+    Binv[1][0] = -B[1][0] / det;
+    Binv[1][1] = B[0][0] / det;
+  } else {
+    det = det3(B);
+    // inverse = adj(B)/det, adj = transpose of cofactor matrix
+    for (int r = 0; r < 3; ++r)
+      for (int c = 0; c < 3; ++c) {
+        int r1 = (c + 1) % 3, r2 = (c + 2) % 3, c1 = (r + 1) % 3, c2 = (r + 2) % 3;
+        Binv[r][c] = (B[r1][c1] * B[r2][c2] - B[r1][c2] * B[r2][c1]) / det;
+      }
+  }
+  double fact = (d == 1) ? 1.0 : (d == 2 ? 2.0 : 6.0);
+  g.vol = std::fabs(det) / fact;
+  for (int a = 1; a <= d; ++a)
+    for (int x = 0; x < d; ++x) g.grad[a][x] = Binv[a - 1][x];
+  for (int x = 0; x < d; ++x) {
+    double s = 0;
+    for (int a = 1; a <= d; ++a) s += g.grad[a][x];
+    g.grad[0][x] = -s;
+  }
+  return g;
+}
+
+// ---------------------------------------------------------------- bases
+// Lagrange bases in barycentric coordinates λ (dim+1 entries).
+// P0: 1.  P1: λ_a.  P2 (2D only, local order v0,v1,v2,m01,m12,m20):
+//   vertex a: λ_a(2λ_a-1),  midpoint (a,b): 4 λ_a λ_b.
+static void basis(int family, int d, const double* lam, const Geo& g, int n_loc,
+                  double* val, double (*grad)[3]) {
+  for (int l = 0; l < n_loc; ++l) {
+    val[l] = 0;
+    for (int x = 0; x < 3; ++x) grad[l][x] = 0;
+  }
+  if (family == OF_P0) {
+    val[0] = 1.0;
+  } else if (family == OF_P1) {
+    for (int a = 0; a <= d; ++a) {
+      val[a] = lam[a];
+      for (int x = 0; x < d; ++x) grad[a][x] = g.grad[a][x];
+    }
+  } else {  // P2, d == 2
+    for (int a = 0; a < 3; ++a) {
+      val[a] = lam[a] * (2 * lam[a] - 1);
+      for (int x = 0; x < d; ++x) grad[a][x] = (4 * lam[a] - 1) * g.grad[a][x];
+    }
+    const int ea[3] = {0, 1, 2}, eb[3] = {1, 2, 0};
+    for (int m = 0; m < 3; ++m) {
+      int a = ea[m], b = eb[m];
+      val[3 + m] = 4 * lam[a] * lam[b];
+      for (int x = 0; x < d; ++x) grad[3 + m][x] = 4 * (lam[a] * g.grad[b][x] + lam[b] * g.grad[a][x]);
+    }
+  }
+}
+
+static int family_degree(int f) { return f == OF_P0 ? 0 : (f == OF_P1 ? 1 : 2); }
+
+// ---------------------------------------------------------------- quadrature
+// Reference rules in barycentric coordinates, weights summing to 1 (physical
+// weight = weight × |K|).  1D: 3-point Gauss.  2D: centroid (deg 1),
+// (2/3,1/6,1/6) (deg 2), 6-point symmetric Dunavant (deg 4).  3D: centroid,
+// 4-point (deg 2).
+struct Rule {
+  int nq;
+  std::vector<double> bary;  // nq*(d+1)
+  std::vector<double> w;
+};
+
+static Rule default_rule(int d, int degree) {
+  Rule R;
+  if (d == 1) {
+    double s = std::sqrt(3.0 / 5.0);
+    double xi[3] = {(1 - s) / 2, 0.5, (1 + s) / 2};
+    double w[3] = {5.0 / 18, 8.0 / 18, 5.0 / 18};
+    R.nq = 3;
+    for (int q = 0; q < 3; ++q) {
+      R.bary.push_back(1 - xi[q]);
+      R.bary.push_back(xi[q]);
+      R.w.push_back(w[q]);
+    }
+    return R;
+  }
+  if (d == 2) {
+    if (degree <= 1) {
+      R.nq = 1;
+      R.bary = {1.0 / 3, 1.0 / 3, 1.0 / 3};
+      R.w = {1.0};
+    } else if (degree <= 2) {
+      R.nq = 3;
+      R.bary = {2.0 / 3, 1.0 / 6, 1.0 / 6, 1.0 / 6, 2.0 / 3, 1.0 / 6, 1.0 / 6, 1.0 / 6, 2.0 / 3};
+      R.w = {1.0 / 3, 1.0 / 3, 1.0 / 3};
+    } else {
+      // Two S21 orbits (a, a, 1-2a): degree-4 exact (reading C3).
+      const double a1 = 0.445948490915965, w1 = 0.2233815896780118;
+      const double a2 = 0.091576213509770549, w2 = 0.10995174365532154;
+      const double A[2] = {a1, a2}, W[2] = {w1, w2};
+      R.nq = 6;
+      for (int o = 0; o < 2; ++o) {
+        double a = A[o], b = 1 - 2 * a;
+        double pts[3][3] = {{b, a, a}, {a, b, a}, {a, a, b}};
+        for (int q = 0; q < 3; ++q) {
+          for (int x = 0; x < 3; ++x) R.bary.push_back(pts[q][x]);
+          R.w.push_back(W[o]);
+        }
+      }
+    }
+    return R;
+  }
+  // d == 3
+  if (degree <= 1) {
+    R.nq = 1;
+    R.bary = {0.25, 0.25, 0.25, 0.25};
+    R.w = {1.0};
+  } else {
+    const double a = 0.1381966011250105, b = 0.5854101966249685;
+    R.nq = 4;
+    for (int q = 0; q < 4; ++q)
+      for (int x = 0; x < 4; ++x) R.bary.push_back(x == q ? b : a);
+    R.w = {0.25, 0.25, 0.25, 0.25};
+  }
+  return R;
+}
+
+// Slot operators of each form, slot order (i, j, k) = (test, u-slot, w-slot).
+static void form_ops(int form, int* opA, int* opB, int* opC) {
+  switch (form) {
+    case OFORM_CONV_K: *opA = OP_VALUE; *opB = OP_VALUE; *opC = OP_DX; break;    // ∫ φ_i φ_j ∂x φ_k
+    case OFORM_CONV_J: *opA = OP_VALUE; *opB = OP_DXDY; *opC = OP_VALUE; break;  // ∫ φ_i (∂x+∂y)φ_j φ_k
+    case OFORM_PLAP:   *opA = OP_GRAD;  *opB = OP_GRAD; *opC = OP_VALUE; break;  // ∫ ψ_k ∇φ_i·∇φ_j
+    case OFORM_MASS3:  *opA = OP_VALUE; *opB = OP_VALUE; *opC = OP_VALUE; break; // ∫ φ_i φ_j η_k
+    default:           *opA = OP_DXDY;  *opB = OP_VALUE; *opC = OP_VALUE; break; // ∫ (∂x+∂y)φ_i φ_j φ_k (paper N)
+  }
+}
+
+static int op_degree(int op, int fam) {
+  int d = family_degree(fam);
+  if (op == OP_VALUE) return d;
+  return d > 0 ? d - 1 : 0;
+}
+
+static double apply_op(int op, int d, double val, const double* grad) {
+  if (op == OP_VALUE) return val;
+  if (op == OP_DX) return grad[0];
+  // (∂x + ∂y): sum of the first min(d,2) partial derivatives
+  double s = grad[0];
+  if (d >= 2) s += grad[1];
+  return s;
+}
+
+}  // namespace
+
+extern "C" {
+
+typedef struct OTensor OTensor_t;
+
+// Build the canonical tensor.  Returns 0 on success, negative on bad input.
+int oracle_build(int dim, int64_t n_vertices, const double* coords, int64_t n_cells,
+                 const int32_t* cells, int v_family, int64_t v_ndofs, int v_nloc,
+                 const int32_t* v_cell_dofs, int w_family, int64_t w_ndofs, int w_nloc,
+                 const int32_t* w_cell_dofs, int form, int nq, const double* qbary,
+                 const double* qw, int64_t row_begin, int64_t row_end, void** out) {
+  if (dim < 1 || dim > 3) return -1;
+  if (v_family == OF_P2 && dim != 2) return -2;
+  if (w_family == OF_P2 && dim != 2) return -2;
+  OTensor* T = new OTensor();
+  T->dim = dim;
+  T->n_vertices = n_vertices;
+  T->n_cells = n_cells;
+  T->coords.assign(coords, coords + n_vertices * dim);
+  T->cells.assign(cells, cells + n_cells * (dim + 1));
+  T->V = {v_family, v_ndofs, v_nloc, std::vector<int32_t>(v_cell_dofs, v_cell_dofs + n_cells * v_nloc)};
+  T->W = {w_family, w_ndofs, w_nloc, std::vector<int32_t>(w_cell_dofs, w_cell_dofs + n_cells * w_nloc)};
+  T->form = form;
+  if (row_begin < 0) row_begin = 0;
+  if (row_end < 0 || row_end > v_ndofs) row_end = v_ndofs;
+  T->row_begin = row_begin;
+  T->row_end = row_end;
+
+  int opA, opB, opC;
+  form_ops(form, &opA, &opB, &opC);
+  if (form == OFORM_PLAP && w_family != OF_P0 && nq <= 0) {
+    // PLAP with a non-P0 W still follows the quadrature definition below.
+  }
+  Rule R;
+  if (nq > 0) {
+    R.nq = nq;
+    R.bary.assign(qbary, qbary + nq * (dim + 1));
+    R.w.assign(qw, qw + nq);
+  } else {
+    int deg = op_degree(opA, v_family) + op_degree(opB, v_family) + op_degree(opC, w_family);
+    if (opA == OP_GRAD) deg = 2 * op_degree(OP_GRAD, v_family) + op_degree(opC, w_family);
+    R = default_rule(dim, deg);
+  }
+
+  // ---- emit every local triple, cell-major then (a,b,c) lexicographic
+  struct Trip { int32_t i, j, k; double v; };
+  std::vector<Trip> trips;
+  const int nA = v_nloc, nC = w_nloc;
+  std::vector<double> vv(nA), wv(nC), Tk(nA * nA * nC);
+  std::vector<double> vg(nA * 3), wg(nC * 3);
+  for (int64_t K = 0; K < n_cells; ++K) {
+    const int32_t* I = &T->V.cell_dofs[K * nA];
+    const int32_t* Wd = &T->W.cell_dofs[K * nC];
+    bool any = false;
+    for (int a = 0; a < nA; ++a) any |= (I[a] >= row_begin && I[a] < row_end);
+    if (!any) continue;
+    Geo g = geometry(*T, K);
+    std::fill(Tk.begin(), Tk.end(), 0.0);
+    for (int q = 0; q < R.nq; ++q) {
+      const double* lam = &R.bary[q * (dim + 1)];
+      basis(v_family, dim, lam, g, nA, vv.data(), reinterpret_cast<double(*)[3]>(vg.data()));
+      basis(w_family, dim, lam, g, nC, wv.data(), reinterpret_cast<double(*)[3]>(wg.data()));
+      double wq = R.w[q] * g.vol;
+      for (int a = 0; a < nA; ++a)
+        for (int b = 0; b < nA; ++b)
+          for (int c = 0; c < nC; ++c) {
+            double fab;
+            if (opA == OP_GRAD) {
+              fab = 0;
+              for (int x = 0; x < dim; ++x) fab += vg[a * 3 + x] * vg[b * 3 + x];
+            } else {
+              fab = apply_op(opA, dim, vv[a], &vg[a * 3]) * apply_op(opB, dim, vv[b], &vg[b * 3]);
+            }
+            double fc = apply_op(opC, dim, wv[c], &wg[c * 3]);
+            Tk[(a * nA + b) * nC + c] += wq * fab * fc;
+          }
+    }
+    for (int a = 0; a < nA; ++a) {
+      if (I[a] < row_begin || I[a] >= row_end) continue;
+      for (int b = 0; b < nA; ++b)
+        for (int c = 0; c < nC; ++c) trips.push_back({I[a], I[b], Wd[c], Tk[(a * nA + b) * nC + c]});
+    }
+  }
+
+  // ---- canonicalise: stable sort by (i,j,k), sum duplicates in emission order
+  std::vector<int64_t> order(trips.size());
+  std::iota(order.begin(), order.end(), 0);
+  std::stable_sort(order.begin(), order.end(), [&](int64_t x, int64_t y) {
+    const Trip& A = trips[x];
+    const Trip& B = trips[y];
+    if (A.i != B.i) return A.i < B.i;
+    if (A.j != B.j) return A.j < B.j;
+    return A.k < B.k;
+  });
+  T->t_row_ptr.assign(v_ndofs + 1, 0);
+  for (size_t s = 0; s < order.size();) {
+    const Trip& A = trips[order[s]];
+    double sum = 0;
+    size_t e = s;
+    while (e < order.size() && trips[order[e]].i == A.i && trips[order[e]].j == A.j &&
+           trips[order[e]].k == A.k) {
+      sum += trips[order[e]].v;
+      ++e;
+    }
+    T->t_j.push_back(A.j);
+    T->t_k.push_back(A.k);
+    T->t_val.push_back(sum);
+    T->t_row_ptr[A.i + 1]++;
+    s = e;
+  }
+  for (int64_t i = 0; i < v_ndofs; ++i) T->t_row_ptr[i + 1] += T->t_row_ptr[i];
+
+  // ---- CSR pattern: union over cells of (I[a], I[b]), sorted and unique per row
+  std::vector<std::pair<int32_t, int32_t>> pairs;
+  for (int64_t K = 0; K < n_cells; ++K) {
+    const int32_t* I = &T->V.cell_dofs[K * nA];
+    for (int a = 0; a < nA; ++a) {
+      if (I[a] < row_begin || I[a] >= row_end) continue;
+      for (int b = 0; b < nA; ++b) pairs.push_back({I[a], I[b]});
+    }
+  }
+  std::sort(pairs.begin(), pairs.end());
+  pairs.erase(std::unique(pairs.begin(), pairs.end()), pairs.end());
+  T->csr_row_ptr.assign(v_ndofs + 1, 0);
+  for (auto& pr : pairs) {
+    T->csr_col.push_back(pr.second);
+    T->csr_row_ptr[pr.first + 1]++;
+  }
+  for (int64_t i = 0; i < v_ndofs; ++i) T->csr_row_ptr[i + 1] += T->csr_row_ptr[i];
+  *out = T;
+  return 0;
+}
+
+void oracle_free(void* h) { delete static_cast<OTensor*>(h); }
+
+void oracle_sizes(const void* h, int64_t* nnz, int64_t* nnz_csr, int64_t* n_u, int64_t* n_f) {
+  const OTensor* T = static_cast<const OTensor*>(h);
+  *nnz = (int64_t)T->t_val.size();
+  *nnz_csr = (int64_t)T->csr_col.size();
+  *n_u = T->V.n_dofs;
+  *n_f = T->W.n_dofs;
+}
+
+static int64_t csr_find(const OTensor* T, int64_t i, int32_t col) {
+  const int32_t* b = T->csr_col.data() + T->csr_row_ptr[i];
+  const int32_t* e = T->csr_col.data() + T->csr_row_ptr[i + 1];
+  const int32_t* p = std::lower_bound(b, e, col);
+  if (p == e || *p != col) return -1;
+  return p - T->csr_col.data();
+}
+
+// Export canonical arrays (NULL = skip).  slot_ik only for W == V numbering,
+// loc only for P0 W (bits 0-1: local index of i in cell k, bits 2-3: of j).
+int oracle_export(const void* h, int64_t* t_row_ptr, int32_t* t_j, int32_t* t_k, double* t_val,
+                  int64_t* csr_row_ptr, int32_t* csr_col, int32_t* slot_ij, int32_t* slot_ik,
+                  uint8_t* loc) {
+  const OTensor* T = static_cast<const OTensor*>(h);
+  size_t nnz = T->t_val.size();
+  if (t_row_ptr) std::copy(T->t_row_ptr.begin(), T->t_row_ptr.end(), t_row_ptr);
+  if (t_j) std::copy(T->t_j.begin(), T->t_j.end(), t_j);
+  if (t_k) std::copy(T->t_k.begin(), T->t_k.end(), t_k);
+  if (t_val) std::copy(T->t_val.begin(), T->t_val.end(), t_val);
+  if (csr_row_ptr) std::copy(T->csr_row_ptr.begin(), T->csr_row_ptr.end(), csr_row_ptr);
+  if (csr_col) std::copy(T->csr_col.begin(), T->csr_col.end(), csr_col);
+  for (int64_t i = 0; i < T->V.n_dofs; ++i) {
+    for (int64_t e = T->t_row_ptr[i]; e < T->t_row_ptr[i + 1]; ++e) {
+      if (slot_ij) {
+        int64_t s = csr_find(T, i, T->t_j[e]);
+        if (s < 0) return -3;
+        slot_ij[e] = (int32_t)s;
+      }
+      if (slot_ik) {
+        int64_t s = csr_find(T, i, T->t_k[e]);
+        if (s < 0) return -4;
+        slot_ik[e] = (int32_t)s;
+      }
+      if (loc) {
+        const int32_t* cv = &T->V.cell_dofs[(int64_t)T->t_k[e] * T->V.n_loc];
+        int li = -1, lj = -1;
+        for (int a = 0; a < T->V.n_loc; ++a) {
+          if (cv[a] == i) li = a;
+          if (cv[a] == T->t_j[e]) lj = a;
+        }
+        if (li < 0 || lj < 0) return -5;
+        loc[e] = (uint8_t)(li | (lj << 2));
+      }
+    }
+  }
+  (void)nnz;
+  return 0;
+}
+
+// ---------------------------------------------------------------- interp
+// w = f(Π_u u, Π_∇u ·₂ u) at the W-DOFs.
+//   IDENTITY:        f(u) = u,  W = V  (GFEM, Π_u = identity, L338)
+//   SQUARE:          f(u) = u², W = V  (L336 with Π = identity)
+//   GRADPOW_P0:      f(∇u) = ‖∇u‖^{p-2} at the P0 DOF of each cell (L574, L582)
+//   P1_TO_P2_SQUARE: f(u) = u² at the P2 DOFs, w = (Π_u u) ⊙ (Π_u u) (L336)
+int oracle_interp(const void* h, int kind, double p, const double* u, double* w) {
+  const OTensor* T = static_cast<const OTensor*>(h);
+  const int d = T->dim;
+  if (kind == OK_IDENTITY || kind == OK_SQUARE) {
+    if (T->W.n_dofs != T->V.n_dofs) return -1;
+    for (int64_t k = 0; k < T->W.n_dofs; ++k) w[k] = (kind == OK_IDENTITY) ? u[k] : u[k] * u[k];
+    return 0;
+  }
+  if (kind == OK_GRADPOW_P0) {
+    if (T->W.family != OF_P0 || T->V.family != OF_P1) return -2;
+    for (int64_t K = 0; K < T->n_cells; ++K) {
+      Geo g = geometry(*T, K);
+      const int32_t* I = &T->V.cell_dofs[K * T->V.n_loc];
+      double gu[3] = {0, 0, 0};  // (Π_∇u ·₂ u) at the cell's DOF
+      for (int a = 0; a <= d; ++a)
+        for (int x = 0; x < d; ++x) gu[x] += u[I[a]] * g.grad[a][x];
+      double nrm = 0;
+      for (int x = 0; x < d; ++x) nrm += gu[x] * gu[x];
+      nrm = std::sqrt(nrm);
+      w[T->W.cell_dofs[K]] = std::pow(nrm, p - 2.0);
+    }
+    return 0;
+  }
+  if (kind == OK_P1_TO_P2_SQUARE) {
+    if (T->W.family != OF_P2 || T->V.family != OF_P1 || d != 2) return -2;
+    // DOF bary points of P2 local order v0,v1,v2,m01,m12,m20
+    const double beta[6][3] = {{1, 0, 0}, {0, 1, 0}, {0, 0, 1}, {0.5, 0.5, 0}, {0, 0.5, 0.5}, {0.5, 0, 0.5}};
+    for (int64_t K = 0; K < T->n_cells; ++K) {
+      const int32_t* I = &T->V.cell_dofs[K * 3];
+      const int32_t* Wd = &T->W.cell_dofs[K * 6];
+      for (int l = 0; l < 6; ++l) {
+        double v = 0;  // (Π_u u)_k = Σ_j φ_j(x_k) u_j
+        for (int a = 0; a < 3; ++a) v += beta[l][a] * u[I[a]];
+        w[Wd[l]] = v * v;
+      }
+    }
+    return 0;
+  }
+  return -3;
+}
+
+// ---------------------------------------------------------------- apply
+// r_i = Σ_{(j,k)} T_ijk u_j w_k, sequential in canonical order.
+void oracle_apply(const void* h, const double* u, const double* w, double* r) {
+  const OTensor* T = static_cast<const OTensor*>(h);
+  for (int64_t i = 0; i < T->V.n_dofs; ++i) {
+    double acc = 0;
+    for (int64_t e = T->t_row_ptr[i]; e < T->t_row_ptr[i + 1]; ++e)
+      acc += T->t_val[e] * u[T->t_j[e]] * w[T->t_k[e]];
+    r[i] = acc;
+  }
+}
+
+// Batched: U, W, R pair-major (U[p*N_u + j], W[p*N_f + k], R[p*N_u + i]).
+void oracle_apply_batched(const void* h, int32_t batch, const double* U, const double* W, double* R) {
+  const OTensor* T = static_cast<const OTensor*>(h);
+  for (int32_t p = 0; p < batch; ++p)
+    oracle_apply(h, U + (int64_t)p * T->V.n_dofs, W + (int64_t)p * T->W.n_dofs, R + (int64_t)p * T->V.n_dofs);
+}
+
+// ---------------------------------------------------------------- jacobian
+// D_u w as a list of (k, m, value) entries (pointwise Jacobian of the
+// interpolated nonlinearity, "defined point-wise").
+struct DEntry { int64_t k; int32_t m; double v; };
+
+static int build_Duw(const OTensor* T, int kind, double p, const double* u, std::vector<DEntry>& D) {
+  const int d = T->dim;
+  if (kind == OK_IDENTITY) {
+    for (int64_t k = 0; k < T->W.n_dofs; ++k) D.push_back({k, (int32_t)k, 1.0});
+    return 0;
+  }
+  if (kind == OK_SQUARE) {
+    for (int64_t k = 0; k < T->W.n_dofs; ++k) D.push_back({k, (int32_t)k, 2.0 * u[k]});
+    return 0;
+  }
+  if (kind == OK_GRADPOW_P0) {
+    // w_K = |g|^{p-2}, g = Σ_a u_a ∇λ_a  ⇒  ∂w_K/∂u_a = (p-2)|g|^{p-4} (g·∇λ_a);
+    // at g = 0 the value 0 is used (reading C11).
+    for (int64_t K = 0; K < T->n_cells; ++K) {
+      Geo g = geometry(*T, K);
+      const int32_t* I = &T->V.cell_dofs[K * T->V.n_loc];
+      double gu[3] = {0, 0, 0};
+      for (int a = 0; a <= d; ++a)
+        for (int x = 0; x < d; ++x) gu[x] += u[I[a]] * g.grad[a][x];
+      double gg = 0;
+      for (int x = 0; x < d; ++x) gg += gu[x] * gu[x];
+      double fac = (gg == 0.0) ? 0.0 : (p - 2.0) * std::pow(std::sqrt(gg), p - 4.0);
+      for (int a = 0; a <= d; ++a) {
+        double gdot = 0;
+        for (int x = 0; x < d; ++x) gdot += gu[x] * g.grad[a][x];
+        D.push_back({(int64_t)T->W.cell_dofs[K], I[a], fac * gdot});
+      }
+    }
+    return 0;
+  }
+  if (kind == OK_P1_TO_P2_SQUARE) {
+    // w = (Π u)⊙(Π u) ⇒ D = diag(2 Π u) Π; only the nonzero entries of Π.
+    const double beta[6][3] = {{1, 0, 0}, {0, 1, 0}, {0, 0, 1}, {0.5, 0.5, 0}, {0, 0.5, 0.5}, {0.5, 0, 0.5}};
+    std::map<std::pair<int64_t, int32_t>, double> Dm;
+    for (int64_t K = 0; K < T->n_cells; ++K) {
+      const int32_t* I = &T->V.cell_dofs[K * 3];
+      const int32_t* Wd = &T->W.cell_dofs[K * 6];
+      for (int l = 0; l < 6; ++l) {
+        double v = 0;
+        for (int a = 0; a < 3; ++a) v += beta[l][a] * u[I[a]];
+        for (int a = 0; a < 3; ++a)
+          if (beta[l][a] != 0.0) Dm[{(int64_t)Wd[l], I[a]}] = 2.0 * v * beta[l][a];
+      }
+    }
+    for (auto& kv : Dm) D.push_back({kv.first.first, kv.first.second, kv.second});
+    return 0;
+  }
+  return -1;
+}
+
+// csr_vals = T·w                                    (PICARD)
+// csr_vals = T·w + (T·₂u)·D_u w                     (NEWTON)
+int oracle_jacobian(const void* h, int mode, int kind, double p, const double* u, const double* w,
+                    double* vals) {
+  const OTensor* T = static_cast<const OTensor*>(h);
+  std::fill(vals, vals + T->csr_col.size(), 0.0);
+  for (int64_t i = 0; i < T->V.n_dofs; ++i)
+    for (int64_t e = T->t_row_ptr[i]; e < T->t_row_ptr[i + 1]; ++e) {
+      int64_t s = csr_find(T, i, T->t_j[e]);
+      if (s < 0) return -3;
+      vals[s] += T->t_val[e] * w[T->t_k[e]];
+    }
+  if (mode == OJ_PICARD) return 0;
+  std::vector<DEntry> D;
+  int rc = build_Duw(T, kind, p, u, D);
+  if (rc) return rc;
+  // index D by k (stable: entries of one k keep insertion order)
+  std::vector<int64_t> dptr(T->W.n_dofs + 1, 0);
+  for (auto& de : D) dptr[de.k + 1]++;
+  for (int64_t k = 0; k < T->W.n_dofs; ++k) dptr[k + 1] += dptr[k];
+  std::vector<DEntry> Ds(D.size());
+  {
+    std::vector<int64_t> fill(dptr.begin(), dptr.end() - 1);
+    for (auto& de : D) Ds[fill[de.k]++] = de;
+  }
+  for (int64_t i = 0; i < T->V.n_dofs; ++i) {
+    // B_{i,k} = (T ·₂ u)_{ik} = Σ_j T_ijk u_j
+    std::map<int64_t, double> B;
+    for (int64_t e = T->t_row_ptr[i]; e < T->t_row_ptr[i + 1]; ++e)
+      B[T->t_k[e]] += T->t_val[e] * u[T->t_j[e]];
+    for (auto& kv : B)
+      for (int64_t q = dptr[kv.first]; q < dptr[kv.first + 1]; ++q) {
+        int64_t s = csr_find(T, i, Ds[q].m);
+        if (s < 0) return -6;
+        vals[s] += kv.second * Ds[q].v;
+      }
+  }
+  return 0;
+}
+
+}  // extern "C"
