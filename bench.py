@@ -1,0 +1,411 @@
+#!/usr/bin/env python
+"""EGFEM hot-path benchmark (BASELINE.json metric: tensor nonzeros/s and achieved HBM GB/s).
+
+One step = one pass of the whole hot path (SURVEY §8(a) A1–A3) over the workload:
+  (1) egfem_interp           w_K = |∇u_h|_K^{p−2} and D_u w       (GRADPOW_P0)
+  (2)+(3) egfem_apply_jacobian  r = T:(u⊗w) and the Newton J = T·w + (T·₂u)·D_u w, fused
+          into one pass over T (both outputs from a single stream of T's nonzeros).
+Default workload: BASELINE configs[3] (3D p-Laplace p=3, 128³×6 tets, 201,326,592 nnz,
+fp64) — the config the north star's headline target is quoted on ("≥70% of HBM at 1 GPU,
+≥6× at 8 GPUs on the largest config"); it fits one B200.  Units: each step processes
+2·nnz tensor nonzeros (apply + Jacobian, reading C25).
+
+N>1 (torchrun): T's rows are partitioned (egfem_partition), each step adds the NCCL u-halo
+exchange; value = all ranks' nonzeros / max-over-ranks device time ("scaling": "strong").
+
+--impl reference: the CPU oracle (oracle/, test infrastructure) on a bounded row sample of
+the same workload, timed on the host cores (rank 0 only).
+"""
+import argparse
+import json
+import os
+import sys
+import threading
+import time
+
+ROOT = os.path.dirname(os.path.abspath(__file__))
+sys.path.insert(0, ROOT)
+
+import numpy as np  # noqa: E402
+
+import egfem_inputs as I  # noqa: E402
+
+ORACLE_SAMPLE_ROWS = 200_000
+
+
+def _peaks():
+    try:
+        with open(os.path.join(ROOT, "MEASURED_PEAKS.json")) as f:
+            d = json.load(f)
+        return float(d["hbm_gbs"]), "measured"
+    except Exception:
+        return 6650.0, "fallback"
+
+
+def _traffic(workload, kernel):
+    """Per-launch DRAM bytes from the committed ncu --set full summary, if any."""
+    p = os.path.join(ROOT, "profiles", "traffic.json")
+    try:
+        with open(p) as f:
+            return json.load(f).get(workload, {}).get(kernel)
+    except Exception:
+        return None
+
+
+class ClockSampler:
+    """Samples SM clock + throttle reasons with NVML every ~2 ms during the timed region."""
+
+    def __init__(self, index):
+        self.samples, self.reasons, self.max_mhz = [], set(), None
+        self._stop = threading.Event()
+        try:
+            import pynvml
+            pynvml.nvmlInit()
+            self.nv = pynvml
+            self.h = pynvml.nvmlDeviceGetHandleByIndex(index)
+            self.max_mhz = pynvml.nvmlDeviceGetMaxClockInfo(self.h, pynvml.NVML_CLOCK_SM)
+        except Exception:
+            self.nv = None
+
+    def _sample(self):
+        nv = self.nv
+        self.samples.append(nv.nvmlDeviceGetClockInfo(self.h, nv.NVML_CLOCK_SM))
+        r = nv.nvmlDeviceGetCurrentClocksEventReasons(self.h)
+        names = {"hw_slowdown": 0x8, "hw_thermal_slowdown": 0x40, "sw_thermal_slowdown": 0x20,
+                 "sw_power_cap": 0x4, "hw_power_brake_slowdown": 0x80}
+        for k, bit in names.items():
+            if r & bit:
+                self.reasons.add(k)
+
+    def _run(self):
+        while not self._stop.is_set():
+            try:
+                self._sample()
+            except Exception:
+                return
+            time.sleep(0.002)
+
+    def __enter__(self):
+        if self.nv:
+            self._sample()
+            self.t = threading.Thread(target=self._run, daemon=True)
+            self.t.start()
+        return self
+
+    def __exit__(self, *a):
+        if self.nv:
+            self._stop.set()
+            self.t.join()
+            self._sample()
+
+    def summary(self):
+        if not self.samples:
+            return {"sm_mhz": None, "sm_max_mhz": self.max_mhz, "reasons": ["nvml unavailable"]}
+        return {"sm_mhz": float(np.median(self.samples)), "sm_max_mhz": self.max_mhz,
+                "reasons": sorted(self.reasons), "samples": len(self.samples)}
+
+
+def algorithmic_bytes(t, pr, s, kind):
+    """Minimal DRAM bytes of one launch in the CSF layout (DESIGN.md §5/§7).
+
+    per nonzero: k (4) + value (s); per fiber: column (4) + offset (4); per row: offset (8);
+    vectors read/written once.  kind: 'apply' | 'jac' (Newton) | 'fused' | 'interp'."""
+    d1 = pr.mesh.dim + 1
+    T = t.nnz * (4 + s) + t.nnz_csr * 8 + (t.n_u + 1) * 8
+    if kind == "apply":
+        return T + s * (2 * t.n_u + t.n_f)
+    if kind == "jac":
+        return T + s * (t.n_u + t.n_f + d1 * t.n_f) + s * t.nnz_csr
+    if kind == "fused":
+        return T + s * (2 * t.n_u + t.n_f + d1 * t.n_f) + s * t.nnz_csr
+    if kind == "interp":  # cells (int32) + w + chain written + u and coords read
+        return pr.mesh.n_cells * (4 * d1 + s * (1 + d1)) + t.n_u * (s + 8 * pr.mesh.dim)
+    raise ValueError(kind)
+
+
+def run_ours(args):
+    import torch
+    import torch.distributed as dist
+
+    import paper_2005_06193_b200 as eg
+    world = int(os.environ.get("WORLD_SIZE", "1"))
+    rank = int(os.environ.get("RANK", "0"))
+    local = int(os.environ.get("LOCAL_RANK", "0"))
+    torch.cuda.set_device(local)
+    dev = torch.device("cuda", local)
+    if world > 1:
+        dist.init_process_group("nccl", device_id=dev)
+    pr = I.make_problem(args.config, batch=args.batch)
+    dtype = eg.F64 if args.dtype == "f64" else eg.F32
+    td = torch.float64 if dtype == eg.F64 else torch.float32
+    s = 8 if dtype == eg.F64 else 4
+    t0 = time.time()
+    tg = eg.egfem_tensor_build(pr.mesh, pr.V, pr.W, pr.form, dtype=dtype, device=local)
+    torch.cuda.synchronize()
+    build_s = time.time() - t0
+    nnz_total = tg.nnz
+    plan = None
+    if world > 1:
+        from paper_2005_06193_b200 import dist as edist
+        t, win = eg.egfem_partition(tg, world, rank, local)
+        del tg
+        torch.cuda.empty_cache()
+        W = edist.Window(win["row_begin"], win["row_end"], win["col_begin"], win["col_end"])
+        plan = edist.make_plan(edist.gather_windows(W), rank)
+        u_np = pr.u[win["col_begin"]:win["col_end"]]
+        u_own = np.zeros_like(u_np)
+        o = plan.owned_offset
+        u_own[o:o + win["row_end"] - win["row_begin"]] = u_np[o:o + win["row_end"] - win["row_begin"]]
+        u_np = u_own  # halos arrive through the exchange
+    else:
+        t = tg
+        u_np = pr.u if not pr.batch else pr.u[0]
+    batched = args.config == "cfg5"
+    if batched:
+        return run_batched(args, eg, t, pr, dev, td, s, build_s, world, rank)
+    u = torch.tensor(u_np, dtype=td, device=dev)
+    w = torch.empty(t.n_f, dtype=td, device=dev)
+    gp = pr.interp == I.INTERP_GRADPOW_P0
+    chain = torch.empty(t.n_f * (pr.mesh.dim + 1), dtype=td, device=dev) if gp else None
+    r = torch.empty(t.n_u, dtype=td, device=dev)
+    J = torch.empty(t.nnz_csr, dtype=td, device=dev)
+    stream = torch.cuda.current_stream(dev)
+
+    def exchange():
+        if plan is not None:
+            edist.halo_exchange(plan, u)
+
+    if plan is not None:
+        from paper_2005_06193_b200 import dist as edist
+
+    K, Wm = args.steps, args.warmup
+    ev = [[torch.cuda.Event(enable_timing=True) for _ in range(4)] for _ in range(K)]
+
+    def step(e=None):
+        if e:
+            e[0].record(stream)
+        exchange()
+        if e:
+            e[1].record(stream)
+        eg.egfem_interp(t, pr.interp, pr.p, u, w, chain, stream)
+        if e:
+            e[2].record(stream)
+        eg.egfem_apply_jacobian(t, eg.JAC_NEWTON, pr.interp, pr.p, u, w, chain, r, J, stream)
+        if e:
+            e[3].record(stream)
+
+    for _ in range(Wm):
+        step()
+    torch.cuda.synchronize()
+    if world > 1:
+        dist.barrier()
+    torch.cuda.synchronize()
+    l0 = eg.launch_count()
+    with ClockSampler(local) as clk:
+        start, stop = torch.cuda.Event(enable_timing=True), torch.cuda.Event(enable_timing=True)
+        start.record(stream)
+        for k in range(K):
+            step(ev[k])
+        stop.record(stream)
+        torch.cuda.synchronize()
+    if world > 1:
+        dist.barrier()
+    torch.cuda.synchronize()
+    launches = eg.launch_count() - l0
+    ms = start.elapsed_time(stop)
+    t_ex = np.mean([e[0].elapsed_time(e[1]) for e in ev])
+    t_interp = np.mean([e[1].elapsed_time(e[2]) for e in ev])
+    t_fused = np.mean([e[2].elapsed_time(e[3]) for e in ev])
+    if world > 1:
+        m = torch.tensor([ms], dtype=torch.float64, device=dev)
+        dist.all_reduce(m, op=dist.ReduceOp.MAX)
+        ms = float(m.item())
+    units = 2 * nnz_total * K
+    value = units / (ms * 1e-3)
+
+    # separate apply / Jacobian launches (explanatory, outside the headline region)
+    def avg_ms(fn, n=max(5, min(K, 50))):
+        a, b = torch.cuda.Event(enable_timing=True), torch.cuda.Event(enable_timing=True)
+        fn()
+        torch.cuda.synchronize()
+        a.record(stream)
+        for _ in range(n):
+            fn()
+        b.record(stream)
+        torch.cuda.synchronize()
+        return a.elapsed_time(b) / n
+    t_apply = avg_ms(lambda: eg.egfem_apply(t, u, w, r, stream))
+    t_jac = avg_ms(lambda: eg.egfem_jacobian(t, eg.JAC_NEWTON, pr.interp, pr.p, u, w, chain, J, stream))
+    t_pic = avg_ms(lambda: eg.egfem_jacobian(t, eg.JAC_PICARD, pr.interp, pr.p, None, w, None, J, stream))
+
+    # end to end: pinned host u → device, the step, device r → pinned host, every step
+    u_host = torch.tensor(u_np, dtype=td).pin_memory()
+    r_host = torch.empty(t.n_u, dtype=td).pin_memory()
+    torch.cuda.synchronize()
+    if world > 1:
+        dist.barrier()
+    a, b = torch.cuda.Event(enable_timing=True), torch.cuda.Event(enable_timing=True)
+    a.record(stream)
+    for _ in range(K):
+        u.copy_(u_host, non_blocking=True)
+        step()
+        r_host.copy_(r, non_blocking=True)
+    b.record(stream)
+    torch.cuda.synchronize()
+    e2e_ms = a.elapsed_time(b)
+    if world > 1:
+        m = torch.tensor([e2e_ms], dtype=torch.float64, device=dev)
+        dist.all_reduce(m, op=dist.ReduceOp.MAX)
+        e2e_ms = float(m.item())
+
+    peak, peak_kind = _peaks()
+    fused_bytes = algorithmic_bytes(t, pr, s, "fused")
+    achieved = fused_bytes / (t_fused * 1e-3) / 1e9
+    workload = f"{args.config}-{args.dtype}"
+    out = {
+        "metric": "tensor nonzeros/s (apply + Newton Jacobian, 2 x nnz per step) and achieved HBM GB/s",
+        "value": value, "unit": "nnz/s", "n_gpus": world, "steps": K, "warmup": Wm,
+        "ms_per_step": ms / K, "higher_is_better": True, "scaling": "strong" if world > 1 else "weak",
+        "vs_baseline": None, "dtype": args.dtype, "data": "synthetic (seeded, BASELINE.json recipe)",
+        "config": {"workload": workload, "description": pr.description, "nnz": nnz_total,
+                   "nnz_csr": t.nnz_csr if world == 1 else None, "n_u": pr.n_u, "n_f": pr.n_f,
+                   "step": "interp(GRADPOW_P0 + D_u w) + fused apply/Newton-Jacobian" +
+                           (" + NCCL u-halo" if world > 1 else ""),
+                   "l2": "inputs larger than L2 (T stream 2.7 GB > 126 MB L2); no flush",
+                   "parallelism": f"row-partition x{world}" if world > 1 else "single GPU"},
+        "roofline": {"bound": "hbm", "kernel": "k_tile<double,DO_R,NewtonP0> (egfem_apply_jacobian)",
+                     "achieved": achieved, "peak": peak, "peak_kind": peak_kind, "unit": "GB/s",
+                     "frac": achieved / peak, "algorithmic_bytes": fused_bytes,
+                     "traffic": _traffic(workload, "fused")},
+        "kernels_ms": {"halo_exchange": t_ex, "interp": t_interp, "apply_jacobian_fused": t_fused,
+                       "apply": t_apply, "jacobian_newton": t_jac, "jacobian_picard": t_pic},
+        "kernels_gbs": {"interp": algorithmic_bytes(t, pr, s, "interp") / (t_interp * 1e-3) / 1e9,
+                        "apply": algorithmic_bytes(t, pr, s, "apply") / (t_apply * 1e-3) / 1e9,
+                        "jacobian_newton": algorithmic_bytes(t, pr, s, "jac") / (t_jac * 1e-3) / 1e9,
+                        "apply_nnz_per_s": t.nnz / (t_apply * 1e-3)},
+        "e2e": {"value": units / (e2e_ms * 1e-3), "unit": "nnz/s", "h2d_bytes_per_step": u.numel() * s,
+                "d2h_bytes_per_step": r.numel() * s},
+        "gpu_launches": int(launches),
+        "clocks": clk.summary(),
+        "build_s": build_s,
+    }
+    if plan is not None:
+        out["config"]["halo_values_per_rank"] = plan.halo_values
+    if rank == 0 and world == 1 and not args.no_cpu_baseline:
+        out["cpu_baseline"] = cpu_baseline(pr)
+    if rank == 0:
+        print(json.dumps(out), flush=True)
+    if world > 1:
+        dist.destroy_process_group()
+
+
+def run_batched(args, eg, t, pr, dev, td, s, build_s, world, rank):
+    """cfg5: batched action, B pairs sharded across ranks (T replicated, no communication)."""
+    import torch
+    import torch.distributed as dist
+    B = pr.batch
+    lo, hi = rank * B // world, (rank + 1) * B // world
+    Bl = hi - lo
+    U = torch.tensor(np.ascontiguousarray(pr.u[lo:hi].T), dtype=td, device=dev)  # node-major
+    R = torch.empty_like(U)
+    stream = torch.cuda.current_stream(dev)
+    for _ in range(args.warmup):
+        eg.egfem_apply_batched(t, Bl, eg.LAYOUT_NODE_MAJOR, U, U, R, stream)
+    torch.cuda.synchronize()
+    if world > 1:
+        dist.barrier()
+    l0 = eg.launch_count()
+    with ClockSampler(dev.index) as clk:
+        a, b = torch.cuda.Event(enable_timing=True), torch.cuda.Event(enable_timing=True)
+        a.record(stream)
+        for _ in range(args.steps):
+            eg.egfem_apply_batched(t, Bl, eg.LAYOUT_NODE_MAJOR, U, U, R, stream)
+        b.record(stream)
+        torch.cuda.synchronize()
+    ms = a.elapsed_time(b)
+    if world > 1:
+        m = torch.tensor([ms], dtype=torch.float64, device=dev)
+        dist.all_reduce(m, op=dist.ReduceOp.MAX)
+        ms = float(m.item())
+    units = t.nnz * B * args.steps
+    byts = t.nnz * (4 + s) + t.nnz_csr * 8 + (t.n_u + 1) * 8 + s * (2 * t.n_u * Bl + t.n_f * Bl)
+    per = ms / args.steps
+    peak, kind = _peaks()
+    out = {"metric": "tensor nonzero-pairs/s (batched action) and achieved HBM GB/s", "value": units / (ms * 1e-3),
+           "unit": "nnz*pair/s", "n_gpus": world, "steps": args.steps, "warmup": args.warmup,
+           "ms_per_step": per, "higher_is_better": True, "scaling": "weak", "vs_baseline": None,
+           "dtype": args.dtype, "data": "synthetic (seeded, BASELINE.json recipe)",
+           "config": {"workload": f"cfg5-{args.dtype}", "batch": B, "nnz": t.nnz, "parallelism": f"batch-shard x{world}"},
+           "roofline": {"bound": "hbm", "achieved": byts / (per * 1e-3) / 1e9, "peak": peak, "peak_kind": kind,
+                        "unit": "GB/s", "frac": byts / (per * 1e-3) / 1e9 / peak, "traffic": None},
+           "gpu_launches": int(eg.launch_count() - l0), "clocks": clk.summary(), "build_s": build_s}
+    if rank == 0:
+        print(json.dumps(out), flush=True)
+
+
+def cpu_baseline(pr, rows=ORACLE_SAMPLE_ROWS, steps=1):
+    """The CPU oracle as it stands (single thread) on rows [0, rows) of the same workload."""
+    import oracle
+    o = oracle.OracleTensor(pr.mesh, pr.V, pr.W, pr.form, rows=(0, rows))
+    t0 = time.time()
+    for _ in range(steps):
+        w = o.interp(pr.interp, pr.p, pr.u)
+        o.apply(pr.u, w)
+        o.jacobian(1, pr.interp, pr.p, pr.u, w)
+    dt = (time.time() - t0) / steps
+    return {"value": 2 * o.nnz / dt, "unit": "nnz/s", "cores": 1, "kind": "oracle",
+            "sample": f"{pr.name} rows [0,{rows}) = {o.nnz} nnz; interp over all {pr.mesh.n_cells} cells "
+                      f"+ apply + Newton Jacobian, {steps} step(s), {dt:.2f} s/step"}
+
+
+def run_reference(args):
+    rank = int(os.environ.get("RANK", "0"))
+    if rank != 0:
+        return
+    pr = I.make_problem(args.config, batch=min(args.batch or 256, 256))
+    if args.config == "cfg5":
+        print(json.dumps({"impl": "reference", "unavailable": "reference arm implemented for cfg1-cfg4"}))
+        return
+    import oracle
+    rows = min(ORACLE_SAMPLE_ROWS, pr.n_u)
+    o = oracle.OracleTensor(pr.mesh, pr.V, pr.W, pr.form, rows=(0, rows))
+    for _ in range(args.warmup if args.warmup <= 1 else 1):
+        w = o.interp(pr.interp, pr.p, pr.u)
+        o.apply(pr.u, w)
+    t0 = time.time()
+    for _ in range(args.steps):
+        w = o.interp(pr.interp, pr.p, pr.u)
+        o.apply(pr.u, w)
+        o.jacobian(1, pr.interp, pr.p, pr.u, w)
+    dt = time.time() - t0
+    value = 2 * o.nnz * args.steps / dt
+    sample = f"{pr.name} rows [0,{rows}) = {o.nnz} nnz per step (interp over all cells + apply + Newton Jacobian)"
+    print(json.dumps({"impl": "reference", "metric": "tensor nonzeros/s (apply + Newton Jacobian, 2 x nnz per step) "
+                      "and achieved HBM GB/s", "value": value, "unit": "nnz/s", "n_gpus": 1, "steps": args.steps,
+                      "warmup": args.warmup, "ms_per_step": dt * 1e3 / args.steps, "higher_is_better": True,
+                      "scaling": "weak", "vs_baseline": None, "dtype": "f64", "data": "synthetic",
+                      "config": {"workload": f"{args.config}-f64"},
+                      "cpu_baseline": {"value": value, "unit": "nnz/s", "cores": 1, "kind": "oracle", "sample": sample},
+                      "e2e": {"value": value, "unit": "nnz/s", "h2d_bytes_per_step": 0, "d2h_bytes_per_step": 0}}),
+          flush=True)
+
+
+def main():
+    ap = argparse.ArgumentParser()
+    ap.add_argument("--gpus", type=int, default=1)
+    ap.add_argument("--steps", type=int, default=50)
+    ap.add_argument("--warmup", type=int, default=5)
+    ap.add_argument("--impl", default="ours", choices=["ours", "reference"])
+    ap.add_argument("--config", default="cfg4", choices=list(I.CONFIG_NAMES))
+    ap.add_argument("--dtype", default="f64", choices=["f64", "f32"])
+    ap.add_argument("--batch", type=int, default=None)
+    ap.add_argument("--no-cpu-baseline", action="store_true")
+    args = ap.parse_args()
+    if args.impl == "reference":
+        run_reference(args)
+    else:
+        run_ours(args)
+
+
+if __name__ == "__main__":
+    main()

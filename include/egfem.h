@@ -1,0 +1,242 @@
+/*
+ * egfem.h — C ABI of libegfem.so, the B200 (sm_100a) hot path of the extended
+ * group finite element method (EGFEM, Tolle & Marheineke, arXiv 2005.06193).
+ *
+ * The method replaces each nonlinear coefficient f(u, ∇u) by its interpolant on a
+ * space W_h tailored to the nonlinearity (§3.1, eq. (egfem_coeffs)),
+ * which turns the nonlinear residual into trilinear forms held as assembled sparse
+ * third-order tensors T_ijk (eq. (egfem_terms)).  Each Picard or
+ * Newton iteration then needs only
+ *   (1) w = f(Π_u u, Π_∇u ·₂ u)                       egfem_interp
+ *   (2) r_i = (T:(u⊗w))_i = Σ_jk T_ijk u_j w_k        egfem_apply
+ *   (3) A = T·w, or J = T·w + (T·₂u)·D_u w             egfem_jacobian
+ * on a tensor precomputed once                         egfem_tensor_build ("offline").
+ *
+ * Conventions for every function:
+ *   - Every function returns egfem_status; none throws, aborts or exits.
+ *   - Validation (null / misaligned pointers, wrong device, bad enum, size or index
+ *     overflow) happens synchronously BEFORE any launch; on a validation error no
+ *     output is written.  egfem_last_error() returns a thread-local detail string.
+ *   - Mesh / space / quadrature arrays passed to egfem_tensor_build are HOST
+ *     pointers, copied during the call; the caller may free them afterwards.
+ *   - u, w, r, chain, csr_vals, U, W, R are caller-owned DEVICE pointers on the
+ *     handle's device, of the handle's dtype, 16-byte aligned, contiguous.
+ *     Lengths are implied by egfem_tensor_info (N_u, N_f, nnz_csr).
+ *   - Compute calls are asynchronous on the given cudaStream_t (0 = legacy default).
+ *     Kernel faults surface at the next call or at the caller's stream sync.
+ *   - The handle is immutable after build; interp/apply/jacobian are pure functions
+ *     of their inputs and may run concurrently on different streams.
+ *   - No floating-point atomics: results are bitwise reproducible run to run.
+ *   - csr_vals is fully overwritten, never accumulated into.
+ */
+#ifndef EGFEM_H
+#define EGFEM_H
+
+#include <stdint.h>
+
+#ifdef __cplusplus
+extern "C" {
+#endif
+
+typedef struct CUstream_st* egfem_stream_t; /* == cudaStream_t */
+
+typedef enum {
+  EGFEM_OK = 0,
+  EGFEM_ERR_INVALID_ARGUMENT = 1,
+  EGFEM_ERR_DIMENSION_MISMATCH = 2,
+  EGFEM_ERR_UNSUPPORTED = 3,
+  EGFEM_ERR_INDEX_OVERFLOW = 4,
+  EGFEM_ERR_OUT_OF_MEMORY = 5,
+  EGFEM_ERR_CUDA = 6,
+  EGFEM_ERR_NCCL = 7
+} egfem_status;
+
+typedef enum { EGFEM_F64 = 0, EGFEM_F32 = 1 } egfem_dtype;
+
+/* Lagrange families (P0 for gradient nonlinearities L584). */
+typedef enum { EGFEM_P0 = 0, EGFEM_P1 = 1, EGFEM_P2 = 2 } egfem_family;
+
+/* Trilinear forms, slot order (i = test, j = u-slot, k = w-slot):
+ *   CONV_K : ∫ φ_i φ_j ∂x φ_k                 (BASELINE cfg1, 1D Burgers)
+ *   CONV_J : ∫ φ_i (∂x+∂y)φ_j φ_k             (BASELINE cfg2/cfg5, 2D Burgers)
+ *   PLAP   : ∫ ψ_k ∇φ_i·∇φ_j                  (K_a of PAPER.md L253, §5.5 p-Laplace)
+ *   MASS3  : ∫ φ_i φ_j η_k                     (M of PAPER.md L327 / M_c̃ of L478)
+ *   CONV_I : ∫ (∂x+∂y)φ_i φ_j φ_k             (N of PAPER.md L400)
+ * (∂x+∂y) sums the first min(d,2) partial derivatives. */
+typedef enum {
+  EGFEM_FORM_CONV_K = 0,
+  EGFEM_FORM_CONV_J = 1,
+  EGFEM_FORM_PLAP = 2,
+  EGFEM_FORM_MASS3 = 3,
+  EGFEM_FORM_CONV_I = 4
+} egfem_form;
+
+/* Pointwise nonlinearities at the W-DOFs:
+ *   IDENTITY        : w = u                     (W = V, GFEM, Π_u = I, L338)
+ *   SQUARE          : w_k = u_k²                (W = V, L336 with Π = I)
+ *   GRADPOW_P0      : w_K = ‖∇u_h|_K‖^{p−2}     (V = P1, W = P0, L574/L582)
+ *   P1_TO_P2_SQUARE : w = (Π_u u) ⊙ (Π_u u)     (V = P1, W = P2, Case 1, L336–338) */
+typedef enum {
+  EGFEM_INTERP_IDENTITY = 0,
+  EGFEM_INTERP_SQUARE = 1,
+  EGFEM_INTERP_GRADPOW_P0 = 2,
+  EGFEM_INTERP_P1_TO_P2_SQUARE = 3
+} egfem_interp_kind;
+
+/* PICARD: A = T·w.  NEWTON: J = T·w + (T·₂u)·D_u w, the Schur
+ * complement of the block Jacobian D_zF̃ of PAPER.md L290 (reading C10). */
+typedef enum { EGFEM_JAC_PICARD = 0, EGFEM_JAC_NEWTON = 1 } egfem_jac_mode;
+
+/* Batched vector layouts: NODE_MAJOR U[i*B + p]; PAIR_MAJOR U[p*N + i]. */
+typedef enum { EGFEM_LAYOUT_NODE_MAJOR = 0, EGFEM_LAYOUT_PAIR_MAJOR = 1 } egfem_layout;
+
+/* Simplicial mesh Ω_h: host arrays. */
+typedef struct {
+  int32_t dim;            /* 1, 2 or 3 */
+  int64_t n_vertices;
+  const double* coords;   /* host, n_vertices*dim, row-major */
+  int64_t n_cells;
+  const int32_t* cells;   /* host, n_cells*(dim+1) vertex ids */
+} egfem_mesh;
+
+/* A DOF numbering of a Lagrange space on the mesh.  cell_dofs == NULL means the
+ * canonical numbering: P0 -> cell id, P1 -> vertex id (mesh cells).  P2 (2D only)
+ * needs an explicit table with local order (v0, v1, v2, m01, m12, m20). */
+typedef struct {
+  egfem_family family;
+  int64_t n_dofs;
+  const int32_t* cell_dofs; /* host, n_cells*n_local, or NULL (P0/P1 canonical) */
+} egfem_space;
+
+/* Quadrature rule in barycentric coordinates, weights summing to 1 (the |K|
+ * factor is applied at assembly).  NULL = form default:
+ * 1D 3-point Gauss; 2D centroid / 3-point degree-2 / 6-point degree-4 chosen by
+ * the integrand's polynomial degree (degree-4 is capped: cfg5's degree-5
+ * integrand is DEFINED by the 6-point rule, reading C3); 3D centroid / 4-point. */
+typedef struct {
+  int32_t n_points;
+  const double* bary;     /* host, n_points*(dim+1) */
+  const double* weights;  /* host, n_points */
+} egfem_quad;
+
+typedef struct egfem_tensor egfem_tensor; /* opaque; owns every device array */
+
+/* ---------------------------------------------------------------- offline build
+ * Assemble T_ijk = Σ_K ∫_K (slot_i φ_i)(slot_j φ_j)(slot_k η_k) over all cells,
+ * keeping every structural triple (numeric zeros included, reading C7), summing
+ * duplicates, in SPEC's canonical lexicographic (i,j,k) order.
+ * The CSR pattern of the Jacobian is the union of element cliques over V-DOFs and
+ * coincides with the (i,j) fibers of T.  Runs on `device`; returns after the
+ * device work is complete.  Errors: INVALID_ARGUMENT (nulls, dim, cell_dofs out of
+ * range), UNSUPPORTED (P2 outside 2D, a row longer than the kernel tile),
+ * INDEX_OVERFLOW (N_f >= 2^28 for P0 W, nnz >= 2^32, n_dofs >= 2^31),
+ * OUT_OF_MEMORY, CUDA.  *out is NULL on error. */
+egfem_status egfem_tensor_build(const egfem_mesh* mesh, const egfem_space* V, const egfem_space* W,
+                                egfem_form form, const egfem_quad* quad, egfem_dtype dtype,
+                                int device, egfem_tensor** out);
+
+/* Build from a user-supplied COO tensor (host arrays, any order, duplicates summed
+ * in the given order).  The CSR pattern is the set of (i,j) fibers.  No mesh is
+ * attached, so only IDENTITY / SQUARE interp and PICARD / IDENTITY- and
+ * SQUARE-NEWTON Jacobians are available (they need W = V: n_f == n_u). */
+egfem_status egfem_tensor_from_coo(int64_t n_u, int64_t n_f, int64_t nnz, const int32_t* i,
+                                   const int32_t* j, const int32_t* k, const double* val,
+                                   egfem_dtype dtype, int device, egfem_tensor** out);
+
+egfem_status egfem_tensor_destroy(egfem_tensor* t);
+
+/* Sizes.  Any output pointer may be NULL. */
+egfem_status egfem_tensor_info(const egfem_tensor* t, int64_t* n_u, int64_t* n_f, int64_t* nnz,
+                               int64_t* nnz_csr, egfem_dtype* dtype);
+
+/* Borrowed device pointers to the CSR pattern (valid for the handle's lifetime):
+ * row_ptr int64[N_u+1], col int32[nnz_csr], columns ascending within a row. */
+egfem_status egfem_tensor_csr_pattern(const egfem_tensor* t, const int64_t** d_row_ptr,
+                                      const int32_t** d_col);
+
+/* Copy the canonical arrays to HOST buffers (NULL = skip):
+ *   t_row_ptr int64[N_u+1], t_j int32[nnz], t_k int32[nnz], t_val (dtype)[nnz],
+ *   csr_row_ptr int64[N_u+1], csr_col int32[nnz_csr],
+ *   slot_ij int32[nnz]  CSR position of (i, t_j[e]),
+ *   slot_ik int32[nnz]  CSR position of (i, t_k[e])  (W = V numbering only, else UNSUPPORTED),
+ *   loc uint8[nnz]      bits 0-1: local index of i in cell t_k[e], bits 2-3: of t_j[e]
+ *                       (P0 W only, else UNSUPPORTED).  Synchronous. */
+egfem_status egfem_tensor_export(const egfem_tensor* t, int64_t* t_row_ptr, int32_t* t_j, int32_t* t_k,
+                                 void* t_val, int64_t* csr_row_ptr, int32_t* csr_col, int32_t* slot_ij,
+                                 int32_t* slot_ik, uint8_t* loc);
+
+/* ---------------------------------------------------------------- per iteration
+ * (1) w = f(Π_u u, Π_∇u ·₂ u) at every W-DOF.
+ * u: device [N_u]; w: device [N_f].  chain (nullable, GRADPOW_P0 only): device
+ * [N_f*(d+1)], chain[K*(d+1)+m] = ∂w_K/∂u_{v_m(K)} (the pointwise D_u w of
+ * PAPER.md L292), consumed by egfem_jacobian NEWTON.  p > 1 required for
+ * GRADPOW_P0 (p ignored otherwise).  At ∇u_h|_K = 0 and p < 4 the derivative is
+ * taken as 0 (reading C11). */
+egfem_status egfem_interp(const egfem_tensor* t, egfem_interp_kind kind, double p, const void* u,
+                          void* w, void* chain, egfem_stream_t stream);
+
+/* (2) r_i = Σ_{(j,k)} T_ijk u_j w_k  (":" with A = u⊗w; L251).
+ * u: [N_u], w: [N_f], r: [N_u], all device. */
+egfem_status egfem_apply(const egfem_tensor* t, const void* u, const void* w, void* r,
+                         egfem_stream_t stream);
+
+/* (2b) the same for `batch` independent (u, w) pairs reusing each T nonzero:
+ * R_p = T:(U_p ⊗ W_p).  Layout NODE_MAJOR: U[j*batch+p], W[k*batch+p], R[i*batch+p];
+ * PAIR_MAJOR: U[p*N_u+j], ... (batch >= 1). */
+egfem_status egfem_apply_batched(const egfem_tensor* t, int32_t batch, egfem_layout layout,
+                                 const void* U, const void* W, void* R, egfem_stream_t stream);
+
+/* (3) Jacobian / Picard matrix values in the CSR pattern:
+ *   PICARD            : A_ij = Σ_k T_ijk w_k
+ *   NEWTON IDENTITY   : J = T·w + T·₂u                (∂w_k/∂u_m = δ_km)
+ *   NEWTON SQUARE     : J = T·w + (T·₂u)·diag(2u)
+ *   NEWTON GRADPOW_P0 : J = T·w + (T·₂u)·D_u w, D_u w from `chain` (egfem_interp)
+ * u: [N_u] (NEWTON), w: [N_f], chain: [N_f*(d+1)] (GRADPOW NEWTON), csr_vals: [nnz_csr].
+ * NEWTON with P1_TO_P2_SQUARE returns UNSUPPORTED. */
+egfem_status egfem_jacobian(const egfem_tensor* t, egfem_jac_mode mode, egfem_interp_kind kind, double p,
+                            const void* u, const void* w, const void* chain, void* csr_vals,
+                            egfem_stream_t stream);
+
+/* Fused (2)+(3): one pass over T produces r and csr_vals (same semantics and
+ * arguments as egfem_apply + egfem_jacobian; results are bitwise identical to the
+ * separate calls). */
+egfem_status egfem_apply_jacobian(const egfem_tensor* t, egfem_jac_mode mode, egfem_interp_kind kind,
+                                  double p, const void* u, const void* w, const void* chain, void* r,
+                                  void* csr_vals, egfem_stream_t stream);
+
+/* ---------------------------------------------------------------- multi-GPU (row partition)
+ * Split the rows of `global` into `nranks` contiguous ranges balanced by nnz and
+ * build rank `rank`'s local tensor on `device`.  The local tensor addresses a
+ * local vector of length n_local = halo_lo + owned + halo_hi laid out as global
+ * indices [col_begin, col_end) (contiguous: the structured lexicographic numbering
+ * makes the referenced columns one range; a non-contiguous range is still
+ * correct, only larger).  Local W (P0) covers cells [w_begin, w_end) referenced by
+ * the owned rows.  Outputs (host scalars, any may be NULL): row_begin/row_end
+ * (owned global rows), col_begin/col_end (local u window), w_begin/w_end. */
+egfem_status egfem_partition(const egfem_tensor* global, int32_t nranks, int32_t rank, int device,
+                             egfem_tensor** local, int64_t* row_begin, int64_t* row_end,
+                             int64_t* col_begin, int64_t* col_end, int64_t* w_begin, int64_t* w_end);
+
+/* Pure host helper behind egfem_partition: nnz-balanced contiguous row split.
+ * row_nnz_prefix: host int64[n_rows+1] (t_row_ptr); out_bounds: host int64[nranks+1]. */
+egfem_status egfem_partition_rows(int64_t n_rows, const int64_t* row_nnz_prefix, int32_t nranks,
+                                  int64_t* out_bounds);
+
+/* Halo gather/scatter for non-contiguous exchanges: send_buf[q] = u_local[idx[q]],
+ * u_local[idx[q]] = recv_buf[q] (device arrays, n entries, handle's dtype). */
+egfem_status egfem_halo_pack(const egfem_tensor* local, const int32_t* d_idx, int64_t n,
+                             const void* u_local, void* send_buf, egfem_stream_t stream);
+egfem_status egfem_halo_unpack(const egfem_tensor* local, const int32_t* d_idx, int64_t n,
+                               const void* recv_buf, void* u_local, egfem_stream_t stream);
+
+/* Number of CUDA kernels this library launched (process-wide, all threads); used
+ * by bench.py to report gpu_launches. */
+uint64_t egfem_launch_count(void);
+
+const char* egfem_status_string(egfem_status s);
+const char* egfem_last_error(void);
+
+#ifdef __cplusplus
+}
+#endif
+#endif /* EGFEM_H */

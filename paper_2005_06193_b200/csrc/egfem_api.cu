@@ -1,0 +1,589 @@
+// C ABI of libegfem.so: validation, handle lifetime, dispatch, multi-GPU
+// partitioning.  See include/egfem.h for the contract of every entry point.
+#include <algorithm>
+#include <atomic>
+#include <cstring>
+#include <numeric>
+#include <string>
+#include <vector>
+
+#include "egfem_internal.cuh"
+
+namespace egfem {
+
+namespace {
+thread_local std::string g_last_error;
+std::atomic<uint64_t> g_launches{0};
+
+// Switch to the handle's device for the duration of a call.
+struct DeviceGuard {
+  int prev = -1;
+  bool ok = true;
+  explicit DeviceGuard(int dev) {
+    if (cudaGetDevice(&prev) != cudaSuccess) prev = -1;
+    if (prev != dev) ok = cudaSetDevice(dev) == cudaSuccess;
+  }
+  ~DeviceGuard() {
+    int cur = -1;
+    if (prev >= 0 && cudaGetDevice(&cur) == cudaSuccess && cur != prev) cudaSetDevice(prev);
+  }
+};
+
+egfem_status fail(egfem_status s, const std::string& msg) {
+  set_error(msg);
+  return s;
+}
+
+bool aligned16(const void* p) { return (reinterpret_cast<uintptr_t>(p) & 15u) == 0; }
+
+// Caller device pointers must be on the handle's device (or managed).
+egfem_status check_dev_ptr(const egfem_tensor* t, const void* p, const char* name, bool required) {
+  if (!p) return required ? fail(EGFEM_ERR_INVALID_ARGUMENT, std::string(name) + " is NULL") : EGFEM_OK;
+  if (!aligned16(p)) return fail(EGFEM_ERR_INVALID_ARGUMENT, std::string(name) + " is not 16-byte aligned");
+  cudaPointerAttributes a;
+  if (cudaPointerGetAttributes(&a, p) != cudaSuccess) {
+    cudaGetLastError();
+    return fail(EGFEM_ERR_INVALID_ARGUMENT, std::string(name) + " is not a CUDA pointer");
+  }
+  if (a.type == cudaMemoryTypeManaged) return EGFEM_OK;
+  if (a.type != cudaMemoryTypeDevice || a.device != t->device)
+    return fail(EGFEM_ERR_INVALID_ARGUMENT, std::string(name) + " is not device memory on the handle's device");
+  return EGFEM_OK;
+}
+
+egfem_status validate_space(const egfem_mesh* m, const egfem_space* S, const char* name) {
+  if (!S) return fail(EGFEM_ERR_INVALID_ARGUMENT, std::string(name) + " is NULL");
+  if (S->family < EGFEM_P0 || S->family > EGFEM_P2)
+    return fail(EGFEM_ERR_INVALID_ARGUMENT, std::string(name) + ": bad family");
+  if (S->family == EGFEM_P2 && m->dim != 2) return fail(EGFEM_ERR_UNSUPPORTED, "P2 is implemented in 2D only");
+  if (S->family == EGFEM_P2 && !S->cell_dofs) return fail(EGFEM_ERR_INVALID_ARGUMENT, "P2 needs cell_dofs");
+  if (S->n_dofs <= 0 || S->n_dofs >= (int64_t(1) << 31))
+    return fail(S->n_dofs <= 0 ? EGFEM_ERR_INVALID_ARGUMENT : EGFEM_ERR_INDEX_OVERFLOW,
+                std::string(name) + ": n_dofs out of range");
+  const int nl = S->family == EGFEM_P0 ? 1 : (S->family == EGFEM_P1 ? m->dim + 1 : 6);
+  if (S->cell_dofs) {
+    const int64_t n = m->n_cells * nl;
+    for (int64_t q = 0; q < n; ++q)
+      if (S->cell_dofs[q] < 0 || S->cell_dofs[q] >= S->n_dofs)
+        return fail(EGFEM_ERR_INVALID_ARGUMENT, std::string(name) + ": cell_dofs entry out of range");
+  } else {
+    if (S->family == EGFEM_P0 && S->n_dofs != m->n_cells)
+      return fail(EGFEM_ERR_DIMENSION_MISMATCH, std::string(name) + ": canonical P0 needs n_dofs == n_cells");
+    if (S->family == EGFEM_P1 && S->n_dofs != m->n_vertices)
+      return fail(EGFEM_ERR_DIMENSION_MISMATCH, std::string(name) + ": canonical P1 needs n_dofs == n_vertices");
+  }
+  if (S->family == EGFEM_P0) {  // one DOF per cell, each used once
+    if (S->n_dofs != m->n_cells) return fail(EGFEM_ERR_DIMENSION_MISMATCH, "P0 needs n_dofs == n_cells");
+    if (S->cell_dofs) {
+      std::vector<uint8_t> seen(S->n_dofs, 0);
+      for (int64_t c = 0; c < m->n_cells; ++c) {
+        if (seen[S->cell_dofs[c]]) return fail(EGFEM_ERR_INVALID_ARGUMENT, "P0 cell_dofs is not a permutation");
+        seen[S->cell_dofs[c]] = 1;
+      }
+    }
+  }
+  return EGFEM_OK;
+}
+
+}  // namespace
+
+void set_error(const std::string& msg) { g_last_error = msg; }
+void count_launch(int n) { g_launches.fetch_add((uint64_t)n, std::memory_order_relaxed); }
+
+}  // namespace egfem
+
+using namespace egfem;
+
+extern "C" {
+
+const char* egfem_status_string(egfem_status s) {
+  switch (s) {
+    case EGFEM_OK: return "EGFEM_OK";
+    case EGFEM_ERR_INVALID_ARGUMENT: return "EGFEM_ERR_INVALID_ARGUMENT";
+    case EGFEM_ERR_DIMENSION_MISMATCH: return "EGFEM_ERR_DIMENSION_MISMATCH";
+    case EGFEM_ERR_UNSUPPORTED: return "EGFEM_ERR_UNSUPPORTED";
+    case EGFEM_ERR_INDEX_OVERFLOW: return "EGFEM_ERR_INDEX_OVERFLOW";
+    case EGFEM_ERR_OUT_OF_MEMORY: return "EGFEM_ERR_OUT_OF_MEMORY";
+    case EGFEM_ERR_CUDA: return "EGFEM_ERR_CUDA";
+    case EGFEM_ERR_NCCL: return "EGFEM_ERR_NCCL";
+  }
+  return "EGFEM_UNKNOWN";
+}
+
+const char* egfem_last_error(void) { return g_last_error.c_str(); }
+
+uint64_t egfem_launch_count(void) { return g_launches.load(); }
+
+egfem_status egfem_tensor_build(const egfem_mesh* mesh, const egfem_space* V, const egfem_space* W, egfem_form form,
+                                const egfem_quad* quad, egfem_dtype dtype, int device, egfem_tensor** out) {
+  if (!out) return fail(EGFEM_ERR_INVALID_ARGUMENT, "out is NULL");
+  *out = nullptr;
+  if (!mesh || !mesh->coords || !mesh->cells) return fail(EGFEM_ERR_INVALID_ARGUMENT, "mesh arrays are NULL");
+  if (mesh->dim < 1 || mesh->dim > 3) return fail(EGFEM_ERR_INVALID_ARGUMENT, "dim must be 1, 2 or 3");
+  if (mesh->n_cells <= 0 || mesh->n_vertices <= 0) return fail(EGFEM_ERR_INVALID_ARGUMENT, "empty mesh");
+  if (mesh->n_vertices >= (int64_t(1) << 31) || mesh->n_cells >= (int64_t(1) << 31))
+    return fail(EGFEM_ERR_INDEX_OVERFLOW, "mesh larger than int32 indices");
+  if (form < EGFEM_FORM_CONV_K || form > EGFEM_FORM_CONV_I) return fail(EGFEM_ERR_INVALID_ARGUMENT, "bad form");
+  if (dtype != EGFEM_F64 && dtype != EGFEM_F32) return fail(EGFEM_ERR_INVALID_ARGUMENT, "bad dtype");
+  const int64_t ncv = mesh->n_cells * (mesh->dim + 1);
+  for (int64_t q = 0; q < ncv; ++q)
+    if (mesh->cells[q] < 0 || mesh->cells[q] >= mesh->n_vertices)
+      return fail(EGFEM_ERR_INVALID_ARGUMENT, "mesh cell vertex out of range");
+  egfem_status st = validate_space(mesh, V, "V");
+  if (st) return st;
+  if ((st = validate_space(mesh, W, "W"))) return st;
+  if (V->family == EGFEM_P0) return fail(EGFEM_ERR_UNSUPPORTED, "V = P0 has no gradients/test functions here");
+  if (form == EGFEM_FORM_PLAP && W->family == EGFEM_P2)
+    ;  // allowed: quadrature definition
+  if (quad && quad->n_points > 0 && (!quad->bary || !quad->weights))
+    return fail(EGFEM_ERR_INVALID_ARGUMENT, "quadrature arrays are NULL");
+  const int nV = V->family == EGFEM_P1 ? mesh->dim + 1 : 6;
+  const int nW = W->family == EGFEM_P0 ? 1 : (W->family == EGFEM_P1 ? mesh->dim + 1 : 6);
+  if ((int64_t)nV * nV * nW * mesh->n_cells >= (int64_t(1) << 32))
+    return fail(EGFEM_ERR_INDEX_OVERFLOW, "more than 2^32 element triples");
+  int ndev = 0;
+  if (cudaGetDeviceCount(&ndev) != cudaSuccess || device < 0 || device >= ndev) {
+    cudaGetLastError();
+    return fail(EGFEM_ERR_INVALID_ARGUMENT, "no such CUDA device");
+  }
+  DeviceGuard g(device);
+  if (!g.ok) return fail(EGFEM_ERR_CUDA, "cudaSetDevice failed");
+  egfem_tensor* t = new egfem_tensor();
+  t->device = device;
+  t->dtype = dtype;
+  t->form = form;
+  st = upload_mesh(t, mesh, V, W);
+  int64_t m = 0;
+  uint64_t* key = nullptr;
+  uint32_t* k = nullptr;
+  double* val = nullptr;
+  if (!st) st = emit_element_triples(t, form, quad, &m, &key, &k, &val);
+  if (!st) {
+    st = build_from_triples(t, m, key, k, val);  // takes ownership of key/k/val
+  } else {
+    if (key) cudaFree(key);
+    if (k) cudaFree(k);
+    if (val) cudaFree(val);
+  }
+  if (st) {
+    free_tensor(t);
+    delete t;
+    return st;
+  }
+  *out = t;
+  return EGFEM_OK;
+}
+
+egfem_status egfem_tensor_from_coo(int64_t n_u, int64_t n_f, int64_t nnz, const int32_t* i, const int32_t* j,
+                                   const int32_t* k, const double* val, egfem_dtype dtype, int device,
+                                   egfem_tensor** out) {
+  if (!out) return fail(EGFEM_ERR_INVALID_ARGUMENT, "out is NULL");
+  *out = nullptr;
+  if (n_u <= 0 || n_f <= 0 || nnz < 0) return fail(EGFEM_ERR_INVALID_ARGUMENT, "bad sizes");
+  if (n_u >= (int64_t(1) << 31) || n_f >= (int64_t(1) << 31) || nnz >= (int64_t(1) << 32))
+    return fail(EGFEM_ERR_INDEX_OVERFLOW, "sizes exceed index widths");
+  if (nnz > 0 && (!i || !j || !k || !val)) return fail(EGFEM_ERR_INVALID_ARGUMENT, "COO arrays are NULL");
+  if (dtype != EGFEM_F64 && dtype != EGFEM_F32) return fail(EGFEM_ERR_INVALID_ARGUMENT, "bad dtype");
+  std::vector<uint64_t> key(nnz);
+  std::vector<uint32_t> kk(nnz);
+  for (int64_t e = 0; e < nnz; ++e) {
+    if (i[e] < 0 || i[e] >= n_u || j[e] < 0 || j[e] >= n_u || k[e] < 0 || k[e] >= n_f)
+      return fail(EGFEM_ERR_INVALID_ARGUMENT, "COO index out of range");
+    key[e] = (uint64_t)i[e] * (uint64_t)n_u + (uint64_t)j[e];
+    kk[e] = (uint32_t)k[e];
+  }
+  bool closed = (n_u == n_f);  // T·₂u lands inside the (i,j) fiber pattern?
+  if (closed) {
+    std::vector<uint64_t> pat(key);
+    std::sort(pat.begin(), pat.end());
+    for (int64_t e = 0; e < nnz && closed; ++e)
+      closed = std::binary_search(pat.begin(), pat.end(), (uint64_t)i[e] * (uint64_t)n_u + (uint64_t)k[e]);
+  }
+  int ndev = 0;
+  if (cudaGetDeviceCount(&ndev) != cudaSuccess || device < 0 || device >= ndev) {
+    cudaGetLastError();
+    return fail(EGFEM_ERR_INVALID_ARGUMENT, "no such CUDA device");
+  }
+  DeviceGuard g(device);
+  egfem_tensor* t = new egfem_tensor();
+  t->device = device;
+  t->dtype = dtype;
+  t->n_u = n_u;
+  t->n_f = n_f;
+  t->w_is_v = (n_u == n_f);
+  t->newton_wv_ok = closed;
+  uint64_t* dkey = nullptr;
+  uint32_t* dk = nullptr;
+  double* dval = nullptr;
+  auto cleanup = [&](egfem_status s) {
+    if (dkey) cudaFree(dkey);
+    if (dk) cudaFree(dk);
+    if (dval) cudaFree(dval);
+    free_tensor(t);
+    delete t;
+    return s;
+  };
+  const size_t n1 = (size_t)std::max<int64_t>(nnz, 1);
+  if (cudaMalloc(&dkey, 8 * n1) || cudaMalloc(&dk, 4 * n1) || cudaMalloc(&dval, 8 * n1))
+    return cleanup(fail(EGFEM_ERR_OUT_OF_MEMORY, "cudaMalloc failed"));
+  if (nnz > 0 && (cudaMemcpy(dkey, key.data(), 8 * nnz, cudaMemcpyHostToDevice) ||
+                  cudaMemcpy(dk, kk.data(), 4 * nnz, cudaMemcpyHostToDevice) ||
+                  cudaMemcpy(dval, val, 8 * nnz, cudaMemcpyHostToDevice)))
+    return cleanup(fail(EGFEM_ERR_CUDA, "cudaMemcpy failed"));
+  egfem_status st = build_from_triples(t, nnz, dkey, dk, dval);
+  dkey = nullptr;
+  dk = nullptr;
+  dval = nullptr;
+  if (st) return cleanup(st);
+  *out = t;
+  return EGFEM_OK;
+}
+
+egfem_status egfem_tensor_destroy(egfem_tensor* t) {
+  if (!t) return EGFEM_OK;
+  DeviceGuard g(t->device);
+  free_tensor(t);
+  delete t;
+  return EGFEM_OK;
+}
+
+egfem_status egfem_tensor_info(const egfem_tensor* t, int64_t* n_u, int64_t* n_f, int64_t* nnz, int64_t* nnz_csr,
+                               egfem_dtype* dtype) {
+  if (!t) return fail(EGFEM_ERR_INVALID_ARGUMENT, "tensor is NULL");
+  if (n_u) *n_u = t->n_u;
+  if (n_f) *n_f = t->n_f;
+  if (nnz) *nnz = t->nnz;
+  if (nnz_csr) *nnz_csr = t->n_fib;
+  if (dtype) *dtype = t->dtype;
+  return EGFEM_OK;
+}
+
+egfem_status egfem_tensor_csr_pattern(const egfem_tensor* t, const int64_t** d_row_ptr, const int32_t** d_col) {
+  if (!t) return fail(EGFEM_ERR_INVALID_ARGUMENT, "tensor is NULL");
+  if (d_row_ptr) *d_row_ptr = t->row_fib;
+  if (d_col) *d_col = t->fib_j;
+  return EGFEM_OK;
+}
+
+egfem_status egfem_tensor_export(const egfem_tensor* t, int64_t* t_row_ptr, int32_t* t_j, int32_t* t_k, void* t_val,
+                                 int64_t* csr_row_ptr, int32_t* csr_col, int32_t* slot_ij, int32_t* slot_ik,
+                                 uint8_t* loc) {
+  if (!t) return fail(EGFEM_ERR_INVALID_ARGUMENT, "tensor is NULL");
+  if (slot_ik && !t->w_is_v) return fail(EGFEM_ERR_UNSUPPORTED, "slot_ik needs W = V numbering");
+  if (loc && !(t->has_mesh && t->w_p0)) return fail(EGFEM_ERR_UNSUPPORTED, "loc needs W = P0");
+  DeviceGuard g(t->device);
+  return export_arrays(t, t_row_ptr, t_j, t_k, t_val, csr_row_ptr, csr_col, slot_ij, slot_ik, loc);
+}
+
+egfem_status egfem_interp(const egfem_tensor* t, egfem_interp_kind kind, double p, const void* u, void* w,
+                          void* chain, egfem_stream_t stream) {
+  if (!t) return fail(EGFEM_ERR_INVALID_ARGUMENT, "tensor is NULL");
+  if (kind < EGFEM_INTERP_IDENTITY || kind > EGFEM_INTERP_P1_TO_P2_SQUARE)
+    return fail(EGFEM_ERR_INVALID_ARGUMENT, "bad interp kind");
+  egfem_status st;
+  if ((st = check_dev_ptr(t, u, "u", true)) || (st = check_dev_ptr(t, w, "w", true)) ||
+      (st = check_dev_ptr(t, chain, "chain", false)))
+    return st;
+  switch (kind) {
+    case EGFEM_INTERP_IDENTITY:
+    case EGFEM_INTERP_SQUARE:
+      if (!t->w_is_v) return fail(EGFEM_ERR_DIMENSION_MISMATCH, "IDENTITY/SQUARE need W = V");
+      if (chain) return fail(EGFEM_ERR_INVALID_ARGUMENT, "chain is only produced by GRADPOW_P0");
+      break;
+    case EGFEM_INTERP_GRADPOW_P0:
+      if (!t->has_mesh || !t->w_p0 || t->vfam != EGFEM_P1)
+        return fail(EGFEM_ERR_UNSUPPORTED, "GRADPOW_P0 needs V = P1, W = P0 and a mesh");
+      if (!(p > 1.0)) return fail(EGFEM_ERR_INVALID_ARGUMENT, "GRADPOW_P0 needs p > 1");
+      break;
+    default:
+      if (!t->has_mesh || t->vfam != EGFEM_P1 || t->wfam != EGFEM_P2 || t->dim != 2)
+        return fail(EGFEM_ERR_UNSUPPORTED, "P1_TO_P2_SQUARE needs V = P1, W = P2 (2D)");
+      if (chain) return fail(EGFEM_ERR_INVALID_ARGUMENT, "chain is only produced by GRADPOW_P0");
+  }
+  DeviceGuard g(t->device);
+  return launch_interp(t, kind, p, u, w, chain, (cudaStream_t)stream);
+}
+
+egfem_status egfem_apply(const egfem_tensor* t, const void* u, const void* w, void* r, egfem_stream_t stream) {
+  if (!t) return fail(EGFEM_ERR_INVALID_ARGUMENT, "tensor is NULL");
+  egfem_status st;
+  if ((st = check_dev_ptr(t, u, "u", true)) || (st = check_dev_ptr(t, w, "w", true)) ||
+      (st = check_dev_ptr(t, r, "r", true)))
+    return st;
+  DeviceGuard g(t->device);
+  return launch_tile(t, true, 0, EGFEM_INTERP_IDENTITY, u, w, nullptr, r, nullptr, (cudaStream_t)stream);
+}
+
+egfem_status egfem_apply_batched(const egfem_tensor* t, int32_t batch, egfem_layout layout, const void* U,
+                                 const void* W, void* R, egfem_stream_t stream) {
+  if (!t) return fail(EGFEM_ERR_INVALID_ARGUMENT, "tensor is NULL");
+  if (batch < 1) return fail(EGFEM_ERR_INVALID_ARGUMENT, "batch must be >= 1");
+  if (layout != EGFEM_LAYOUT_NODE_MAJOR && layout != EGFEM_LAYOUT_PAIR_MAJOR)
+    return fail(EGFEM_ERR_INVALID_ARGUMENT, "bad layout");
+  if ((int64_t)batch * std::max(t->n_u, t->n_f) >= (int64_t(1) << 62))
+    return fail(EGFEM_ERR_INDEX_OVERFLOW, "batch too large");
+  egfem_status st;
+  if ((st = check_dev_ptr(t, U, "U", true)) || (st = check_dev_ptr(t, W, "W", true)) ||
+      (st = check_dev_ptr(t, R, "R", true)))
+    return st;
+  DeviceGuard g(t->device);
+  return launch_batched(t, batch, layout, U, W, R, (cudaStream_t)stream);
+}
+
+static egfem_status jac_mode_code(const egfem_tensor* t, egfem_jac_mode mode, egfem_interp_kind kind, double p,
+                                  const void* u, const void* chain, int* code) {
+  if (mode == EGFEM_JAC_PICARD) {
+    *code = 1;
+    return EGFEM_OK;
+  }
+  if (mode != EGFEM_JAC_NEWTON) return fail(EGFEM_ERR_INVALID_ARGUMENT, "bad Jacobian mode");
+  egfem_status st;
+  if ((st = check_dev_ptr(t, u, "u", true))) return st;
+  switch (kind) {
+    case EGFEM_INTERP_IDENTITY:
+    case EGFEM_INTERP_SQUARE:
+      if (!t->w_is_v) return fail(EGFEM_ERR_DIMENSION_MISMATCH, "IDENTITY/SQUARE Newton needs W = V");
+      if (!t->newton_wv_ok)
+        return fail(EGFEM_ERR_UNSUPPORTED, "T·₂u has entries outside the CSR pattern (from_coo tensor)");
+      *code = 2;
+      return EGFEM_OK;
+    case EGFEM_INTERP_GRADPOW_P0:
+      if (!t->has_mesh || !t->w_p0 || t->vfam != EGFEM_P1)
+        return fail(EGFEM_ERR_UNSUPPORTED, "GRADPOW_P0 Newton needs V = P1, W = P0");
+      if (!(p > 1.0)) return fail(EGFEM_ERR_INVALID_ARGUMENT, "GRADPOW_P0 needs p > 1");
+      if ((st = check_dev_ptr(t, chain, "chain", true))) return st;
+      *code = 3;
+      return EGFEM_OK;
+    case EGFEM_INTERP_P1_TO_P2_SQUARE:
+      return fail(EGFEM_ERR_UNSUPPORTED, "NEWTON with P1_TO_P2_SQUARE is not implemented on the GPU");
+    default:
+      return fail(EGFEM_ERR_INVALID_ARGUMENT, "bad interp kind");
+  }
+}
+
+egfem_status egfem_jacobian(const egfem_tensor* t, egfem_jac_mode mode, egfem_interp_kind kind, double p,
+                            const void* u, const void* w, const void* chain, void* csr_vals, egfem_stream_t stream) {
+  if (!t) return fail(EGFEM_ERR_INVALID_ARGUMENT, "tensor is NULL");
+  egfem_status st;
+  if ((st = check_dev_ptr(t, w, "w", true)) || (st = check_dev_ptr(t, csr_vals, "csr_vals", true))) return st;
+  int code = 0;
+  if ((st = jac_mode_code(t, mode, kind, p, u, chain, &code))) return st;
+  DeviceGuard g(t->device);
+  return launch_tile(t, false, code, kind, u, w, chain, nullptr, csr_vals, (cudaStream_t)stream);
+}
+
+egfem_status egfem_apply_jacobian(const egfem_tensor* t, egfem_jac_mode mode, egfem_interp_kind kind, double p,
+                                  const void* u, const void* w, const void* chain, void* r, void* csr_vals,
+                                  egfem_stream_t stream) {
+  if (!t) return fail(EGFEM_ERR_INVALID_ARGUMENT, "tensor is NULL");
+  egfem_status st;
+  if ((st = check_dev_ptr(t, u, "u", true)) || (st = check_dev_ptr(t, w, "w", true)) ||
+      (st = check_dev_ptr(t, r, "r", true)) || (st = check_dev_ptr(t, csr_vals, "csr_vals", true)))
+    return st;
+  int code = 0;
+  if ((st = jac_mode_code(t, mode, kind, p, u, chain, &code))) return st;
+  DeviceGuard g(t->device);
+  return launch_tile(t, true, code, kind, u, w, chain, r, csr_vals, (cudaStream_t)stream);
+}
+
+egfem_status egfem_halo_pack(const egfem_tensor* local, const int32_t* d_idx, int64_t n, const void* u_local,
+                             void* send_buf, egfem_stream_t stream) {
+  if (!local) return fail(EGFEM_ERR_INVALID_ARGUMENT, "tensor is NULL");
+  if (n < 0) return fail(EGFEM_ERR_INVALID_ARGUMENT, "n < 0");
+  if (n == 0) return EGFEM_OK;
+  egfem_status st;
+  if ((st = check_dev_ptr(local, d_idx, "idx", true)) || (st = check_dev_ptr(local, u_local, "u_local", true)) ||
+      (st = check_dev_ptr(local, send_buf, "send_buf", true)))
+    return st;
+  DeviceGuard g(local->device);
+  return launch_halo(local, d_idx, n, u_local, send_buf, true, (cudaStream_t)stream);
+}
+
+egfem_status egfem_halo_unpack(const egfem_tensor* local, const int32_t* d_idx, int64_t n, const void* recv_buf,
+                               void* u_local, egfem_stream_t stream) {
+  if (!local) return fail(EGFEM_ERR_INVALID_ARGUMENT, "tensor is NULL");
+  if (n < 0) return fail(EGFEM_ERR_INVALID_ARGUMENT, "n < 0");
+  if (n == 0) return EGFEM_OK;
+  egfem_status st;
+  if ((st = check_dev_ptr(local, d_idx, "idx", true)) || (st = check_dev_ptr(local, recv_buf, "recv_buf", true)) ||
+      (st = check_dev_ptr(local, u_local, "u_local", true)))
+    return st;
+  DeviceGuard g(local->device);
+  return launch_halo(local, d_idx, n, recv_buf, u_local, false, (cudaStream_t)stream);
+}
+
+// ------------------------------------------------------------------ partition
+egfem_status egfem_partition_rows(int64_t n_rows, const int64_t* prefix, int32_t nranks, int64_t* bounds) {
+  if (n_rows < 0 || !prefix || !bounds || nranks < 1) return fail(EGFEM_ERR_INVALID_ARGUMENT, "bad arguments");
+  // Rank r owns rows [bounds[r], bounds[r+1]): the first row whose prefix reaches
+  // r·nnz/nranks (ceil) starts rank r.  Deterministic and monotone.
+  const int64_t total = prefix[n_rows];
+  bounds[0] = 0;
+  for (int32_t r = 1; r < nranks; ++r) {
+    const int64_t target = (total * r + nranks - 1) / nranks;
+    const int64_t* p = std::lower_bound(prefix, prefix + n_rows + 1, target);
+    int64_t row = (int64_t)(p - prefix);
+    row = std::min<int64_t>(std::max<int64_t>(row, bounds[r - 1]), n_rows);
+    bounds[r] = row;
+  }
+  bounds[nranks] = n_rows;
+  return EGFEM_OK;
+}
+
+egfem_status egfem_partition(const egfem_tensor* G, int32_t nranks, int32_t rank, int device, egfem_tensor** out,
+                             int64_t* row_begin, int64_t* row_end, int64_t* col_begin, int64_t* col_end,
+                             int64_t* w_begin, int64_t* w_end) {
+  if (!G || !out) return fail(EGFEM_ERR_INVALID_ARGUMENT, "NULL argument");
+  *out = nullptr;
+  if (nranks < 1 || rank < 0 || rank >= nranks) return fail(EGFEM_ERR_INVALID_ARGUMENT, "bad rank / nranks");
+  if (device != G->device) return fail(EGFEM_ERR_UNSUPPORTED, "partition onto another device");
+  if (G->has_mesh && !G->w_p0 && !G->w_is_v)
+    return fail(EGFEM_ERR_UNSUPPORTED, "row partition needs W = V or W = P0");
+  DeviceGuard g(G->device);
+  // host copies of the integer structure (offline)
+  std::vector<int64_t> row_fib(G->n_u + 1);
+  std::vector<uint32_t> fib_nz(G->n_fib + 1);
+  EGFEM_CUDA_TRY(cudaMemcpy(row_fib.data(), G->row_fib, 8 * (G->n_u + 1), cudaMemcpyDeviceToHost));
+  EGFEM_CUDA_TRY(cudaMemcpy(fib_nz.data(), G->fib_nz, 4 * (G->n_fib + 1), cudaMemcpyDeviceToHost));
+  std::vector<int64_t> prefix(G->n_u + 1);
+  for (int64_t i = 0; i <= G->n_u; ++i) prefix[i] = fib_nz[row_fib[i]];
+  std::vector<int64_t> bounds(nranks + 1);
+  egfem_partition_rows(G->n_u, prefix.data(), nranks, bounds.data());
+  const int64_t rb = bounds[rank], re = bounds[rank + 1];
+  const int64_t f0 = row_fib[rb], f1 = row_fib[re];
+  const int64_t e0 = fib_nz[f0], e1 = fib_nz[f1];
+  const int64_t nf = f1 - f0, ne = e1 - e0, nr = re - rb;
+  std::vector<int32_t> fj(nf);
+  std::vector<uint32_t> nk(ne);
+  if (nf) EGFEM_CUDA_TRY(cudaMemcpy(fj.data(), G->fib_j + f0, 4 * nf, cudaMemcpyDeviceToHost));
+  if (ne) EGFEM_CUDA_TRY(cudaMemcpy(nk.data(), G->nz_k + e0, 4 * ne, cudaMemcpyDeviceToHost));
+  int64_t cb = rb, ce = re;  // column window includes the owned rows
+  for (int32_t j : fj) {
+    cb = std::min<int64_t>(cb, j);
+    ce = std::max<int64_t>(ce, (int64_t)j + 1);
+  }
+  const bool p0 = G->has_mesh && G->w_p0;
+  std::vector<int32_t> wlist;  // P0: referenced cells, ascending
+  if (p0) {
+    wlist.reserve(ne / 4 + 1);
+    for (uint32_t x : nk) wlist.push_back((int32_t)(x & kKMask));
+    std::sort(wlist.begin(), wlist.end());
+    wlist.erase(std::unique(wlist.begin(), wlist.end()), wlist.end());
+  } else {
+    for (uint32_t x : nk) {  // W = V: k lies in the column window
+      const int64_t k = x & kKMaskAny;
+      cb = std::min<int64_t>(cb, k);
+      ce = std::max<int64_t>(ce, k + 1);
+    }
+  }
+  // local arrays
+  egfem_tensor* t = new egfem_tensor();
+  t->device = device;
+  t->dtype = G->dtype;
+  t->form = G->form;
+  t->dim = G->dim;
+  t->vfam = G->vfam;
+  t->wfam = G->wfam;
+  t->nV = G->nV;
+  t->nW = G->nW;
+  t->n_u = nr;  // local rows
+  t->nnz = ne;
+  t->n_fib = nf;
+  t->row_begin = rb;
+  t->col_begin = cb;
+  t->w_is_v = G->w_is_v;
+  t->w_p0 = G->w_p0;
+  t->newton_wv_ok = G->newton_wv_ok;
+  const int64_t n_local = ce - cb;
+  auto bail = [&](egfem_status s) {
+    free_tensor(t);
+    delete t;
+    return s;
+  };
+  std::vector<int64_t> lrf(nr + 1);
+  for (int64_t i = 0; i <= nr; ++i) lrf[i] = row_fib[rb + i] - f0;
+  std::vector<uint32_t> lfn(nf + 1);
+  for (int64_t f = 0; f <= nf; ++f) lfn[f] = (uint32_t)(fib_nz[f0 + f] - e0);
+  for (auto& j : fj) j = (int32_t)(j - cb);
+  if (p0) {
+    for (auto& x : nk) {
+      const int32_t K = (int32_t)(x & kKMask);
+      const int32_t lk = (int32_t)(std::lower_bound(wlist.begin(), wlist.end(), K) - wlist.begin());
+      x = (uint32_t)lk | (x & ~kKMask);
+    }
+    t->n_f = (int64_t)wlist.size();
+  } else {
+    for (auto& x : nk) x = (uint32_t)((int64_t)(x & kKMaskAny) - cb) | (x & kHead);
+    t->n_f = n_local;
+  }
+  // NOTE: the local column space has n_local entries; rows are a prefix-free subset.
+  const size_t vs = t->dtype == EGFEM_F64 ? 8 : 4;
+  std::vector<int64_t> lrn(nr + 1);
+  for (int64_t i = 0; i <= nr; ++i) lrn[i] = (int64_t)lfn[lrf[i]];
+  if (dmalloc_padded((void**)&t->row_nz, 8 * (nr + 1)) ||
+      cudaMemcpy(t->row_nz, lrn.data(), 8 * (nr + 1), cudaMemcpyHostToDevice))
+    return bail(fail(EGFEM_ERR_OUT_OF_MEMORY, "row_nz upload failed"));
+  if (dmalloc_padded((void**)&t->row_fib, 8 * (nr + 1)) || dmalloc_padded((void**)&t->fib_j, 4 * nf) ||
+      dmalloc_padded((void**)&t->fib_nz, 4 * (nf + 1)) || dmalloc_padded((void**)&t->nz_k, 4 * ne) ||
+      dmalloc_padded(&t->nz_val, vs * ne) || (p0 && dmalloc_padded((void**)&t->nz_aux, ne)))
+    return bail(fail(EGFEM_ERR_OUT_OF_MEMORY, "cudaMalloc failed"));
+  if (p0 && ne && cudaMemcpy(t->nz_aux, G->nz_aux + e0, ne, cudaMemcpyDeviceToDevice))
+    return bail(fail(EGFEM_ERR_CUDA, "cudaMemcpy failed"));
+  if (cudaMemcpy(t->row_fib, lrf.data(), 8 * (nr + 1), cudaMemcpyHostToDevice) ||
+      (nf && cudaMemcpy(t->fib_j, fj.data(), 4 * nf, cudaMemcpyHostToDevice)) ||
+      cudaMemcpy(t->fib_nz, lfn.data(), 4 * (nf + 1), cudaMemcpyHostToDevice) ||
+      (ne && cudaMemcpy(t->nz_k, nk.data(), 4 * ne, cudaMemcpyHostToDevice)) ||
+      (ne && cudaMemcpy(t->nz_val, (const char*)G->nz_val + vs * e0, vs * ne, cudaMemcpyDeviceToDevice)))
+    return bail(fail(EGFEM_ERR_CUDA, "cudaMemcpy failed"));
+  // local mesh data for GRADPOW interp: referenced cells with local vertex ids
+  if (p0) {
+    t->has_mesh = true;
+    const int d1 = G->dim + 1;
+    const int64_t ncl = (int64_t)wlist.size();
+    t->n_cells = ncl;
+    t->n_vertices = n_local;
+    std::vector<int32_t> gcells(G->n_cells * d1), gv(G->n_cells * G->nV);
+    EGFEM_CUDA_TRY(cudaMemcpy(gcells.data(), G->cells, 4 * gcells.size(), cudaMemcpyDeviceToHost));
+    EGFEM_CUDA_TRY(cudaMemcpy(gv.data(), G->vdofs, 4 * gv.size(), cudaMemcpyDeviceToHost));
+    std::vector<int32_t> gwcell(G->n_f);
+    EGFEM_CUDA_TRY(cudaMemcpy(gwcell.data(), G->wcell, 4 * G->n_f, cudaMemcpyDeviceToHost));
+    std::vector<int32_t> lc(ncl * d1), lv(ncl * G->nV), lw(ncl);
+    for (int64_t c = 0; c < ncl; ++c) {
+      const int64_t gc = gwcell[wlist[c]];
+      for (int a = 0; a < d1; ++a) {
+        const int64_t v = gcells[gc * d1 + a] - cb;
+        if (v < 0 || v >= n_local) return bail(fail(EGFEM_ERR_UNSUPPORTED, "cell vertex outside the halo window"));
+        lc[c * d1 + a] = (int32_t)v;
+      }
+      for (int a = 0; a < G->nV; ++a) lv[c * G->nV + a] = gv[gc * G->nV + a] - (int32_t)cb;
+      lw[c] = (int32_t)c;
+    }
+    // P1 geometry: vertex ids are V dofs, coordinates of the window [cb, ce)
+    if (cudaMalloc(&t->coords, 8 * std::max<int64_t>(n_local * G->dim, 1)) ||
+        cudaMalloc(&t->cells, 4 * std::max<int64_t>(ncl * d1, 1)) ||
+        cudaMalloc(&t->vdofs, 4 * std::max<int64_t>(ncl * G->nV, 1)) ||
+        cudaMalloc(&t->wdofs, 4 * std::max<int64_t>(ncl, 1)) || cudaMalloc(&t->wcell, 4 * std::max<int64_t>(ncl, 1)))
+      return bail(fail(EGFEM_ERR_OUT_OF_MEMORY, "cudaMalloc failed"));
+    if (cudaMemcpy(t->coords, G->coords + cb * G->dim, 8 * n_local * G->dim, cudaMemcpyDeviceToDevice) ||
+        (ncl && cudaMemcpy(t->cells, lc.data(), 4 * lc.size(), cudaMemcpyHostToDevice)) ||
+        (ncl && cudaMemcpy(t->vdofs, lv.data(), 4 * lv.size(), cudaMemcpyHostToDevice)) ||
+        (ncl && cudaMemcpy(t->wdofs, lw.data(), 4 * lw.size(), cudaMemcpyHostToDevice)) ||
+        (ncl && cudaMemcpy(t->wcell, lw.data(), 4 * lw.size(), cudaMemcpyHostToDevice)))
+      return bail(fail(EGFEM_ERR_CUDA, "cudaMemcpy failed"));
+  }
+  // tiles of the local rows
+  {
+    egfem_status st = make_tiles(t, lrf, lfn);
+    if (st) return bail(st);
+  }
+  if (row_begin) *row_begin = rb;
+  if (row_end) *row_end = re;
+  if (col_begin) *col_begin = cb;
+  if (col_end) *col_end = ce;
+  if (w_begin) *w_begin = p0 ? (wlist.empty() ? 0 : wlist.front()) : cb;
+  if (w_end) *w_end = p0 ? (wlist.empty() ? 0 : wlist.back() + 1) : ce;
+  *out = t;
+  return EGFEM_OK;
+}
+
+}  // extern "C"

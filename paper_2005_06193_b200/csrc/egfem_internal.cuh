@@ -1,0 +1,122 @@
+// Internal definitions of libegfem.so (B200 / sm_100a).  Not part of the ABI.
+//
+// Device layout of a tensor: a fiber-compressed (CSF) T,
+//   rows i -> fibers (i, j) -> nonzeros (k, value),
+// whose fibers coincide one-to-one with the CSR slots of the Jacobian pattern:
+//   row_fib[i] .. row_fib[i+1]   fibers of row i      (== csr_row_ptr)
+//   fib_j[f]                     column j of fiber f   (== csr_col)
+//   fib_nz[f] .. fib_nz[f+1]     nonzeros of fiber f   (uint32 offsets)
+//   nz_k[e]                      k; bit 31 flags the first nonzero of a fiber; for
+//                                W = P0 bits 28-29 hold loc_j (local index of j in cell k)
+//   row_nz[i]                    first nonzero of row i (== canonical t_row_ptr)
+//   nz_val[e]                    T_ijk in the handle dtype
+// Rows are grouped into tiles (tile_row) of at most kTileNnz nonzeros, kTileFib
+// fibers and kTileRows rows; one CTA processes one tile entirely in shared memory.
+#pragma once
+
+#include <cuda_runtime.h>
+#include <stdint.h>
+
+#include <string>
+#include <vector>
+
+#include "egfem.h"
+
+namespace egfem {
+
+constexpr int kTileNnz = 1024;   // max nonzeros per tile
+constexpr int kTileFib = 512;    // max fibers per tile
+constexpr int kTileRows = 256;   // max rows per tile
+constexpr int kThreads = 256;    // CTA size of the tile kernels
+constexpr int kKShift = 28;      // loc_j packing in nz_k for P0 W (bits 28-29)
+constexpr uint32_t kKMask = (1u << kKShift) - 1u;   // k of a P0-W tensor
+constexpr uint32_t kKMaskAny = 0x7FFFFFFFu;          // k of any other tensor
+constexpr uint32_t kHead = 0x80000000u;              // bit 31: first nonzero of a fiber
+constexpr int kMaxQuad = 16;
+constexpr int kRowsMaxNnz = 256;  // rows up to this length take the row-group path
+
+void set_error(const std::string& msg);
+void count_launch(int n = 1);
+void count_launch_kernel(const char* name);
+
+}  // namespace egfem
+
+struct egfem_tensor {
+  int device = 0;
+  egfem_dtype dtype = EGFEM_F64;
+  bool has_mesh = false;
+  int dim = 0;
+  int64_t n_u = 0, n_f = 0, n_cells = 0, n_vertices = 0;
+  egfem_family vfam = EGFEM_P1, wfam = EGFEM_P1;
+  int nV = 0, nW = 0;
+  egfem_form form = EGFEM_FORM_CONV_J;
+  int64_t nnz = 0, n_fib = 0;
+  bool w_is_v = false;   // W numbering identical to V numbering (IDENTITY/SQUARE allowed)
+  bool w_p0 = false;     // W = P0 (loc packed into nz_k)
+  bool newton_wv_ok = false;  // every (i, k) of T is an (i, j) fiber (T·₂u fits the CSR pattern)
+  int max_row_nnz = 0, max_row_fib = 0;
+  uint32_t kmask() const { return (has_mesh && w_p0) ? egfem::kKMask : egfem::kKMaskAny; }
+
+  // CSF tensor (device)
+  int64_t* row_fib = nullptr;   // n_u+1
+  int64_t* row_nz = nullptr;    // n_u+1 (first nonzero of each row)
+  int32_t* fib_j = nullptr;     // n_fib
+  uint32_t* fib_nz = nullptr;   // n_fib+1
+  uint32_t* nz_k = nullptr;     // nnz
+  void* nz_val = nullptr;       // nnz, dtype
+  uint8_t* nz_aux = nullptr;    // nnz, P0 W only: position of k among the cells of row i
+
+  // tiles (device + host copy of the count)
+  int32_t n_tiles = 0;
+  int64_t* tile_row = nullptr;  // n_tiles+1 first row of each tile
+  int64_t* tile_fib = nullptr;  // n_tiles+1 first fiber
+  int64_t* tile_nz = nullptr;   // n_tiles+1 first nonzero
+
+  // interpolation data (device): geometry in fp64 regardless of dtype
+  double* coords = nullptr;     // n_vertices*dim
+  int32_t* cells = nullptr;     // n_cells*(dim+1) mesh vertex ids (geometry)
+  int32_t* vdofs = nullptr;     // n_cells*nV  V dof ids (u indices)
+  int32_t* wdofs = nullptr;     // n_cells*nW  W dof ids
+  int32_t* wcell = nullptr;     // n_f: cell owning P0 dof k (P0 W only)
+
+  // partition bookkeeping (global handles: 0 / identity)
+  int64_t row_begin = 0, col_begin = 0;
+};
+
+namespace egfem {
+
+// builder / export (egfem_build.cu)
+egfem_status build_from_triples(egfem_tensor* t, int64_t m, uint64_t* d_key_ij, uint32_t* d_k, double* d_val);
+egfem_status upload_mesh(egfem_tensor* t, const egfem_mesh* mesh, const egfem_space* V, const egfem_space* W);
+egfem_status emit_element_triples(egfem_tensor* t, egfem_form form, const egfem_quad* quad, int64_t* m_out,
+                                  uint64_t** key, uint32_t** k, double** val);
+egfem_status export_arrays(const egfem_tensor* t, int64_t* t_row_ptr, int32_t* t_j, int32_t* t_k, void* t_val,
+                           int64_t* csr_row_ptr, int32_t* csr_col, int32_t* slot_ij, int32_t* slot_ik,
+                           uint8_t* loc);
+void free_tensor(egfem_tensor* t);
+egfem_status make_tiles(egfem_tensor* t, const std::vector<int64_t>& row_fib_h, const std::vector<uint32_t>& fib_nz_h);
+cudaError_t dmalloc_padded(void** p, size_t bytes);
+
+// compute kernels (egfem_kernels.cu)
+egfem_status launch_interp(const egfem_tensor* t, egfem_interp_kind kind, double p, const void* u, void* w,
+                           void* chain, cudaStream_t s);
+egfem_status launch_tile(const egfem_tensor* t, bool do_r, int jac, egfem_interp_kind kind, const void* u,
+                         const void* w, const void* chain, void* r, void* csr_vals, cudaStream_t s);
+egfem_status launch_rows(const egfem_tensor* t, bool do_r, int jac, egfem_interp_kind kind, const void* u,
+                         const void* w, const void* chain, void* r, void* csr_vals, cudaStream_t s);
+bool rows_path_ok(const egfem_tensor* t);
+egfem_status launch_batched(const egfem_tensor* t, int32_t batch, egfem_layout layout, const void* U,
+                            const void* W, void* R, cudaStream_t s);
+egfem_status launch_halo(const egfem_tensor* t, const int32_t* idx, int64_t n, const void* src, void* dst,
+                         bool pack, cudaStream_t s);
+
+}  // namespace egfem
+
+#define EGFEM_CUDA_TRY(expr)                                                                  \
+  do {                                                                                        \
+    cudaError_t _e = (expr);                                                                  \
+    if (_e != cudaSuccess) {                                                                  \
+      egfem::set_error(std::string(#expr) + ": " + cudaGetErrorString(_e));                 \
+      return _e == cudaErrorMemoryAllocation ? EGFEM_ERR_OUT_OF_MEMORY : EGFEM_ERR_CUDA;      \
+    }                                                                                         \
+  } while (0)

@@ -1,0 +1,366 @@
+"""GPU ↔ oracle parity through the C ABI (-m gpu).
+
+Bars (BASELINE.json north_star): integer arrays (pattern, slot and
+index maps) bit-exact; fp64 relative L2 ≤ 1e-12; fp32 ≤ 2e-5 against the fp64
+oracle on the fp64 inputs (reading C16).  Small cases run every element through
+the oracle at sizes that span many tiles plus a ragged last tile; full BASELINE
+sizes run whole (cfg1–3, cfg5) or on sampled row blocks the oracle builds row by
+row (cfg4: first, middle and last blocks).
+"""
+import numpy as np
+import pytest
+
+import egfem_inputs as I
+from gpu_helpers import SIX_PT, gpu_pass, oracle_pass
+from helpers import rel_l2
+
+pytestmark = pytest.mark.gpu
+
+FP64_TOL = 1e-12
+FP32_TOL = 2e-5
+INT_KEYS = ("t_row_ptr", "t_j", "t_k", "csr_row_ptr", "csr_col", "slot_ij")
+
+
+@pytest.fixture(scope="module")
+def eg():
+    import torch
+    if not torch.cuda.is_available():
+        pytest.skip("no CUDA device")
+    import __graft_entry__
+    __graft_entry__.build()
+    import paper_2005_06193_b200 as eg
+    return eg
+
+
+@pytest.fixture(scope="module")
+def orc():
+    import oracle
+    oracle.build()
+    return oracle
+
+
+def _build_both(eg, orc, pr, dtype=0, rows=None):
+    t = eg.egfem_tensor_build(pr.mesh, pr.V, pr.W, pr.form, dtype=dtype, device=0)
+    o = orc.OracleTensor(pr.mesh, pr.V, pr.W, pr.form, rows=rows)
+    return t, o
+
+
+def _maps_kw(pr):
+    p0 = pr.W.family == I.P0
+    return dict(slot_ik=not p0, loc=p0)
+
+
+SMALL = [("cfg1", None), ("cfg2", None), ("cfg3", None), ("cfg4", None), ("cfg5", None),
+         ("cfg2", 7), ("cfg3", 5), ("cfg4", 3), ("cfg4", 1), ("cfg3", 1), ("cfg1", 1), ("cfg5", 1)]
+
+
+@pytest.mark.parametrize("name,n", SMALL)
+def test_builder_bit_exact_small(eg, orc, name, n):
+    """A0: canonical integer arrays memcmp-equal; values within 1e-12 (fp64)."""
+    pr = I.make_problem(name, n=n if n else I.SMALL_N[name], batch=1)
+    t, o = _build_both(eg, orc, pr)
+    assert (t.nnz, t.nnz_csr) == (o.nnz, o.nnz_csr)
+    kw = _maps_kw(pr)
+    ex, oex = t.export(**kw), o.export(**kw)
+    for key in INT_KEYS + tuple(k for k, v in kw.items() if v):
+        assert np.array_equal(ex[key], oex[key]), key
+    assert rel_l2(ex["t_val"], oex["t_val"]) <= FP64_TOL
+    assert np.abs(ex["t_val"] - oex["t_val"]).max() <= 1e-15 * max(1.0, np.abs(oex["t_val"]).max()) * 8
+
+
+@pytest.mark.parametrize("name,n", SMALL)
+@pytest.mark.parametrize("fused", [False, True])
+def test_hot_path_small(eg, orc, name, n, fused):
+    """A1–A3 on every element: interp, apply, Picard and Newton Jacobians (fp64)."""
+    pr = I.make_problem(name, n=n if n else I.SMALL_N[name], batch=1)
+    u = pr.u[0] if pr.batch else pr.u
+    t, o = _build_both(eg, orc, pr)
+    g = gpu_pass(eg, t, pr, u, fused=fused)
+    ref = oracle_pass(o, pr, u)
+    if pr.interp == I.INTERP_IDENTITY:
+        assert np.array_equal(g["w"], ref["w"])  # IDENTITY is a copy: bit-exact
+    for key in ("w", "r", "A", "J"):
+        assert rel_l2(g[key], ref[key]) <= FP64_TOL, (key, rel_l2(g[key], ref[key]))
+
+
+def test_fused_equals_separate_bitwise(eg):
+    """egfem_apply_jacobian is bitwise identical to egfem_apply + egfem_jacobian; runs are reproducible."""
+    for name in ("cfg2", "cfg4"):
+        pr = I.make_problem(name, n=I.SMALL_N[name])
+        t = eg.egfem_tensor_build(pr.mesh, pr.V, pr.W, pr.form, device=0)
+        a = gpu_pass(eg, t, pr, pr.u, fused=False)
+        b = gpu_pass(eg, t, pr, pr.u, fused=True)
+        c = gpu_pass(eg, t, pr, pr.u, fused=False)
+        for key in ("r", "A", "J", "w"):
+            assert np.array_equal(a[key], b[key]), key
+            assert np.array_equal(a[key], c[key]), key
+
+
+@pytest.mark.parametrize("name", ["cfg1", "cfg2", "cfg3", "cfg5"])
+def test_full_size_whole(eg, orc, name):
+    """BASELINE sizes, every element: builder maps bit-exact, hot path within 1e-12."""
+    pr = I.make_problem(name, batch=2)
+    u = pr.u[0] if pr.batch else pr.u
+    t, o = _build_both(eg, orc, pr)
+    kw = _maps_kw(pr)
+    ex, oex = t.export(**kw), o.export(**kw)
+    for key in INT_KEYS + tuple(k for k, v in kw.items() if v):
+        assert np.array_equal(ex[key], oex[key]), key
+    assert rel_l2(ex["t_val"], oex["t_val"]) <= FP64_TOL
+    newton = name != "cfg5"  # cfg5 is action-only (reading C24)
+    g = gpu_pass(eg, t, pr, u, newton=newton)
+    ref = oracle_pass(o, pr, u, newton=newton)
+    for key in ("w", "r", "A") + (("J",) if newton else ()):
+        assert rel_l2(g[key], ref[key]) <= FP64_TOL, key
+
+
+def _row_blocks(n_u, size):
+    return [(0, size), (n_u // 2 - size // 2, n_u // 2 + size // 2), (n_u - size, n_u)]
+
+
+@pytest.mark.parametrize("dtype", [0, 1])
+def test_cfg4_full_size_sampled_rows(eg, orc, dtype):
+    """cfg4 at BASELINE size in the launch configuration bench.py times: whole w (interp over
+    all 12.58M cells) and the first/middle/last row blocks of T, r, A, J vs a row-restricted
+    oracle build.  fp32 compares against the fp64 oracle (reading C16)."""
+    import torch
+    pr = I.make_problem("cfg4")
+    t = eg.egfem_tensor_build(pr.mesh, pr.V, pr.W, pr.form, dtype=dtype, device=0)
+    assert (t.nnz, t.nnz_csr) == (201326592, 31802497)
+    g = gpu_pass(eg, t, pr, pr.u, fused=True)
+    ex = t.export(loc=True)
+    tol = FP64_TOL if dtype == 0 else FP32_TOL
+    o_full = orc.OracleTensor(pr.mesh, pr.V, pr.W, pr.form, rows=(0, 1))
+    ow = o_full.interp(pr.interp, pr.p, pr.u)
+    assert rel_l2(g["w"], ow) <= tol
+    for r0, r1 in _row_blocks(t.n_u, 4000):
+        o = orc.OracleTensor(pr.mesh, pr.V, pr.W, pr.form, rows=(r0, r1))
+        oex = o.export(loc=True)
+        a, b = ex["t_row_ptr"][r0], ex["t_row_ptr"][r1]
+        for key in ("t_j", "t_k", "loc"):
+            assert np.array_equal(ex[key][a:b], oex[key]), key
+        assert np.array_equal(ex["t_row_ptr"][r0:r1 + 1] - a, oex["t_row_ptr"][r0:r1 + 1])
+        assert rel_l2(ex["t_val"][a:b], oex["t_val"]) <= (FP64_TOL if dtype == 0 else 1e-7)
+        ca, cb = ex["csr_row_ptr"][r0], ex["csr_row_ptr"][r1]
+        assert np.array_equal(ex["csr_col"][ca:cb], oex["csr_col"])
+        ref_r = o.apply(pr.u, ow)[r0:r1]
+        assert rel_l2(g["r"][r0:r1], ref_r) <= tol
+        assert rel_l2(g["A"][ca:cb], o.jacobian(0, pr.interp, pr.p, pr.u, ow)) <= tol
+        assert rel_l2(g["J"][ca:cb], o.jacobian(1, pr.interp, pr.p, pr.u, ow)) <= tol
+    del t
+    torch.cuda.empty_cache()
+
+
+@pytest.mark.parametrize("n", [6, 10])
+def test_cfg4_fp32_small(eg, orc, n):
+    pr = I.make_problem("cfg4", n=n)
+    t, o = _build_both(eg, orc, pr, dtype=1)
+    g = gpu_pass(eg, t, pr, pr.u)
+    ref = oracle_pass(o, pr, pr.u)
+    for key in ("w", "r", "A", "J"):
+        assert rel_l2(g[key], ref[key]) <= FP32_TOL, key
+
+
+@pytest.mark.parametrize("layout", [0, 1])
+@pytest.mark.parametrize("B", [1, 8, 37])
+def test_batched_small(eg, orc, layout, B):
+    """A2 batched: R_p = T:(U_p ⊗ W_p), NODE_MAJOR and PAIR_MAJOR, B not a multiple of 32."""
+    import torch
+    pr = I.make_problem("cfg5", n=I.SMALL_N["cfg5"], batch=B)
+    t, o = _build_both(eg, orc, pr)
+    U = pr.u
+    rng = np.random.default_rng(5)
+    Wv = U + 0.1 * rng.standard_normal(U.shape)  # w ≠ u to catch slot mix-ups
+    R_ref = o.apply_batched(U, Wv)
+    if layout == 0:
+        Ud = torch.tensor(U.T.copy(), device="cuda").contiguous()
+        Wd = torch.tensor(Wv.T.copy(), device="cuda").contiguous()
+    else:
+        Ud = torch.tensor(U, device="cuda")
+        Wd = torch.tensor(Wv, device="cuda")
+    R = torch.empty_like(Ud)
+    eg.egfem_apply_batched(t, B, layout, Ud, Wd, R)
+    Rh = R.cpu().numpy()
+    Rh = Rh.T if layout == 0 else Rh
+    assert rel_l2(Rh, R_ref) <= FP64_TOL
+
+
+def test_cfg5_full_size_batched_sampled_pairs(eg, orc):
+    """cfg5 at BASELINE size, B = 256 node-major (the bench launch): pairs 0, 77, 255 whole."""
+    import torch
+    pr = I.make_problem("cfg5")
+    t = eg.egfem_tensor_build(pr.mesh, pr.V, pr.W, pr.form, device=0)
+    o = orc.OracleTensor(pr.mesh, pr.V, pr.W, pr.form)
+    U = torch.tensor(pr.u.T.copy(), device="cuda")
+    R = torch.empty_like(U)
+    eg.egfem_apply_batched(t, 256, 0, U, U, R)
+    Rh = R.cpu().numpy()
+    for p in (0, 77, 255):
+        assert rel_l2(Rh[:, p], o.apply(pr.u[p], pr.u[p])) <= FP64_TOL
+
+
+def test_interp_kinds(eg, orc):
+    """SQUARE (W = V) and P1_TO_P2_SQUARE (Case 1) interpolation plus their Jacobians."""
+    import torch
+    m = I.mesh_square(9)
+    V, W2 = I.space_p1(m), I.space_p2_square(9)
+    u = np.random.default_rng(3).standard_normal(V.n_dofs)
+    # P1 -> P2 square with MASS3
+    t = eg.egfem_tensor_build(m, V, W2, I.FORM_MASS3, device=0)
+    o = orc.OracleTensor(m, V, W2, I.FORM_MASS3)
+    ud = torch.tensor(u, device="cuda")
+    w = torch.empty(t.n_f, dtype=torch.float64, device="cuda")
+    eg.egfem_interp(t, I.INTERP_P1_TO_P2_SQUARE, 0, ud, w)
+    ow = o.interp(I.INTERP_P1_TO_P2_SQUARE, 0, u)
+    assert rel_l2(w.cpu().numpy(), ow) <= FP64_TOL
+    r = torch.empty(t.n_u, dtype=torch.float64, device="cuda")
+    eg.egfem_apply(t, ud, w, r)
+    assert rel_l2(r.cpu().numpy(), o.apply(u, ow)) <= FP64_TOL
+    # SQUARE with W = V
+    t = eg.egfem_tensor_build(m, V, V, I.FORM_CONV_J, device=0)
+    o = orc.OracleTensor(m, V, V, I.FORM_CONV_J)
+    w = torch.empty(t.n_f, dtype=torch.float64, device="cuda")
+    eg.egfem_interp(t, I.INTERP_SQUARE, 0, ud, w)
+    ow = o.interp(I.INTERP_SQUARE, 0, u)
+    assert rel_l2(w.cpu().numpy(), ow) <= FP64_TOL
+    J = torch.empty(t.nnz_csr, dtype=torch.float64, device="cuda")
+    eg.egfem_jacobian(t, I.JAC_NEWTON, I.INTERP_SQUARE, 0, ud, w, None, J)
+    assert rel_l2(J.cpu().numpy(), o.jacobian(1, I.INTERP_SQUARE, 0, u, ow)) <= FP64_TOL
+
+
+def test_user_quadrature_and_jittered_mesh(eg, orc):
+    """Explicit quadrature (the 6-point rule passed in) on an unstructured (jittered) P2 mesh."""
+    n = 8
+    m = I.mesh_square(n)
+    rng = np.random.default_rng(2)
+    x = m.coords.copy()
+    inner = np.all((x > 1e-12) & (x < 1 - 1e-12), axis=1)
+    x[inner] += 0.2 / n * rng.uniform(-1, 1, (inner.sum(), 2))
+    m = I.Mesh(2, x, m.cells)
+    V = I.space_p2_square(n)
+    bary, wq = [], []
+    for a, ww in ((SIX_PT[0], SIX_PT[1]), (SIX_PT[2], SIX_PT[3])):
+        for pnt in ((1 - 2 * a, a, a), (a, 1 - 2 * a, a), (a, a, 1 - 2 * a)):
+            bary.append(pnt)
+            wq.append(ww)
+    t = eg.egfem_tensor_build(m, V, V, I.FORM_CONV_I, quad=(np.array(bary), np.array(wq)), device=0)
+    o = orc.OracleTensor(m, V, V, I.FORM_CONV_I, quad=(np.array(bary), np.array(wq)))
+    ex, oex = t.export(), o.export()
+    for key in INT_KEYS:
+        assert np.array_equal(ex[key], oex[key]), key
+    assert rel_l2(ex["t_val"], oex["t_val"]) <= FP64_TOL
+
+
+def test_from_coo_random_with_duplicates(eg):
+    """egfem_tensor_from_coo: arbitrary order, duplicates summed; apply vs a dense einsum."""
+    import torch
+    rng = np.random.default_rng(11)
+    n_u, n_f, nnz = 300, 300, 20000
+    i = rng.integers(0, n_u, nnz)
+    j = rng.integers(0, n_u, nnz)
+    k = rng.integers(0, n_f, nnz)
+    v = rng.standard_normal(nnz)
+    t = eg.egfem_tensor_from_coo(n_u, n_f, i, j, k, v, device=0)
+    D = np.zeros((n_u, n_u, n_f))
+    np.add.at(D, (i, j, k), v)
+    assert t.nnz == len(set(zip(i.tolist(), j.tolist(), k.tolist())))
+    u, w = rng.standard_normal(n_u), rng.standard_normal(n_f)
+    ud, wd = torch.tensor(u, device="cuda"), torch.tensor(w, device="cuda")
+    r = torch.empty(n_u, dtype=torch.float64, device="cuda")
+    eg.egfem_apply(t, ud, wd, r)
+    assert rel_l2(r.cpu().numpy(), np.einsum("ijk,j,k->i", D, u, w)) <= FP64_TOL
+    A = torch.empty(t.nnz_csr, dtype=torch.float64, device="cuda")
+    eg.egfem_jacobian(t, 0, 0, 0, None, wd, None, A)
+    ex = t.export()
+    Ad = np.zeros((n_u, n_u))
+    Ad[np.repeat(np.arange(n_u), np.diff(ex["csr_row_ptr"])), ex["csr_col"]] = A.cpu().numpy()
+    assert rel_l2(Ad, np.einsum("ijk,k->ij", D, w)) <= FP64_TOL
+    J = torch.empty_like(A)
+    with pytest.raises(eg.EgfemError) as e:  # T·₂u leaves the (i,j) pattern of a random tensor
+        eg.egfem_jacobian(t, 1, 0, 0, ud, wd, None, J)
+    assert e.value.status == 3
+    # a tensor whose (i,k) pairs are all fibers: k ∈ {i, j} plus the diagonal (i,i,i)
+    k2 = np.where(rng.random(nnz) < 0.5, i, j)
+    i2, j2 = np.concatenate([i, np.arange(n_u)]), np.concatenate([j, np.arange(n_u)])
+    k2 = np.concatenate([k2, np.arange(n_u)])
+    v2 = rng.standard_normal(len(i2))
+    t2 = eg.egfem_tensor_from_coo(n_u, n_f, i2, j2, k2, v2, device=0)
+    D2 = np.zeros((n_u, n_u, n_f))
+    np.add.at(D2, (i2, j2, k2), v2)
+    J = torch.empty(t2.nnz_csr, dtype=torch.float64, device="cuda")
+    eg.egfem_jacobian(t2, 1, 0, 0, ud, wd, None, J)
+    ex2 = t2.export()
+    Jd = np.zeros((n_u, n_u))
+    Jd[np.repeat(np.arange(n_u), np.diff(ex2["csr_row_ptr"])), ex2["csr_col"]] = J.cpu().numpy()
+    assert rel_l2(Jd, np.einsum("ijk,k->ij", D2, w) + np.einsum("ijk,j->ik", D2, u)) <= FP64_TOL
+
+
+def test_validation_errors(eg):
+    """Validation happens before any launch and returns the documented status codes."""
+    import torch
+    pr = I.make_problem("cfg3", n=4)
+    t = eg.egfem_tensor_build(pr.mesh, pr.V, pr.W, pr.form, device=0)
+    u = torch.zeros(t.n_u, dtype=torch.float64, device="cuda")
+    w = torch.zeros(t.n_f, dtype=torch.float64, device="cuda")
+    r = torch.zeros(t.n_u, dtype=torch.float64, device="cuda")
+    with pytest.raises(eg.EgfemError) as e:
+        eg.egfem_apply(t, u, None, r)
+    assert e.value.status == 1
+    with pytest.raises(eg.EgfemError) as e:
+        eg.egfem_apply(t, u, w.cpu(), r)  # host pointer
+    assert e.value.status == 1
+    with pytest.raises(eg.EgfemError) as e:
+        eg.egfem_interp(t, I.INTERP_IDENTITY, 0, u, w)  # W = P0 ≠ V
+    assert e.value.status == 2
+    with pytest.raises(eg.EgfemError) as e:
+        eg.egfem_interp(t, I.INTERP_GRADPOW_P0, 1.0, u, w)  # p ≤ 1
+    assert e.value.status == 1
+    with pytest.raises(eg.EgfemError) as e:
+        eg.egfem_apply(t, u[1:], w, r)  # misaligned
+    assert e.value.status == 1
+    bad = I.Mesh(2, pr.mesh.coords, pr.mesh.cells.copy())
+    bad.cells[3, 1] = 10 ** 6
+    with pytest.raises(eg.EgfemError) as e:
+        eg.egfem_tensor_build(bad, pr.V, pr.W, pr.form, device=0)
+    assert e.value.status == 1
+
+
+@pytest.mark.parametrize("name,nranks", [("cfg4", 2), ("cfg4", 3), ("cfg3", 4), ("cfg2", 3), ("cfg1", 5)])
+def test_partition_emulation_bitwise(eg, name, nranks):
+    """8(e): the G local problems run one after another on one GPU, each on its u window
+    [col_begin, col_end), reproduce the single-GPU r and CSR values bitwise."""
+    import torch
+    pr = I.make_problem(name, n=I.SMALL_N[name])
+    t = eg.egfem_tensor_build(pr.mesh, pr.V, pr.W, pr.form, device=0)
+    ref = gpu_pass(eg, t, pr, pr.u)
+    r_all, J_all = [], []
+    for rank in range(nranks):
+        loc, win = eg.egfem_partition(t, nranks, rank)
+        ul = torch.tensor(pr.u[win["col_begin"]:win["col_end"]], device="cuda")
+        wl = torch.empty(loc.n_f, dtype=torch.float64, device="cuda")
+        chain = None
+        if pr.interp == I.INTERP_GRADPOW_P0:
+            chain = torch.empty(loc.n_f * (pr.mesh.dim + 1), dtype=torch.float64, device="cuda")
+        eg.egfem_interp(loc, pr.interp, pr.p, ul, wl, chain)
+        r = torch.empty(loc.n_u, dtype=torch.float64, device="cuda")
+        J = torch.empty(loc.nnz_csr, dtype=torch.float64, device="cuda")
+        eg.egfem_apply_jacobian(loc, 1, pr.interp, pr.p, ul, wl, chain, r, J)
+        torch.cuda.synchronize()
+        assert loc.n_u == win["row_end"] - win["row_begin"]
+        r_all.append(r.cpu().numpy())
+        J_all.append(J.cpu().numpy())
+    assert np.array_equal(np.concatenate(r_all), ref["r"])
+    assert np.array_equal(np.concatenate(J_all), ref["J"])
+
+
+def test_tile_path(eg):
+    """The TMA-pipelined tile kernel (general path for rows > 256 nonzeros) matches the oracle."""
+    import os
+    import subprocess
+    import sys
+    here = os.path.dirname(os.path.abspath(__file__))
+    env = dict(os.environ, EGFEM_PATH="tile")
+    res = subprocess.run([sys.executable, os.path.join(here, "tile_path_check.py")], env=env,
+                         capture_output=True, text=True, timeout=600)
+    assert res.returncode == 0, res.stdout + res.stderr
+    assert "tile path ok" in res.stdout

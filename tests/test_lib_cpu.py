@@ -1,0 +1,90 @@
+"""C-ABI library checks that need no GPU (-m "not gpu"): the .so loads, exports every
+symbol include/egfem.h declares, and its host-only logic behaves."""
+import os
+import re
+
+import numpy as np
+import pytest
+
+ROOT = os.path.dirname(os.path.dirname(os.path.abspath(__file__)))
+
+
+@pytest.fixture(scope="module")
+def eg():
+    import __graft_entry__
+    __graft_entry__.build()
+    import paper_2005_06193_b200 as eg
+    return eg
+
+
+def header_functions():
+    src = open(os.path.join(ROOT, "include", "egfem.h")).read()
+    return sorted(set(re.findall(r"^\s*(?:egfem_status|uint64_t|const char\*)\s+(egfem_\w+)\s*\(", src, re.M)))
+
+
+def test_header_declares_the_north_star_boundary():
+    fns = header_functions()
+    for name in ("egfem_tensor_build", "egfem_interp", "egfem_apply", "egfem_jacobian"):
+        assert name in fns
+
+
+def test_library_exports_every_declared_symbol(eg):
+    import ctypes
+    lib = ctypes.CDLL(eg.LIB_PATH)
+    missing = [f for f in header_functions() if not hasattr(lib, f)]
+    assert not missing, missing
+    assert sorted(eg.EXPORTS) == header_functions()
+
+
+def test_nm_shows_sm100a_cubin(eg):
+    """The library carries sm_100a device code (cuobjdump lists the ELF arch)."""
+    import shutil
+    import subprocess
+    if not shutil.which("cuobjdump"):
+        pytest.skip("cuobjdump missing")
+    out = subprocess.run(["cuobjdump", "--list-elf", eg.LIB_PATH], capture_output=True, text=True).stdout
+    assert "sm_100a" in out
+
+
+def test_status_strings(eg):
+    L = eg.lib()
+    for code, name in eg.STATUS.items():
+        assert L.egfem_status_string(code).decode() == name
+
+
+def test_null_handle_is_rejected_without_gpu(eg):
+    """Validation runs before any CUDA call: a NULL tensor returns INVALID_ARGUMENT."""
+    L = eg.lib()
+    assert L.egfem_apply(None, None, None, None, None) == 1
+    assert L.egfem_interp(None, 0, 0.0, None, None, None, None) == 1
+    assert L.egfem_jacobian(None, 0, 0, 0.0, None, None, None, None, None) == 1
+    assert "NULL" in L.egfem_last_error().decode()
+    assert L.egfem_tensor_destroy(None) == 0
+
+
+def _py_partition(prefix, nranks):
+    total = prefix[-1]
+    b = [0]
+    for r in range(1, nranks):
+        target = -(-total * r // nranks)
+        row = int(np.searchsorted(prefix, target, side="left"))
+        b.append(min(max(row, b[-1]), len(prefix) - 1))
+    b.append(len(prefix) - 1)
+    return np.array(b)
+
+
+@pytest.mark.parametrize("nranks", [1, 2, 3, 8, 17])
+def test_partition_rows_matches_python(eg, nranks):
+    rng = np.random.default_rng(nranks)
+    counts = rng.integers(0, 100, 5000)
+    prefix = np.concatenate([[0], np.cumsum(counts)])
+    b = eg.egfem_partition_rows(prefix, nranks)
+    assert np.array_equal(b, _py_partition(prefix, nranks))
+    assert b[0] == 0 and b[-1] == 5000 and np.all(np.diff(b) >= 0)
+    loads = prefix[b[1:]] - prefix[b[:-1]]
+    assert loads.max() - loads.min() <= 2 * counts.max() + 1  # nnz-balanced
+
+
+def test_partition_rows_edge_cases(eg):
+    assert np.array_equal(eg.egfem_partition_rows(np.array([0]), 4), [0, 0, 0, 0, 0])
+    assert np.array_equal(eg.egfem_partition_rows(np.array([0, 5]), 3), [0, 1, 1, 1])
