@@ -564,6 +564,11 @@ egfem_status egfem_partition(const egfem_tensor* G, int32_t nranks, int32_t rank
         cudaMalloc(&t->vdofs, 4 * std::max<int64_t>(ncl * G->nV, 1)) ||
         cudaMalloc(&t->wdofs, 4 * std::max<int64_t>(ncl, 1)) || cudaMalloc(&t->wcell, 4 * std::max<int64_t>(ncl, 1)))
       return bail(fail(EGFEM_ERR_OUT_OF_MEMORY, "cudaMalloc failed"));
+    t->vdofs_is_cells = G->vdofs_is_cells;
+    t->wdofs_is_iota = true;
+    if (G->dim == 3 && (cudaMalloc(&t->coords4, 32 * std::max<int64_t>(n_local, 1)) ||
+                        cudaMemcpy(t->coords4, G->coords4 + cb * 4, 32 * n_local, cudaMemcpyDeviceToDevice)))
+      return bail(fail(EGFEM_ERR_CUDA, "coords4 copy failed"));
     if (cudaMemcpy(t->coords, G->coords + cb * G->dim, 8 * n_local * G->dim, cudaMemcpyDeviceToDevice) ||
         (ncl && cudaMemcpy(t->cells, lc.data(), 4 * lc.size(), cudaMemcpyHostToDevice)) ||
         (ncl && cudaMemcpy(t->vdofs, lv.data(), 4 * lv.size(), cudaMemcpyHostToDevice)) ||

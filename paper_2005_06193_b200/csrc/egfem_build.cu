@@ -400,6 +400,18 @@ egfem_status upload_mesh(egfem_tensor* t, const egfem_mesh* mesh, const egfem_sp
   const int32_t* hw = table(W, t->nW);
   EGFEM_CUDA_TRY(cudaMalloc(&t->wdofs, sizeof(int32_t) * nc * t->nW));
   EGFEM_CUDA_TRY(cudaMemcpy(t->wdofs, hw, sizeof(int32_t) * nc * t->nW, cudaMemcpyHostToDevice));
+  t->vdofs_is_cells = (V->family == EGFEM_P1) && std::equal(hvcopy.begin(), hvcopy.end(), mesh->cells);
+  if (W->family == EGFEM_P0) {
+    t->wdofs_is_iota = true;
+    for (int64_t c = 0; c < nc && t->wdofs_is_iota; ++c) t->wdofs_is_iota = (hw[c] == (int32_t)c);
+  }
+  if (d == 3) {
+    std::vector<double> c4((size_t)mesh->n_vertices * 4, 0.0);
+    for (int64_t v = 0; v < mesh->n_vertices; ++v)
+      for (int q = 0; q < 3; ++q) c4[v * 4 + q] = mesh->coords[v * 3 + q];
+    EGFEM_CUDA_TRY(cudaMalloc(&t->coords4, sizeof(double) * c4.size()));
+    EGFEM_CUDA_TRY(cudaMemcpy(t->coords4, c4.data(), sizeof(double) * c4.size(), cudaMemcpyHostToDevice));
+  }
   t->w_is_v = (V->family == W->family) && (V->n_dofs == W->n_dofs) &&
               std::equal(hvcopy.begin(), hvcopy.end(), hw);
   t->w_p0 = (W->family == EGFEM_P0);
@@ -832,7 +844,7 @@ egfem_status export_arrays(const egfem_tensor* t, int64_t* t_row_ptr, int32_t* t
 
 void free_tensor(egfem_tensor* t) {
   void* ptrs[] = {t->row_fib, t->row_nz, t->fib_j, t->fib_nz, t->nz_k, t->nz_val, t->nz_aux, t->tile_row, t->tile_fib,
-                  t->tile_nz, t->coords, t->cells, t->vdofs, t->wdofs, t->wcell};
+                  t->tile_nz, t->coords, t->coords4, t->cells, t->vdofs, t->wdofs, t->wcell};
   for (void* p : ptrs)
     if (p) cudaFree(p);
 }

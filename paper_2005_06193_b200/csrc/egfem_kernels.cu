@@ -44,26 +44,60 @@ __global__ void k_interp_copy(const S* __restrict__ u, S* __restrict__ w, int64_
 
 // GRADPOW_P0: g_K = Σ_a u_{v_a} ∇λ_a (Π_∇u ·₂ u at the cell's DOF), w_K = ‖g_K‖^{p−2},
 // chain[K][m] = ∂w_K/∂u_{v_m} = (p−2)‖g‖^{p−4} g·∇λ_m (reading C11).
-template <typename S, int D>
-__global__ void k_interp_gradpow(const double* __restrict__ coords, const int32_t* __restrict__ cells,
+// Thread per cell; 3D reads the cell as one int4 and each vertex as two double2 from the
+// 32-byte padded coordinate array, and writes the chain row as two 16-byte stores.
+template <int D>
+struct CellIdx {
+  int32_t v[D + 1];
+};
+template <int D>
+__device__ __forceinline__ CellIdx<D> load_cell(const int32_t* __restrict__ t, int64_t c) {
+  CellIdx<D> r;
+  if constexpr (D == 3) {
+    const int4 q = __ldg(reinterpret_cast<const int4*>(t) + c);
+    r.v[0] = q.x;
+    r.v[1] = q.y;
+    r.v[2] = q.z;
+    r.v[3] = q.w;
+  } else {
+#pragma unroll
+    for (int a = 0; a <= D; ++a) r.v[a] = __ldg(t + c * (D + 1) + a);
+  }
+  return r;
+}
+
+template <typename S, int D, bool SAME, bool IOTA>
+__global__ void __launch_bounds__(128) k_interp_gradpow(const double* __restrict__ coords, const int32_t* __restrict__ cells,
                                  const int32_t* __restrict__ vdofs, const int32_t* __restrict__ wdofs, int64_t n_cells,
                                  const S* __restrict__ u, S* __restrict__ w, S* __restrict__ chain, double p) {
   int64_t c = (int64_t)blockIdx.x * blockDim.x + threadIdx.x;
   if (c >= n_cells) return;
+  const CellIdx<D> cv = load_cell<D>(cells, c);
+  const CellIdx<D> dv = SAME ? cv : load_cell<D>(vdofs, c);
   double x[D + 1][D];
   double uv[D + 1];
 #pragma unroll
   for (int a = 0; a <= D; ++a) {
-    const int64_t v = __ldg(cells + c * (D + 1) + a);
-#pragma unroll
-    for (int q = 0; q < D; ++q) x[a][q] = __ldg(coords + v * D + q);
-    uv[a] = (double)ld_ro(u + __ldg(vdofs + c * (D + 1) + a));
+    const int64_t v = cv.v[a];
+    if constexpr (D == 3) {
+      const double2 xy = __ldg(reinterpret_cast<const double2*>(coords + v * 4));
+      x[a][0] = xy.x;
+      x[a][1] = xy.y;
+      x[a][2] = __ldg(coords + v * 4 + 2);
+    } else if constexpr (D == 2) {
+      const double2 xy = __ldg(reinterpret_cast<const double2*>(coords + v * 2));
+      x[a][0] = xy.x;
+      x[a][1] = xy.y;
+    } else {
+      x[a][0] = __ldg(coords + v);
+    }
+    uv[a] = (double)__ldg(u + dv.v[a]);
   }
-  // edge vectors e_a = x_a − x_0 and the barycentric gradients of vertices 1..D
+  // barycentric gradients of vertices 1..D from the edge vectors e_a = x_a − x_0
   double g[D + 1][D];
-  if (D == 1) {
+  if constexpr (D == 1) {
     g[1][0] = 1.0 / (x[1][0] - x[0][0]);
-  } else if (D == 2) {
+  } else if constexpr (D == 2) {
     const double e1x = x[1][0] - x[0][0], e1y = x[1][1] - x[0][1];
     const double e2x = x[2][0] - x[0][0], e2y = x[2][1] - x[0][1];
     const double inv = 1.0 / (e1x * e2y - e1y * e2x);
@@ -124,15 +158,26 @@ __global__ void k_interp_gradpow(const double* __restrict__ coords, const int32_
     wk = pow(gg, 0.5 * (p - 2.0));
     fac = gg > 0.0 ? (p - 2.0) * pow(gg, 0.5 * (p - 4.0)) : 0.0;
   }
-  const int64_t K = __ldg(wdofs + c);
+  const int64_t K = IOTA ? c : (int64_t)__ldg(wdofs + c);
   w[K] = (S)wk;
   if (chain) {
+    S dm[D + 1];
 #pragma unroll
     for (int a = 0; a <= D; ++a) {
       double s = 0.0;
 #pragma unroll
       for (int q = 0; q < D; ++q) s += gu[q] * g[a][q];
-      chain[K * (D + 1) + a] = (S)(fac * s);
+      dm[a] = (S)(fac * s);
+    }
+    if constexpr (D == 3 && sizeof(S) == 8) {
+      double2* o = reinterpret_cast<double2*>(chain + K * 4);
+      o[0] = make_double2(dm[0], dm[1]);
+      o[1] = make_double2(dm[2], dm[3]);
+    } else if constexpr (D == 3) {
+      reinterpret_cast<float4*>(chain)[K] = make_float4(dm[0], dm[1], dm[2], dm[3]);
+    } else {
+#pragma unroll
+      for (int a = 0; a <= D; ++a) chain[K * (D + 1) + a] = dm[a];
     }
   }
 }
@@ -631,14 +676,20 @@ egfem_status launch_interp(const egfem_tensor* t, egfem_interp_kind kind, double
   } else if (kind == EGFEM_INTERP_GRADPOW_P0) {
     const int grid = nblk(t->n_cells, 128);
     if (t->n_cells > 0) {
-#define EGFEM_GP(S, D)                                                                                        \
-  k_interp_gradpow<S, D><<<grid, 128, 0, s>>>(t->coords, t->cells, t->vdofs, t->wdofs, t->n_cells, (const S*)u, \
-                                              (S*)w, (S*)chain, p)
+#define EGFEM_GP3(S, D, SA, IO)                                                                       \
+  k_interp_gradpow<S, D, SA, IO><<<grid, 128, 0, s>>>(D == 3 ? t->coords4 : t->coords, t->cells, t->vdofs,   \
+                                                      t->wdofs, t->n_cells, (const S*)u, (S*)w, (S*)chain, p)
+#define EGFEM_GP(S, D)                                                          \
+  do {                                                                          \
+    if (t->vdofs_is_cells && t->wdofs_is_iota) EGFEM_GP3(S, D, true, true);     \
+    else EGFEM_GP3(S, D, false, false);                                         \
+  } while (0)
       if (f64) {
         if (t->dim == 1) EGFEM_GP(double, 1); else if (t->dim == 2) EGFEM_GP(double, 2); else EGFEM_GP(double, 3);
       } else {
         if (t->dim == 1) EGFEM_GP(float, 1); else if (t->dim == 2) EGFEM_GP(float, 2); else EGFEM_GP(float, 3);
       }
+#undef EGFEM_GP3
 #undef EGFEM_GP
       count_launch();
     }

@@ -4,5 +4,5 @@ timeout 300 python __graft_entry__.py smoke > gpurun_out/smoke.log 2>&1; echo "s
 timeout 1500 python -m pytest tests -m gpu -q -x --timeout 900 -p no:cacheprovider > gpurun_out/pytest_gpu.log 2>&1; echo "pytest rc=$?" >> gpurun_out/pytest_gpu.log
 timeout 600 python bench.py --steps 20 --warmup 3 --no-cpu-baseline > gpurun_out/bench.log 2>&1; echo "bench rc=$?" >> gpurun_out/bench.log
 timeout 300 python scripts/profile_cfg4.py > gpurun_out/prof_plain.log 2>&1 && \
-timeout 900 ncu --set full --clock-control none --import-source on -k 'regex:k_rows|k_interp_gradpow' -c 4 -o gpurun_out/prof_cfg4_v3 -f python scripts/profile_cfg4.py > gpurun_out/ncu.log 2>&1
+timeout 900 ncu --set full --clock-control none --import-source on -k 'regex:k_rows|k_interp_gradpow' -c 4 -o gpurun_out/prof_cfg4_v5 -f python scripts/profile_cfg4.py > gpurun_out/ncu.log 2>&1
 echo "ncu rc=$?" >> gpurun_out/ncu.log
