@@ -273,7 +273,7 @@ def run_ours(args):
                            (" + NCCL u-halo" if world > 1 else ""),
                    "l2": "inputs larger than L2 (T stream 2.7 GB > 126 MB L2); no flush",
                    "parallelism": f"row-partition x{world}" if world > 1 else "single GPU"},
-        "roofline": {"bound": "hbm", "kernel": "k_tile<double,DO_R,NewtonP0> (egfem_apply_jacobian)",
+        "roofline": {"bound": "hbm", "kernel": "k_rows<S,G,NCH,FREG,DO_R=1,NewtonP0> (egfem_apply_jacobian)",
                      "achieved": achieved, "peak": peak, "peak_kind": peak_kind, "unit": "GB/s",
                      "frac": achieved / peak, "algorithmic_bytes": fused_bytes,
                      "traffic": _traffic(workload, "fused")},
