@@ -714,7 +714,7 @@ egfem_status launch_tile(const egfem_tensor* t, bool do_r, int jac, egfem_interp
   // TMA-pipelined tile kernel (kept as the general path and as a cross-check in the tests).
   static const char* force = getenv("EGFEM_PATH");
   const bool tile = force && force[0] == 't';
-  if (!tile && rows_path_ok(t)) return launch_rows(t, do_r, jac, kind, u, w, chain, r, csr_vals, s);
+  if (!tile && rows_path_ok(t, jac)) return launch_rows(t, do_r, jac, kind, u, w, chain, r, csr_vals, s);
   if (t->dtype == EGFEM_F64) return tile_dispatch<double>(t, do_r, jac, kind, u, w, chain, r, csr_vals, s);
   return tile_dispatch<float>(t, do_r, jac, kind, u, w, chain, r, csr_vals, s);
 }
