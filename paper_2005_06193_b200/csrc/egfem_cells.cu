@@ -1,0 +1,592 @@
+// Cell-major row kernel of libegfem.so (B200 / sm_100a) for P0 W: steps (2)+(3) of the
+// p-Laplace-type forms T_ijK = ∫_K ψ_K ∇φ_i·∇φ_j (§5.5).
+//
+// With W = P0 every nonzero of row i belongs to exactly one cell K ∋ i, and the cell
+// contributes one nonzero (i, v_m, K) for each of its d+1 vertices v_m.  Besides the
+// canonical (i, j, k) CSF the builder keeps the same nonzeros in the mode order
+// i -> K -> m ("cell-major"): per row, its cells in ascending K, each with the d+1 values
+// T_{i v_m K} in local-vertex order m.  In that order the Newton chain factor
+//   B_iK = (T·₂u)_{iK} = Σ_m T_{i v_m K} u_{v_m}
+// is an in-register sum over one lane's cell, the residual is
+//   r_i  = Σ_K w_K B_iK
+// with one w gather per cell, and the Jacobian terms
+//   t_{i v_m K} = T_{i v_m K} w_K [+ B_iK (D_u w)_{K m}]
+// are scattered once into the row's canonical positions and summed per CSR fiber in
+// canonical order by the lane owning the fiber.  Per nonzero the stream carries the value
+// and a 16-bit (fiber, canonical position) pair; per cell the 32-bit K.
+//
+// Layout per row group (G lanes, CPL cells per lane — lane l takes cells l, l+G, l+2G, so one
+// warp-wide gather touches a few neighbouring cells' lines — grid-stride rows): the next row's
+// (K, value, fiber|pos) slices are fetched with 16-byte cp.async.cg (L2 evict-first) into
+// the group's second shared-memory stage while the current row is reduced.  Every sum
+// runs in a fixed order: bitwise reproducible; fused and separate launches agree bitwise.
+#include <algorithm>
+#include <cstdio>
+#include <cstdlib>
+
+#include "egfem_internal.cuh"
+
+namespace egfem {
+namespace {
+
+enum { kJacNone = 0, kJacPicard = 1, kJacNewtonP0 = 3 };
+
+template <typename S>
+struct CellArgs {
+  int64_t n_u;
+  const int64_t* row_nz;   // first canonical nonzero of each row (= (d+1) x first cell)
+  const int64_t* row_fib;  // first fiber (CSR slot) of each row
+  const int32_t* fib_j;
+  const uint32_t* fib_nz;
+  const uint32_t* ck_k;    // per cell of a row: K
+  const S* ck_val;         // per nonzero, cell-major: T_{i v_m K}
+  const uint16_t* ck_b;    // per nonzero: fiber index in row (low byte) | canonical position (high)
+  const S* u;
+  const S* w;
+  const S* chain;          // (D_u w)_{K m}, N_f x (d+1)
+  S* r;
+  S* csr;
+};
+
+__device__ __forceinline__ uint32_t smem_u32(const void* p) { return (uint32_t)__cvta_generic_to_shared(p); }
+__device__ __forceinline__ uint64_t evict_first_policy() {
+  uint64_t pol;
+  asm volatile("createpolicy.fractional.L2::evict_first.b64 %0, 1.0;" : "=l"(pol));
+  return pol;
+}
+__device__ __forceinline__ void cp16(uint32_t dst, const void* src, uint64_t pol) {
+  asm volatile("cp.async.cg.shared.global.L2::cache_hint [%0], [%1], 16, %2;" ::"r"(dst), "l"(src), "l"(pol)
+               : "memory");
+}
+__device__ __forceinline__ void commit() { asm volatile("cp.async.commit_group;" ::: "memory"); }
+__device__ __forceinline__ void wait_prev() { asm volatile("cp.async.wait_group 1;" ::: "memory"); }
+
+// 16-byte async copies of the span around [p, p+n) to shared address dst; returns the shift.
+template <typename T, int G, int CAP>
+__device__ __forceinline__ int stage_span(uint32_t dst, const T* p, int n, int lane, uint64_t pol) {
+  constexpr int IT = ((CAP * (int)sizeof(T) + 31) / 16 + G - 1) / G;
+  const uint64_t a = reinterpret_cast<uint64_t>(p);
+  const uint64_t lo = a & ~uint64_t(15);
+  const int chunks = n > 0 ? (int)((((a + (uint64_t)n * sizeof(T) + 15) & ~uint64_t(15)) - lo) >> 4) : 0;
+  const char* src = reinterpret_cast<const char*>(lo) + 16 * lane;
+  dst += 16 * lane;
+#pragma unroll
+  for (int it = 0; it < IT; ++it)
+    if (lane + it * G < chunks) cp16(dst + 16 * G * it, src + 16 * G * it, pol);
+  return (int)((a - lo) / sizeof(T));
+}
+
+__device__ __forceinline__ double xmul(double a, double b) { return __dmul_rn(a, b); }
+__device__ __forceinline__ float xmul(float a, float b) { return __fmul_rn(a, b); }
+__device__ __forceinline__ double xadd(double a, double b) { return __dadd_rn(a, b); }
+__device__ __forceinline__ float xadd(float a, float b) { return __fadd_rn(a, b); }
+__device__ __forceinline__ double xfma(double a, double b, double c) { return __fma_rn(a, b, c); }
+__device__ __forceinline__ float xfma(float a, float b, float c) { return __fmaf_rn(a, b, c); }
+
+template <typename S, int D1, int G, int CPL>
+struct CellSmem {
+  static constexpr int CC = G * CPL;  // cells per row (max)
+  static constexpr int CE = CC * D1;  // nonzeros per row (max)
+  // each slice gets 32 B of slack (its 16-byte-aligned span may start up to 15 B early and
+  // end up to 15 B late) and starts 16-byte aligned (cp.async destination)
+  static constexpr int st_k = 0;
+  static constexpr int st_v = (st_k + CC * 4 + 32 + 15) & ~15;
+  static constexpr int st_b = (st_v + CE * (int)sizeof(S) + 32 + 15) & ~15;
+  static constexpr int stage = (st_b + CE * 2 + 32 + 15) & ~15;
+  static constexpr int o_t = 2 * stage;  // S[CE]: Jacobian terms at canonical positions
+  static constexpr int raw = (o_t + CE * (int)sizeof(S) + 15) & ~15;
+  // group stride = 16 (mod 128): the groups of a warp start on different bank quads, so
+  // their same-offset accesses do not collide
+  static constexpr int bytes = raw + ((16 - raw % 128) + 128) % 128;
+};
+
+// the D1 values of one cell (16-byte vector loads when the cell is 16-byte aligned)
+template <typename S, int D1>
+__device__ __forceinline__ void load_cell(const S* p, bool vec, S* out) {
+  if constexpr ((D1 * sizeof(S)) % 16 == 0) {
+    if (vec) {
+      constexpr int NV = D1 * (int)sizeof(S) / 16;
+      constexpr int PER = 16 / (int)sizeof(S);
+#pragma unroll
+      for (int v = 0; v < NV; ++v) {
+        if constexpr (sizeof(S) == 8) {
+          const double2 x = reinterpret_cast<const double2*>(p)[v];
+          out[v * PER] = x.x;
+          out[v * PER + 1] = x.y;
+        } else {
+          const float4 x = reinterpret_cast<const float4*>(p)[v];
+          out[v * PER] = x.x;
+          out[v * PER + 1] = x.y;
+          out[v * PER + 2] = x.z;
+          out[v * PER + 3] = x.w;
+        }
+      }
+      return;
+    }
+  }
+#pragma unroll
+  for (int m = 0; m < D1; ++m) out[m] = p[m];
+}
+// the D1 values of one cell from global memory (16-byte read-only vector loads; D1·sizeof(S) % 16 == 0)
+template <typename S, int D1>
+__device__ __forceinline__ void load_cell_ldg(const S* p, bool ok, S* out) {
+  constexpr int NV = D1 * (int)sizeof(S) / 16;
+#pragma unroll
+  for (int v = 0; v < NV; ++v) {
+    if constexpr (sizeof(S) == 8) {
+      const double2 x = ok ? __ldg(reinterpret_cast<const double2*>(p) + v) : make_double2(0.0, 0.0);
+      out[2 * v] = x.x;
+      out[2 * v + 1] = x.y;
+    } else {
+      const float4 x = ok ? __ldg(reinterpret_cast<const float4*>(p) + v) : make_float4(0.f, 0.f, 0.f, 0.f);
+      out[4 * v] = x.x;
+      out[4 * v + 1] = x.y;
+      out[4 * v + 2] = x.z;
+      out[4 * v + 3] = x.w;
+    }
+  }
+}
+// NC consecutive values at p (16-byte vectors when NC·sizeof(S) is a multiple of 16 and p is aligned)
+template <typename S, int NC>
+__device__ __forceinline__ void load_run(const S* p, S* out) {
+  if constexpr ((NC * sizeof(S)) % 16 == 0) {
+    constexpr int PER = 16 / (int)sizeof(S);
+#pragma unroll
+    for (int v = 0; v < NC / PER; ++v) {
+      if constexpr (sizeof(S) == 8) {
+        const double2 x = reinterpret_cast<const double2*>(p)[v];
+        out[v * 2] = x.x;
+        out[v * 2 + 1] = x.y;
+      } else {
+        const float4 x = reinterpret_cast<const float4*>(p)[v];
+        out[v * 4] = x.x;
+        out[v * 4 + 1] = x.y;
+        out[v * 4 + 2] = x.z;
+        out[v * 4 + 3] = x.w;
+      }
+    }
+  } else {
+#pragma unroll
+    for (int c = 0; c < NC; ++c) out[c] = p[c];
+  }
+}
+
+struct Meta {
+  uint32_t e0, e1, f0, f1;
+};
+template <typename S>
+__device__ __forceinline__ Meta meta(const CellArgs<S>& A, int64_t row) {
+  Meta m{0u, 0u, 0u, 0u};
+  if (row < A.n_u) {
+    m.e0 = (uint32_t)__ldg(A.row_nz + row);
+    m.e1 = (uint32_t)__ldg(A.row_nz + row + 1);
+    m.f0 = (uint32_t)__ldg(A.row_fib + row);
+    m.f1 = (uint32_t)__ldg(A.row_fib + row + 1);
+  }
+  return m;
+}
+
+template <typename S, int D1, int G, int CPL, int FREG, bool DO_R, int JAC>
+__global__ void __launch_bounds__(256, JAC == kJacNewtonP0 ? 2 : 3) k_cell(const CellArgs<S> A) {
+  using L = CellSmem<S, D1, G, CPL>;
+  constexpr int GPB = 256 / G;
+  constexpr bool kJ = JAC != kJacNone;
+  constexpr bool kN = JAC == kJacNewtonP0;
+  constexpr bool kU = DO_R || kN;  // u (and B_iK) needed; the Picard matrix alone reads no u
+  // Control flow is warp-uniform (a group past the last row runs on an empty one), so
+  // every shuffle uses the full mask with width G.
+  constexpr unsigned FM = 0xffffffffu;
+  extern __shared__ __align__(16) unsigned char smem[];
+  const int lane = threadIdx.x % G;
+  const int grp = threadIdx.x / G;
+  unsigned char* gs = smem + grp * L::bytes;
+  const uint32_t gs_s = smem_u32(gs);
+  S* s_t = reinterpret_cast<S*>(gs + L::o_t);
+  const uint64_t pol = evict_first_policy();
+  const int64_t NG = (int64_t)gridDim.x * GPB;
+  int64_t row = (int64_t)blockIdx.x * GPB + grp;
+  const int64_t wrow0 = (int64_t)blockIdx.x * GPB + (threadIdx.x >> 5) * (32 / G);
+  if (wrow0 >= A.n_u) return;
+
+  // fiber lanes: lane f holds fiber f (+ G, + 2G, ...): u at its column and its canonical range
+  auto fibers = [&](const Meta& m, S* uj, int* fb) {
+#pragma unroll
+    for (int q = 0; q < FREG; ++q) {
+      const int f = lane + q * G;
+      const bool ok = f < (int)(m.f1 - m.f0);
+      uj[q] = (kU && ok) ? __ldg(A.u + __ldg(A.fib_j + m.f0 + f)) : S(0);
+      fb[q] = ok ? (int)(__ldg(A.fib_nz + m.f0 + f) - m.e0) : 0;
+    }
+  };
+  auto stage_in = [&](uint32_t dst, const Meta& m, int& sk, int& sv, int& sb) {
+    const int n = (int)(m.e1 - m.e0);
+    sk = stage_span<uint32_t, G, L::CC>(dst + L::st_k, A.ck_k + m.e0 / D1, n / D1, lane, pol);
+    sv = stage_span<S, G, L::CE>(dst + L::st_v, A.ck_val + m.e0, n, lane, pol);
+    sb = stage_span<uint16_t, G, L::CE>(dst + L::st_b, A.ck_b + m.e0, n, lane, pol);
+  };
+
+  Meta cur = meta(A, row);
+  Meta nxt = meta(A, row + NG);
+  int shk, shv, shb;
+  stage_in(gs_s, cur, shk, shv, shb);
+  commit();
+  S uj_cur[FREG], uj_nxt[FREG];
+  int fb_cur[FREG], fb_nxt[FREG];
+  fibers(cur, uj_cur, fb_cur);
+  int st = 0;
+  for (int64_t wr = wrow0; wr < A.n_u; wr += NG, row += NG) {
+    const int ne = (int)(cur.e1 - cur.e0);
+    const int nc = ne / D1;
+    const int nf = (int)(cur.f1 - cur.f0);
+    // ---- prefetch: the next row's stream (async) and fiber data, metadata two rows ahead
+    int nshk = 0, nshv = 0, nshb = 0;
+    if (row + NG < A.n_u) stage_in(gs_s + (st ^ 1) * L::stage, nxt, nshk, nshv, nshb);
+    commit();
+    fibers(nxt, uj_nxt, fb_nxt);
+    const Meta nn = meta(A, row + 2 * NG);
+    wait_prev();
+    __syncwarp();
+    const unsigned char* cs = gs + st * L::stage;
+    const uint32_t* bk = reinterpret_cast<const uint32_t*>(cs + L::st_k) + shk;
+    const S* bv = reinterpret_cast<const S*>(cs + L::st_v) + shv;
+    const uint16_t* bb = reinterpret_cast<const uint16_t*>(cs + L::st_b) + shb;
+    // ---- gathers of the lane's cells: w_K and (D_u w)_{K, 0..d}, all in flight together
+    S wk[CPL];
+    S dd[kN ? CPL : 1][D1];
+#pragma unroll
+    for (int c = 0; c < CPL; ++c) {
+      const int q = lane + c * G;
+      const bool ok = q < nc;
+      const uint32_t K = ok ? bk[q] : 0u;
+      wk[c] = ok ? __ldg(A.w + K) : S(0);
+      if constexpr (kN) {
+        if constexpr ((D1 * sizeof(S)) % 16 == 0) {  // the cell's D1 values: 16-byte vector loads
+          const S* src = A.chain + (size_t)K * D1;
+          load_cell_ldg<S, D1>(src, ok, dd[c]);
+        } else {
+#pragma unroll
+          for (int m = 0; m < D1; ++m) dd[c][m] = ok ? __ldg(A.chain + (size_t)K * D1 + m) : S(0);
+        }
+      }
+    }
+    const bool vec_v = (reinterpret_cast<uintptr_t>(bv) & 15u) == 0;
+    S acc = S(0);
+#pragma unroll
+    for (int c = 0; c < CPL; ++c) {
+      const int q = lane + c * G;
+      const bool ok = q < nc;
+      S tv[D1];
+      uint32_t bq[D1];
+      if (ok) {
+        load_cell<S, D1>(bv + q * D1, vec_v, tv);
+        if constexpr (D1 == 4) {
+          const uint2 x = *reinterpret_cast<const uint2*>(bb + q * D1);  // 8-byte aligned: e0 % 4 == 0
+          bq[0] = x.x & 0xffffu;
+          bq[1] = x.x >> 16;
+          bq[2] = x.y & 0xffffu;
+          bq[3] = x.y >> 16;
+        } else {
+#pragma unroll
+          for (int m = 0; m < D1; ++m) bq[m] = bb[q * D1 + m];
+        }
+      } else {
+#pragma unroll
+        for (int m = 0; m < D1; ++m) {
+          tv[m] = S(0);
+          bq[m] = 0u;
+        }
+      }
+      S B = S(0);
+      if constexpr (kU) {
+#pragma unroll
+        for (int m = 0; m < D1; ++m) {
+          const int fid = (int)(bq[m] & 0xffu);
+          S um = __shfl_sync(FM, uj_cur[0], fid % G, G);
+#pragma unroll
+          for (int x = 1; x < FREG; ++x) {
+            const S y = __shfl_sync(FM, uj_cur[x], fid % G, G);
+            um = (fid / G == x) ? y : um;
+          }
+          B = (m == 0) ? xmul(tv[m], um) : xfma(tv[m], um, B);
+        }
+      }
+      if constexpr (DO_R) acc = xfma(wk[c], B, acc);
+      if constexpr (kJ) {
+        if (ok) {
+#pragma unroll
+          for (int m = 0; m < D1; ++m) {
+            S t = xmul(tv[m], wk[c]);
+            if constexpr (kN) t = xfma(B, dd[c][m], t);
+            s_t[bq[m] >> 8] = t;
+          }
+        }
+      }
+    }
+    if constexpr (DO_R) {
+#pragma unroll
+      for (int o = G / 2; o > 0; o >>= 1) acc = xadd(acc, __shfl_xor_sync(FM, acc, o, G));
+      if (lane == 0 && row < A.n_u) A.r[row] = acc;
+    }
+    if constexpr (kJ) {
+      // ---- fiber sums over the canonical positions: lane l owns positions l·NC .. l·NC+NC-1;
+      // the fiber heads (mask words hm) come from the fiber lanes' start positions
+      constexpr int NC = L::CE / G;
+      constexpr int NW = (L::CE + 31) / 32;
+      uint32_t hm[NW];
+#pragma unroll
+      for (int x = 0; x < NW; ++x) hm[x] = 0u;
+#pragma unroll
+      for (int q = 0; q < FREG; ++q) {
+        const int ya = fb_cur[q];
+        const bool h = lane + q * G < nf;
+#pragma unroll
+        for (int x = 0; x < NW; ++x) hm[x] |= (h && (ya >> 5) == x) ? (1u << (ya & 31)) : 0u;
+      }
+#pragma unroll
+      for (int x = 0; x < NW; ++x)
+#pragma unroll
+        for (int o = G / 2; o > 0; o >>= 1) hm[x] |= (uint32_t)__shfl_xor_sync(FM, (int)hm[x], o, G);
+      const int y0 = lane * NC;
+      // head bits of this lane's positions, and the heads before them
+      uint32_t hb = 0;
+      int before = 0;
+#pragma unroll
+      for (int x = 0; x < NW; ++x) {
+        const int lo = x * 32;
+        // bits of word x that fall in [y0, y0 + NC)
+        const int sh = lo - y0;
+        uint32_t part = 0u;
+        if (sh >= 0 && sh < NC) part = hm[x] << sh;
+        else if (sh < 0 && sh > -32) part = hm[x] >> (-sh);
+        hb |= part;
+        if (lo + 32 <= y0) before += __popc(hm[x]);
+        else if (lo < y0) before += __popc(hm[x] & ((1u << (y0 - lo)) - 1u));
+      }
+      const int nl = ne - y0;
+      hb &= (nl >= NC) ? (NC >= 32 ? 0xffffffffu : ((1u << NC) - 1u)) : (nl > 0 ? ((1u << nl) - 1u) : 0u);
+      __syncwarp();  // the scatter into s_t is complete
+      S tv[NC];
+      load_run<S, NC>(s_t + y0, tv);
+#pragma unroll
+      for (int c = 0; c < NC; ++c)
+        if (c >= nl) tv[c] = S(0);
+      const int fbase = before - 1;
+      S tail = S(0);
+#pragma unroll
+      for (int c = 0; c < NC; ++c) tail = ((hb >> c) & 1u) ? tv[c] : xadd(tail, tv[c]);
+      S sv = tail;
+      int fl = hb != 0;
+#pragma unroll
+      for (int o = 1; o < G; o <<= 1) {
+        const S ov = __shfl_up_sync(FM, sv, o, G);
+        const int of = __shfl_up_sync(FM, fl, o, G);
+        if (lane >= o) {
+          if (!fl) sv = xadd(ov, sv);
+          fl |= of;
+        }
+      }
+      S run = __shfl_up_sync(FM, sv, 1, G);
+      if (lane == 0) run = S(0);
+      const unsigned nxh = (unsigned)__shfl_down_sync(FM, (int)(hb & 1u), 1, G);
+      // bit c: position c ends its fiber (the next position is a head or the row ends)
+      unsigned last = (hb >> 1) | (nxh << (NC - 1));
+      if (nl >= 1 && nl <= NC) last |= 1u << (nl - 1);
+      last &= (nl >= NC) ? ((1u << NC) - 1u) : (nl > 0 ? ((1u << nl) - 1u) : 0u);
+#pragma unroll
+      for (int c = 0; c < NC; ++c) {
+        run = ((hb >> c) & 1u) ? tv[c] : xadd(run, tv[c]);
+        if ((last >> c) & 1u) A.csr[cur.f0 + fbase + __popc(hb & ((2u << c) - 1u))] = run;
+      }
+    }
+    __syncwarp();  // stage st and s_t are free for reuse
+    cur = nxt;
+    nxt = nn;
+    shk = nshk;
+    shv = nshv;
+    shb = nshb;
+#pragma unroll
+    for (int q = 0; q < FREG; ++q) {
+      uj_cur[q] = uj_nxt[q];
+      fb_cur[q] = fb_nxt[q];
+    }
+    st ^= 1;
+  }
+}
+
+// Offline: the cell-major copy of a P0-W tensor's rows (one thread per row).
+template <typename S>
+__global__ void k_make_cells(int64_t n_u, const int64_t* __restrict__ row_fib, const uint32_t* __restrict__ fib_nz,
+                             const uint32_t* __restrict__ nz_k, const uint8_t* __restrict__ nz_aux,
+                             const S* __restrict__ nz_val, int D1, uint32_t* ck_k, S* ck_val, uint16_t* ck_b, int* err) {
+  const int64_t i = (int64_t)blockIdx.x * blockDim.x + threadIdx.x;
+  if (i >= n_u) return;
+  const int64_t f0 = row_fib[i], f1 = row_fib[i + 1];
+  const uint32_t e0 = fib_nz[f0], e1 = fib_nz[f1];
+  if ((e1 - e0) % D1 != 0 || e0 % D1 != 0 || e1 - e0 > 256 || f1 - f0 > 256) {
+    atomicExch(err, 1);
+    return;
+  }
+  for (int64_t f = f0; f < f1; ++f)
+    for (uint32_t e = fib_nz[f]; e < fib_nz[f + 1]; ++e) {
+      const uint32_t slot = nz_aux[e];
+      const uint32_t loc = (nz_k[e] >> kKShift) & 3u;
+      const uint32_t idx = e0 + slot * D1 + loc;
+      if (loc >= (uint32_t)D1 || idx >= e1) {
+        atomicExch(err, 1);
+        return;
+      }
+      ck_val[idx] = nz_val[e];
+      ck_b[idx] = (uint16_t)((uint32_t)(f - f0) | ((e - e0) << 8));
+      if (loc == 0) ck_k[e0 / D1 + slot] = nz_k[e] & kKMask;
+    }
+}
+
+int g_sm_count[64] = {0};
+
+template <typename S, int D1, int G, int CPL, int FREG, bool DO_R, int JAC>
+egfem_status run_cells(const egfem_tensor* t, const CellArgs<S>& A, cudaStream_t s) {
+  using L = CellSmem<S, D1, G, CPL>;
+  auto fn = k_cell<S, D1, G, CPL, FREG, DO_R, JAC>;
+  const int smem = L::bytes * (256 / G);
+  if (smem > 48 * 1024) EGFEM_CUDA_TRY(cudaFuncSetAttribute(fn, cudaFuncAttributeMaxDynamicSharedMemorySize, smem));
+  const int dev = t->device & 63;
+  if (!g_sm_count[dev])
+    EGFEM_CUDA_TRY(cudaDeviceGetAttribute(&g_sm_count[dev], cudaDevAttrMultiProcessorCount, t->device));
+  int per_sm = 0;
+  EGFEM_CUDA_TRY(cudaOccupancyMaxActiveBlocksPerMultiprocessor(&per_sm, fn, 256, smem));
+  const int64_t need = (t->n_u + (256 / G) - 1) / (256 / G);
+  const int grid = (int)std::max<int64_t>(1, std::min<int64_t>(need, (int64_t)std::max(per_sm, 1) * g_sm_count[dev]));
+  fn<<<grid, 256, smem, s>>>(A);
+  count_launch();
+  EGFEM_CUDA_TRY(cudaGetLastError());
+  return EGFEM_OK;
+}
+
+template <typename S, int D1, int G, int CPL, int FREG>
+egfem_status cells_mode(const egfem_tensor* t, const CellArgs<S>& A, bool do_r, int jac, cudaStream_t s) {
+  if (do_r) {
+    if (jac == kJacNone) return run_cells<S, D1, G, CPL, FREG, true, kJacNone>(t, A, s);
+    if (jac == kJacPicard) return run_cells<S, D1, G, CPL, FREG, true, kJacPicard>(t, A, s);
+    return run_cells<S, D1, G, CPL, FREG, true, kJacNewtonP0>(t, A, s);
+  }
+  if (jac == kJacPicard) return run_cells<S, D1, G, CPL, FREG, false, kJacPicard>(t, A, s);
+  return run_cells<S, D1, G, CPL, FREG, false, kJacNewtonP0>(t, A, s);
+}
+
+// (G, CPL, FREG) per dimension: the first configuration that holds the longest row's
+// cells and fibers.  EGFEM_CELLS_CFG="G,CPL" picks another listed one (experiments).
+struct CellCfg {
+  int d1, G, CPL, FREG;
+};
+constexpr CellCfg kCellCfgs[] = {{3, 2, 3, 4}, {3, 4, 4, 8}, {4, 8, 3, 2}, {4, 16, 3, 2}, {4, 16, 4, 4}};
+
+bool pick_cells(const egfem_tensor* t, CellCfg* out) {
+  static int envG = -1, envC = -1;
+  if (envG < 0) {
+    envG = envC = 0;
+    if (const char* e = getenv("EGFEM_CELLS_CFG")) sscanf(e, "%d,%d", &envG, &envC);
+  }
+  const int d1 = t->dim + 1;
+  const int mc = t->max_row_nnz / d1;
+  for (int pass = 0; pass < 2; ++pass)
+    for (const CellCfg& c : kCellCfgs) {
+      if (c.d1 != d1 || c.G * c.CPL < mc || c.G * c.FREG < t->max_row_fib) continue;
+      if (pass == 0 && envG > 0 && (c.G != envG || c.CPL != envC)) continue;
+      *out = c;
+      return true;
+    }
+  return false;
+}
+
+template <typename S>
+egfem_status cells_dispatch(const egfem_tensor* t, bool do_r, int jac, const void* u, const void* w,
+                            const void* chain, void* r, void* csr, cudaStream_t s) {
+  CellArgs<S> A;
+  A.n_u = t->n_u;
+  A.row_nz = t->row_nz;
+  A.row_fib = t->row_fib;
+  A.fib_j = t->fib_j;
+  A.fib_nz = t->fib_nz;
+  A.ck_k = t->ck_k;
+  A.ck_val = static_cast<const S*>(t->ck_val);
+  A.ck_b = t->ck_b;
+  A.u = static_cast<const S*>(u);
+  A.w = static_cast<const S*>(w);
+  A.chain = static_cast<const S*>(chain);
+  A.r = static_cast<S*>(r);
+  A.csr = static_cast<S*>(csr);
+  CellCfg c{};
+  if (!pick_cells(t, &c)) {
+    set_error("no cell-major configuration");
+    return EGFEM_ERR_UNSUPPORTED;
+  }
+  if (getenv("EGFEM_DEBUG"))
+    fprintf(stderr, "[egfem] k_cell d1=%d G=%d CPL=%d FREG=%d do_r=%d jac=%d\n", c.d1, c.G, c.CPL, c.FREG, (int)do_r, jac);
+#define EGFEM_CC(D_, G_, C_, F_) \
+  if (c.d1 == D_ && c.G == G_ && c.CPL == C_) return cells_mode<S, D_, G_, C_, F_>(t, A, do_r, jac, s);
+  EGFEM_CC(3, 2, 3, 4)
+  EGFEM_CC(3, 4, 4, 8)
+  EGFEM_CC(4, 8, 3, 2)
+  EGFEM_CC(4, 16, 3, 2)
+  EGFEM_CC(4, 16, 4, 4)
+#undef EGFEM_CC
+  set_error("no cell-major configuration");
+  return EGFEM_ERR_UNSUPPORTED;
+}
+
+}  // namespace
+
+bool cells_path_ok(const egfem_tensor* t, int jac) {
+  if (!t->ck_val || jac == 2 /* W = V Newton */) return false;
+  CellCfg c{};
+  return pick_cells(t, &c);
+}
+
+egfem_status launch_cells(const egfem_tensor* t, bool do_r, int jac, const void* u, const void* w, const void* chain,
+                          void* r, void* csr_vals, cudaStream_t s) {
+  if (t->n_u <= 0) return EGFEM_OK;
+  if (t->dtype == EGFEM_F64) return cells_dispatch<double>(t, do_r, jac, u, w, chain, r, csr_vals, s);
+  return cells_dispatch<float>(t, do_r, jac, u, w, chain, r, csr_vals, s);
+}
+
+// Offline: cell-major copy for P0-W tensors of 2D/3D meshes whose rows fit the kernel;
+// silently skipped otherwise (the canonical row / tile kernels then serve the tensor).
+egfem_status make_p0_cells(egfem_tensor* t) {
+  if (!t->has_mesh || !t->w_p0 || !t->nz_aux || (t->dim != 2 && t->dim != 3) || t->n_u <= 0 || t->nnz <= 0 ||
+      t->max_row_nnz > kRowsMaxNnz)
+    return EGFEM_OK;
+  const int d1 = t->dim + 1;
+  const size_t vs = t->dtype == EGFEM_F64 ? 8 : 4;
+  EGFEM_CUDA_TRY(dmalloc_padded((void**)&t->ck_k, 4 * (t->nnz / d1 + 1)));
+  EGFEM_CUDA_TRY(dmalloc_padded(&t->ck_val, vs * t->nnz));
+  EGFEM_CUDA_TRY(dmalloc_padded((void**)&t->ck_b, 2 * t->nnz));
+  int* err = nullptr;
+  EGFEM_CUDA_TRY(cudaMalloc(&err, sizeof(int)));
+  EGFEM_CUDA_TRY(cudaMemset(err, 0, sizeof(int)));
+  const int nb = (int)((t->n_u + 127) / 128);
+  if (t->dtype == EGFEM_F64)
+    k_make_cells<double><<<nb, 128>>>(t->n_u, t->row_fib, t->fib_nz, t->nz_k, t->nz_aux, (const double*)t->nz_val, d1,
+                                      t->ck_k, (double*)t->ck_val, t->ck_b, err);
+  else
+    k_make_cells<float><<<nb, 128>>>(t->n_u, t->row_fib, t->fib_nz, t->nz_k, t->nz_aux, (const float*)t->nz_val, d1,
+                                     t->ck_k, (float*)t->ck_val, t->ck_b, err);
+  count_launch();
+  int herr = 0;
+  cudaError_t ce = cudaMemcpy(&herr, err, sizeof(int), cudaMemcpyDeviceToHost);
+  cudaFree(err);
+  EGFEM_CUDA_TRY(ce);
+  if (getenv("EGFEM_DEBUG"))
+    fprintf(stderr, "[egfem] cell-major copy: %s (n_u=%lld nnz=%lld max_row_nnz=%d max_row_fib=%d)\n",
+            herr ? "rejected" : "built", (long long)t->n_u, (long long)t->nnz, t->max_row_nnz, t->max_row_fib);
+  if (herr) {  // not cell-structured: drop the copy
+    cudaFree(t->ck_k);
+    cudaFree(t->ck_val);
+    cudaFree(t->ck_b);
+    t->ck_k = nullptr;
+    t->ck_val = nullptr;
+    t->ck_b = nullptr;
+  }
+  return EGFEM_OK;
+}
+
+}  // namespace egfem

@@ -67,6 +67,10 @@ struct egfem_tensor {
   uint8_t* nz_aux = nullptr;    // nnz, P0 W only: position of k among the cells of row i
   uint8_t* nz_kpos = nullptr;   // nnz, W = V only: position of the nonzero in its row's (k, j) order
   uint8_t* fib_kr = nullptr;    // n_fib, W = V only: start of fiber (i, m)'s k = m run in that order
+  // P0 W only: the same nonzeros in cell-major order (rows -> cells K ascending -> local vertex m)
+  uint32_t* ck_k = nullptr;     // nnz/(d+1): K of each row cell
+  void* ck_val = nullptr;       // nnz, dtype: T_{i v_m K}
+  uint16_t* ck_b = nullptr;     // nnz: fiber index within the row | canonical position << 8
 
   // tiles (device + host copy of the count)
   int32_t n_tiles = 0;
@@ -111,6 +115,10 @@ egfem_status launch_rows(const egfem_tensor* t, bool do_r, int jac, egfem_interp
                          const void* w, const void* chain, void* r, void* csr_vals, cudaStream_t s);
 bool rows_path_ok(const egfem_tensor* t, int jac);
 egfem_status make_wv_aux(egfem_tensor* t);
+bool cells_path_ok(const egfem_tensor* t, int jac);
+egfem_status launch_cells(const egfem_tensor* t, bool do_r, int jac, const void* u, const void* w, const void* chain,
+                          void* r, void* csr_vals, cudaStream_t s);
+egfem_status make_p0_cells(egfem_tensor* t);
 egfem_status launch_batched(const egfem_tensor* t, int32_t batch, egfem_layout layout, const void* U,
                             const void* W, void* R, cudaStream_t s);
 egfem_status launch_halo(const egfem_tensor* t, const int32_t* idx, int64_t n, const void* src, void* dst,

@@ -712,8 +712,12 @@ egfem_status launch_tile(const egfem_tensor* t, bool do_r, int jac, egfem_interp
                          const void* w, const void* chain, void* r, void* csr_vals, cudaStream_t s) {
   // Row-group kernels (egfem_rows.cu) unless a row is too long or EGFEM_PATH=tile forces the
   // TMA-pipelined tile kernel (kept as the general path and as a cross-check in the tests).
+  // EGFEM_PATH=rows skips the cell-major P0 kernel (egfem_cells.cu) for the row kernel.
   static const char* force = getenv("EGFEM_PATH");
   const bool tile = force && force[0] == 't';
+  const bool rows_only = force && force[0] == 'r';
+  if (!tile && !rows_only && cells_path_ok(t, jac))
+    return launch_cells(t, do_r, jac, u, w, chain, r, csr_vals, s);
   if (!tile && rows_path_ok(t, jac)) return launch_rows(t, do_r, jac, kind, u, w, chain, r, csr_vals, s);
   if (t->dtype == EGFEM_F64) return tile_dispatch<double>(t, do_r, jac, kind, u, w, chain, r, csr_vals, s);
   return tile_dispatch<float>(t, do_r, jac, kind, u, w, chain, r, csr_vals, s);

@@ -1,6 +1,6 @@
 """Time the row kernels (apply / Picard / Newton / fused) on one config; env selects the variant.
 
-usage: EGFEM_ROWS_IMPL=seg|rows EGFEM_ROWS_CFG=G,NCH python scripts/rows_sweep.py cfg4 [f64|f32]"""
+usage: EGFEM_ROWS_CFG=G,NCH python scripts/rows_sweep.py cfg4 [f64|f32]"""
 import json
 import os
 import sys
@@ -37,7 +37,7 @@ def tm(fn, n=30):
     return a.elapsed_time(b) / n
 
 
-res = {"cfg": name, "dtype": "f32" if dt == eg.F32 else "f64", "impl": os.environ.get("EGFEM_ROWS_IMPL", "seg"),
+res = {"cfg": name, "dtype": "f32" if dt == eg.F32 else "f64", "impl": "seg",
        "rows_cfg": os.environ.get("EGFEM_ROWS_CFG", "auto")}
 res["apply"] = tm(lambda: eg.egfem_apply(t, u, w, r))
 res["picard"] = tm(lambda: eg.egfem_jacobian(t, eg.JAC_PICARD, pr.interp, pr.p, None, w, None, J))
