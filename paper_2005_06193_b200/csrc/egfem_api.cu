@@ -582,6 +582,7 @@ egfem_status egfem_partition(const egfem_tensor* G, int32_t nranks, int32_t rank
     if (st) return bail(st);
     if ((st = make_wv_aux(t))) return bail(st);
     if ((st = make_p0_cells(t))) return bail(st);
+    if ((st = make_dense_blocks(t, lrf))) return bail(st);
   }
   if (row_begin) *row_begin = rb;
   if (row_end) *row_end = re;

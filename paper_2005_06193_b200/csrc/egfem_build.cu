@@ -718,6 +718,7 @@ egfem_status build_from_triples(egfem_tensor* t, int64_t m, uint64_t* d_key_ij, 
   if (st) return st;
   if ((st = make_wv_aux(t))) return st;
   if ((st = make_p0_cells(t))) return st;
+  if ((st = make_dense_blocks(t, hrf))) return st;
   EGFEM_CUDA_TRY(cudaDeviceSynchronize());
   return EGFEM_OK;
 }
@@ -845,7 +846,7 @@ egfem_status export_arrays(const egfem_tensor* t, int64_t* t_row_ptr, int32_t* t
 }
 
 void free_tensor(egfem_tensor* t) {
-  void* ptrs[] = {t->row_fib, t->row_nz, t->fib_j, t->fib_nz, t->nz_k, t->nz_val, t->nz_aux, t->nz_kpos, t->fib_kr, t->ck_k, t->ck_val, t->ck_b,
+  void* ptrs[] = {t->row_fib, t->row_nz, t->fib_j, t->fib_nz, t->nz_k, t->nz_val, t->nz_aux, t->nz_kpos, t->fib_kr, t->ck_k, t->ck_val, t->ck_b, t->blk_off, t->blk,
                   t->tile_row, t->tile_fib, t->tile_nz, t->coords, t->coords4, t->cells, t->vdofs, t->wdofs, t->wcell};
   for (void* p : ptrs)
     if (p) cudaFree(p);

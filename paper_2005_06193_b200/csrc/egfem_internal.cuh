@@ -71,6 +71,9 @@ struct egfem_tensor {
   uint32_t* ck_k = nullptr;     // nnz/(d+1): K of each row cell
   void* ck_val = nullptr;       // nnz, dtype: T_{i v_m K}
   uint16_t* ck_b = nullptr;     // nnz: fiber index within the row | canonical position << 8
+  // W = V only (batched action): per row the dense |N|x|N| block over its CSR stencil N(i)
+  int64_t* blk_off = nullptr;   // n_u+1: block offsets (row stride |N| rounded up to even)
+  void* blk = nullptr;          // dtype: M_i[a][b] = T_{i, N_a, N_b}
 
   // tiles (device + host copy of the count)
   int32_t n_tiles = 0;
@@ -119,6 +122,10 @@ bool cells_path_ok(const egfem_tensor* t, int jac);
 egfem_status launch_cells(const egfem_tensor* t, bool do_r, int jac, const void* u, const void* w, const void* chain,
                           void* r, void* csr_vals, cudaStream_t s);
 egfem_status make_p0_cells(egfem_tensor* t);
+bool dense_path_ok(const egfem_tensor* t);
+egfem_status launch_dense(const egfem_tensor* t, int32_t batch, egfem_layout layout, const void* U, const void* W,
+                          void* R, cudaStream_t s);
+egfem_status make_dense_blocks(egfem_tensor* t, const std::vector<int64_t>& hrf);
 egfem_status launch_batched(const egfem_tensor* t, int32_t batch, egfem_layout layout, const void* U,
                             const void* W, void* R, cudaStream_t s);
 egfem_status launch_halo(const egfem_tensor* t, const int32_t* idx, int64_t n, const void* src, void* dst,

@@ -726,6 +726,10 @@ egfem_status launch_tile(const egfem_tensor* t, bool do_r, int jac, egfem_interp
 egfem_status launch_batched(const egfem_tensor* t, int32_t batch, egfem_layout layout, const void* U, const void* W,
                             void* R, cudaStream_t s) {
   if (t->n_tiles == 0) return EGFEM_OK;
+  // dense-local-block kernel (egfem_dense.cu) for W = V stencils; EGFEM_BATCHED=csf forces
+  // the CSF tile kernel below
+  static const char* force = getenv("EGFEM_BATCHED");
+  if (dense_path_ok(t) && !(force && force[0] == 'c')) return launch_dense(t, batch, layout, U, W, R, s);
   const bool p0 = t->has_mesh && t->w_p0;
   const bool nm = layout == EGFEM_LAYOUT_NODE_MAJOR;
 #define EGFEM_B(S, NM)                                                                                           \
