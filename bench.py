@@ -42,6 +42,16 @@ def _peaks():
         return 6650.0, "fallback"
 
 
+def _fp64_peak():
+    """FP64 FMA peak: profiles/fp64_peak.json (tools/fp64_peak on this pool's B200) if present,
+    else 148 SMs x 64 DFMA/clk x 2 x 1.965 GHz."""
+    try:
+        with open(os.path.join(ROOT, "profiles", "fp64_peak.json")) as f:
+            return float(json.load(f)["fp64_fma_tflops"]), "measured (tools/fp64_peak)"
+    except Exception:
+        return 148 * 64 * 2 * 1.965e9 / 1e12, "derived (148 SM x 64 DFMA/clk x 1.965 GHz)"
+
+
 def _traffic(workload, kernel):
     """Per-launch DRAM bytes from the committed ncu --set full summary, if any."""
     p = os.path.join(ROOT, "profiles", "traffic.json")
@@ -273,7 +283,7 @@ def run_ours(args):
                            (" + NCCL u-halo" if world > 1 else ""),
                    "l2": "inputs larger than L2 (T stream 2.7 GB > 126 MB L2); no flush",
                    "parallelism": f"row-partition x{world}" if world > 1 else "single GPU"},
-        "roofline": {"bound": "hbm", "kernel": "k_rows<S,G,NCH,FREG,DO_R=1,NewtonP0> (egfem_apply_jacobian)",
+        "roofline": {"bound": "hbm", "kernel": "k_cell<S,D1,G,CPL,FREG,DO_R=1,NewtonP0> (egfem_apply_jacobian, cell-major P0 path)",
                      "achieved": achieved, "peak": peak, "peak_kind": peak_kind, "unit": "GB/s",
                      "frac": achieved / peak, "algorithmic_bytes": fused_bytes,
                      "traffic": _traffic(workload, "fused")},
@@ -329,15 +339,21 @@ def run_batched(args, eg, t, pr, dev, td, s, build_s, world, rank):
         ms = float(m.item())
     units = t.nnz * B * args.steps
     byts = t.nnz * (4 + s) + t.nnz_csr * 8 + (t.n_u + 1) * 8 + s * (2 * t.n_u * Bl + t.n_f * Bl)
+    flops = 2 * (t.nnz + t.nnz_csr) * Bl  # fiber-factored: per pair, an FMA per nonzero and per fiber
     per = ms / args.steps
     peak, kind = _peaks()
+    fpeak, fkind = _fp64_peak()
     out = {"metric": "tensor nonzero-pairs/s (batched action) and achieved HBM GB/s", "value": units / (ms * 1e-3),
            "unit": "nnz*pair/s", "n_gpus": world, "steps": args.steps, "warmup": args.warmup,
            "ms_per_step": per, "higher_is_better": True, "scaling": "weak", "vs_baseline": None,
            "dtype": args.dtype, "data": "synthetic (seeded, BASELINE.json recipe)",
            "config": {"workload": f"cfg5-{args.dtype}", "batch": B, "nnz": t.nnz, "parallelism": f"batch-shard x{world}"},
-           "roofline": {"bound": "hbm", "achieved": byts / (per * 1e-3) / 1e9, "peak": peak, "peak_kind": kind,
-                        "unit": "GB/s", "frac": byts / (per * 1e-3) / 1e9 / peak, "traffic": None},
+           "roofline": {"bound": "alu", "kernel": "k_dense<double,NODE_MAJOR> (egfem_apply_batched)",
+                        "achieved": flops / (per * 1e-3) / 1e12, "peak": fpeak, "peak_kind": fkind,
+                        "unit": "TFLOP/s", "frac": flops / (per * 1e-3) / 1e12 / fpeak,
+                        "algorithmic_flops": flops, "traffic": None},
+           "roofline_hbm": {"achieved": byts / (per * 1e-3) / 1e9, "peak": peak, "peak_kind": kind, "unit": "GB/s",
+                            "frac": byts / (per * 1e-3) / 1e9 / peak, "algorithmic_bytes": byts},
            "gpu_launches": int(eg.launch_count() - l0), "clocks": clk.summary(), "build_s": build_s}
     if rank == 0:
         print(json.dumps(out), flush=True)
