@@ -83,7 +83,7 @@ __device__ __forceinline__ float xadd(float a, float b) { return __fadd_rn(a, b)
 __device__ __forceinline__ double xfma(double a, double b, double c) { return __fma_rn(a, b, c); }
 __device__ __forceinline__ float xfma(float a, float b, float c) { return __fmaf_rn(a, b, c); }
 
-template <typename S, int D1, int G, int CPL>
+template <typename S, int D1, int G, int CPL, bool JT>
 struct CellSmem {
   static constexpr int CC = G * CPL;  // cells per row (max)
   static constexpr int CE = CC * D1;  // nonzeros per row (max)
@@ -94,7 +94,7 @@ struct CellSmem {
   static constexpr int st_b = (st_v + CE * (int)sizeof(S) + 32 + 15) & ~15;
   static constexpr int stage = (st_b + CE * 2 + 32 + 15) & ~15;
   static constexpr int o_t = 2 * stage;  // S[CE]: Jacobian terms at canonical positions
-  static constexpr int raw = (o_t + CE * (int)sizeof(S) + 15) & ~15;
+  static constexpr int raw = (o_t + (JT ? CE * (int)sizeof(S) : 0) + 15) & ~15;  // s_t only with a Jacobian
   // group stride = 16 (mod 128): the groups of a warp start on different bank quads, so
   // their same-offset accesses do not collide
   static constexpr int bytes = raw + ((16 - raw % 128) + 128) % 128;
@@ -187,8 +187,8 @@ __device__ __forceinline__ Meta meta(const CellArgs<S>& A, int64_t row) {
 }
 
 template <typename S, int D1, int G, int CPL, int FREG, bool DO_R, int JAC>
-__global__ void __launch_bounds__(256, JAC == kJacNewtonP0 ? 2 : 3) k_cell(const CellArgs<S> A) {
-  using L = CellSmem<S, D1, G, CPL>;
+__global__ void __launch_bounds__(256, (JAC == kJacNone || G >= 16) ? 3 : 2) k_cell(const CellArgs<S> A) {
+  using L = CellSmem<S, D1, G, CPL, JAC != kJacNone>;
   constexpr int GPB = 256 / G;
   constexpr bool kJ = JAC != kJacNone;
   constexpr bool kN = JAC == kJacNewtonP0;
@@ -208,15 +208,20 @@ __global__ void __launch_bounds__(256, JAC == kJacNewtonP0 ? 2 : 3) k_cell(const
   const int64_t wrow0 = (int64_t)blockIdx.x * GPB + (threadIdx.x >> 5) * (32 / G);
   if (wrow0 >= A.n_u) return;
 
-  // fiber lanes: lane f holds fiber f (+ G, + 2G, ...): u at its column and its canonical range
-  auto fibers = [&](const Meta& m, S* uj, int* fb) {
+  // fiber lanes: lane f holds fiber f (+ G, + 2G, ...): its column and canonical start (loaded
+  // two rows ahead) and u at its column (one row ahead), so no load waits on another in-row
+  auto fibers = [&](const Meta& m, int* fj, int* fb) {
 #pragma unroll
     for (int q = 0; q < FREG; ++q) {
       const int f = lane + q * G;
       const bool ok = f < (int)(m.f1 - m.f0);
-      uj[q] = (kU && ok) ? __ldg(A.u + __ldg(A.fib_j + m.f0 + f)) : S(0);
+      fj[q] = (kU && ok) ? __ldg(A.fib_j + m.f0 + f) : -1;
       fb[q] = ok ? (int)(__ldg(A.fib_nz + m.f0 + f) - m.e0) : 0;
     }
+  };
+  auto ucols = [&](const int* fj, S* uj) {
+#pragma unroll
+    for (int q = 0; q < FREG; ++q) uj[q] = (kU && fj[q] >= 0) ? __ldg(A.u + fj[q]) : S(0);
   };
   auto stage_in = [&](uint32_t dst, const Meta& m, int& sk, int& sv, int& sb) {
     const int n = (int)(m.e1 - m.e0);
@@ -227,12 +232,15 @@ __global__ void __launch_bounds__(256, JAC == kJacNewtonP0 ? 2 : 3) k_cell(const
 
   Meta cur = meta(A, row);
   Meta nxt = meta(A, row + NG);
+  Meta nn = meta(A, row + 2 * NG);
   int shk, shv, shb;
   stage_in(gs_s, cur, shk, shv, shb);
   commit();
   S uj_cur[FREG], uj_nxt[FREG];
-  int fb_cur[FREG], fb_nxt[FREG];
-  fibers(cur, uj_cur, fb_cur);
+  int fb_cur[FREG], fb_nxt[FREG], fj_cur[FREG], fj_nxt[FREG];
+  fibers(cur, fj_cur, fb_cur);
+  fibers(nxt, fj_nxt, fb_nxt);
+  ucols(fj_cur, uj_cur);
   int st = 0;
   for (int64_t wr = wrow0; wr < A.n_u; wr += NG, row += NG) {
     const int ne = (int)(cur.e1 - cur.e0);
@@ -242,8 +250,10 @@ __global__ void __launch_bounds__(256, JAC == kJacNewtonP0 ? 2 : 3) k_cell(const
     int nshk = 0, nshv = 0, nshb = 0;
     if (row + NG < A.n_u) stage_in(gs_s + (st ^ 1) * L::stage, nxt, nshk, nshv, nshb);
     commit();
-    fibers(nxt, uj_nxt, fb_nxt);
-    const Meta nn = meta(A, row + 2 * NG);
+    ucols(fj_nxt, uj_nxt);
+    int fj_nn[FREG], fb_nn[FREG];
+    fibers(nn, fj_nn, fb_nn);
+    const Meta n3 = meta(A, row + 3 * NG);
     wait_prev();
     __syncwarp();
     const unsigned char* cs = gs + st * L::stage;
@@ -401,6 +411,7 @@ __global__ void __launch_bounds__(256, JAC == kJacNewtonP0 ? 2 : 3) k_cell(const
     __syncwarp();  // stage st and s_t are free for reuse
     cur = nxt;
     nxt = nn;
+    nn = n3;
     shk = nshk;
     shv = nshv;
     shb = nshb;
@@ -408,6 +419,8 @@ __global__ void __launch_bounds__(256, JAC == kJacNewtonP0 ? 2 : 3) k_cell(const
     for (int q = 0; q < FREG; ++q) {
       uj_cur[q] = uj_nxt[q];
       fb_cur[q] = fb_nxt[q];
+      fb_nxt[q] = fb_nn[q];
+      fj_nxt[q] = fj_nn[q];
     }
     st ^= 1;
   }
@@ -445,7 +458,7 @@ int g_sm_count[64] = {0};
 
 template <typename S, int D1, int G, int CPL, int FREG, bool DO_R, int JAC>
 egfem_status run_cells(const egfem_tensor* t, const CellArgs<S>& A, cudaStream_t s) {
-  using L = CellSmem<S, D1, G, CPL>;
+  using L = CellSmem<S, D1, G, CPL, JAC != kJacNone>;
   auto fn = k_cell<S, D1, G, CPL, FREG, DO_R, JAC>;
   const int smem = L::bytes * (256 / G);
   if (smem > 48 * 1024) EGFEM_CUDA_TRY(cudaFuncSetAttribute(fn, cudaFuncAttributeMaxDynamicSharedMemorySize, smem));

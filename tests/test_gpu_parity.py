@@ -162,7 +162,7 @@ def test_cfg4_fp32_small(eg, orc, n):
 
 
 @pytest.mark.parametrize("layout", [0, 1])
-@pytest.mark.parametrize("B", [1, 8, 37])
+@pytest.mark.parametrize("B", [1, 8, 37, 64, 65, 130])
 def test_batched_small(eg, orc, layout, B):
     """A2 batched: R_p = T:(U_p ⊗ W_p), NODE_MAJOR and PAIR_MAJOR, B not a multiple of 32."""
     import torch
@@ -353,14 +353,15 @@ def test_partition_emulation_bitwise(eg, name, nranks):
     assert np.array_equal(np.concatenate(J_all), ref["J"])
 
 
-def test_tile_path(eg):
-    """The TMA-pipelined tile kernel (general path for rows > 256 nonzeros) matches the oracle."""
+@pytest.mark.parametrize("env", [{"EGFEM_PATH": "tile"}, {"EGFEM_PATH": "rows", "EGFEM_BATCHED": "csf"}])
+def test_kernel_paths(eg, env):
+    """The non-default kernels (TMA tile kernel, canonical-CSF row kernel for P0 W, CSF batched
+    kernel) match the oracle: they are the fallbacks for long rows / wide stencils."""
     import os
     import subprocess
     import sys
     here = os.path.dirname(os.path.abspath(__file__))
-    env = dict(os.environ, EGFEM_PATH="tile")
-    res = subprocess.run([sys.executable, os.path.join(here, "tile_path_check.py")], env=env,
+    res = subprocess.run([sys.executable, os.path.join(here, "path_check.py")], env=dict(os.environ, **env),
                          capture_output=True, text=True, timeout=600)
     assert res.returncode == 0, res.stdout + res.stderr
-    assert "tile path ok" in res.stdout
+    assert "path ok" in res.stdout
