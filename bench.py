@@ -175,7 +175,7 @@ def run_ours(args):
         return run_batched(args, eg, t, pr, dev, td, s, build_s, world, rank)
     u = torch.tensor(u_np, dtype=td, device=dev)
     w = torch.empty(t.n_f, dtype=td, device=dev)
-    gp = pr.interp == I.INTERP_GRADPOW_P0
+    gp = pr.W.family == I.P0 and pr.interp in (I.INTERP_GRADPOW_P0, I.INTERP_MINSURF_P0, I.INTERP_RECIPROCAL)
     chain = torch.empty(t.n_f * (pr.mesh.dim + 1), dtype=td, device=dev) if gp else None
     r = torch.empty(t.n_u, dtype=td, device=dev)
     J = torch.empty(t.nnz_csr, dtype=td, device=dev)
@@ -412,7 +412,7 @@ def main():
     ap.add_argument("--steps", type=int, default=50)
     ap.add_argument("--warmup", type=int, default=5)
     ap.add_argument("--impl", default="ours", choices=["ours", "reference"])
-    ap.add_argument("--config", default="cfg4", choices=list(I.CONFIG_NAMES))
+    ap.add_argument("--config", default="cfg4", choices=list(I.CONFIG_NAMES) + list(I.EXTRA_NAMES))
     ap.add_argument("--dtype", default="f64", choices=["f64", "f32"])
     ap.add_argument("--batch", type=int, default=None)
     ap.add_argument("--no-cpu-baseline", action="store_true")

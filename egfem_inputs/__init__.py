@@ -26,6 +26,7 @@ P0, P1, P2 = 0, 1, 2
 FORM_CONV_K, FORM_CONV_J, FORM_PLAP, FORM_MASS3, FORM_CONV_I = 0, 1, 2, 3, 4
 # Interp kinds (include/egfem.h egfem_interp_kind).
 INTERP_IDENTITY, INTERP_SQUARE, INTERP_GRADPOW_P0, INTERP_P1_TO_P2_SQUARE = 0, 1, 2, 3
+INTERP_MINSURF_P0, INTERP_RECIPROCAL = 4, 5
 # Jacobian modes.
 JAC_PICARD, JAC_NEWTON = 0, 1
 
@@ -208,11 +209,23 @@ def _u_cfg5(x, batch):
     return U
 
 
+def _u_paper_bc(x, seed):
+    """x1 x2 (x1 + x2) (the exact solution of PAPER.md §5.4 L521 / §5.6) + 0.01·N(0,1)."""
+    rng = np.random.default_rng(seed)
+    return x[:, 0] * x[:, 1] * (x[:, 0] + x[:, 1]) + 0.01 * rng.standard_normal(x.shape[0])
+
+
 # Full BASELINE.json sizes; "small" variants use the same recipe at a size the
 # oracle finishes in seconds but that still spans many kernel tiles.
-FULL_N = {"cfg1": 256, "cfg2": 512, "cfg3": 1024, "cfg4": 128, "cfg5": 256}
-SMALL_N = {"cfg1": 256, "cfg2": 40, "cfg3": 48, "cfg4": 10, "cfg5": 24}
+FULL_N = {"cfg1": 256, "cfg2": 512, "cfg3": 1024, "cfg4": 128, "cfg5": 256,
+          "minsurf2d": 1024, "minsurf3d": 64, "biochem_p1": 512, "biochem_p0": 512}
+SMALL_N = {"cfg1": 256, "cfg2": 40, "cfg3": 48, "cfg4": 10, "cfg5": 24,
+           "minsurf2d": 40, "minsurf3d": 8, "biochem_p1": 32, "biochem_p0": 32}
 CONFIG_NAMES = ("cfg1", "cfg2", "cfg3", "cfg4", "cfg5")
+# SURVEY §8(f) F1 pointwise kinds (not BASELINE configs): minimal surface a = (1+|∇u|²)^{-1/2}
+# with P0 W (PAPER.md §5.6, L596–611) and the biochemical c̃ = σ/(k+u), σ = 1 = k, on the
+# trilinear mass tensor M_c̃ with W = P1 (GFEM) or P0 (PAPER.md §5.4, L516–559).
+EXTRA_NAMES = ("minsurf2d", "minsurf3d", "biochem_p1", "biochem_p0")
 
 
 def make_problem(name: str, n: Optional[int] = None, batch: Optional[int] = None) -> Problem:
@@ -245,6 +258,20 @@ def make_problem(name: str, n: Optional[int] = None, batch: Optional[int] = None
         return Problem(name, mesh, V, V, FORM_CONV_J, INTERP_IDENTITY, 0.0, ("f64",),
                        _u_cfg5(V.dof_coords, batch), batch=batch,
                        description=f"batched 2D Burgers P2, {n}x{n}, B={batch}")
+    if name == "minsurf2d":
+        mesh = mesh_square(n)
+        return Problem(name, mesh, space_p1(mesh), space_p0(mesh), FORM_PLAP, INTERP_MINSURF_P0, 0.0,
+                       ("f64",), _u_paper_bc(mesh.coords, 6), description=f"2D minimal surface P1/P0, {n}x{n}")
+    if name == "minsurf3d":
+        mesh = mesh_cube(n)
+        return Problem(name, mesh, space_p1(mesh), space_p0(mesh), FORM_PLAP, INTERP_MINSURF_P0, 0.0,
+                       ("f64",), _u_paper_bc(mesh.coords, 7), description=f"3D minimal surface P1/P0, {n}^3x6")
+    if name in ("biochem_p1", "biochem_p0"):
+        mesh = mesh_square(n)
+        V = space_p1(mesh)
+        W = V if name == "biochem_p1" else space_p0(mesh)
+        return Problem(name, mesh, V, W, FORM_MASS3, INTERP_RECIPROCAL, 1.0, ("f64",),
+                       _u_paper_bc(mesh.coords, 8), description=f"2D biochemical sigma/(k+u), W={name[-2:]}, {n}x{n}")
     raise KeyError(name)
 
 

@@ -74,13 +74,19 @@ typedef enum {
 /* Pointwise nonlinearities at the W-DOFs:
  *   IDENTITY        : w = u                     (W = V, GFEM, Π_u = I, L338)
  *   SQUARE          : w_k = u_k²                (W = V, L336 with Π = I)
- *   GRADPOW_P0      : w_K = ‖∇u_h|_K‖^{p−2}     (V = P1, W = P0, L574/L582)
- *   P1_TO_P2_SQUARE : w = (Π_u u) ⊙ (Π_u u)     (V = P1, W = P2, Case 1, L336–338) */
+ *   GRADPOW_P0      : w_K = ‖∇u_h|_K‖^{p−2}     (V = P1, W = P0, p-Laplace, L574/L582)
+ *   P1_TO_P2_SQUARE : w = (Π_u u) ⊙ (Π_u u)     (V = P1, W = P2, Case 1, L336–338)
+ *   MINSURF_P0      : w_K = (1 + ‖∇u_h|_K‖²)^{−1/2}  (V = P1, W = P0, minimal surface a(·), L605–611)
+ *   RECIPROCAL      : w_k = 1 / (p + u_h(x_k))  (the biochemical c̃ = σ/(k+u) with σ = 1, k = p,
+ *                     L520–535; W = V: at the nodes; W = P0 with V = P1: at the centroid,
+ *                     u_h(x_K) = mean of the cell's vertex values) */
 typedef enum {
   EGFEM_INTERP_IDENTITY = 0,
   EGFEM_INTERP_SQUARE = 1,
   EGFEM_INTERP_GRADPOW_P0 = 2,
-  EGFEM_INTERP_P1_TO_P2_SQUARE = 3
+  EGFEM_INTERP_P1_TO_P2_SQUARE = 3,
+  EGFEM_INTERP_MINSURF_P0 = 4,
+  EGFEM_INTERP_RECIPROCAL = 5
 } egfem_interp_kind;
 
 /* PICARD: A = T·w.  NEWTON: J = T·w + (T·₂u)·D_u w, the Schur
@@ -167,10 +173,11 @@ egfem_status egfem_tensor_export(const egfem_tensor* t, int64_t* t_row_ptr, int3
 
 /* ---------------------------------------------------------------- per iteration
  * (1) w = f(Π_u u, Π_∇u ·₂ u) at every W-DOF.
- * u: device [N_u]; w: device [N_f].  chain (nullable, GRADPOW_P0 only): device
- * [N_f*(d+1)], chain[K*(d+1)+m] = ∂w_K/∂u_{v_m(K)} (the pointwise D_u w of
- * PAPER.md L292), consumed by egfem_jacobian NEWTON.  p > 1 required for
- * GRADPOW_P0 (p ignored otherwise).  At ∇u_h|_K = 0 and p < 4 the derivative is
+ * u: device [N_u]; w: device [N_f].  chain (nullable; P0-W kinds only: GRADPOW_P0,
+ * MINSURF_P0, RECIPROCAL with W = P0): device [N_f*(d+1)], chain[K*(d+1)+m] =
+ * ∂w_K/∂u_{v_m(K)} (the pointwise D_u w of PAPER.md L292), consumed by egfem_jacobian
+ * NEWTON.  p > 1 required for GRADPOW_P0; p is k of RECIPROCAL (any value; p + u = 0
+ * gives ±inf); p ignored otherwise.  At ∇u_h|_K = 0 and p < 4 the GRADPOW derivative is
  * taken as 0 (reading C11). */
 egfem_status egfem_interp(const egfem_tensor* t, egfem_interp_kind kind, double p, const void* u,
                           void* w, void* chain, egfem_stream_t stream);
@@ -187,11 +194,13 @@ egfem_status egfem_apply_batched(const egfem_tensor* t, int32_t batch, egfem_lay
                                  const void* U, const void* W, void* R, egfem_stream_t stream);
 
 /* (3) Jacobian / Picard matrix values in the CSR pattern:
- *   PICARD            : A_ij = Σ_k T_ijk w_k
- *   NEWTON IDENTITY   : J = T·w + T·₂u                (∂w_k/∂u_m = δ_km)
- *   NEWTON SQUARE     : J = T·w + (T·₂u)·diag(2u)
- *   NEWTON GRADPOW_P0 : J = T·w + (T·₂u)·D_u w, D_u w from `chain` (egfem_interp)
- * u: [N_u] (NEWTON), w: [N_f], chain: [N_f*(d+1)] (GRADPOW NEWTON), csr_vals: [nnz_csr].
+ *   PICARD              : A_ij = Σ_k T_ijk w_k
+ *   NEWTON IDENTITY     : J = T·w + T·₂u                (∂w_k/∂u_m = δ_km)
+ *   NEWTON SQUARE       : J = T·w + (T·₂u)·diag(2u)
+ *   NEWTON RECIPROCAL   : J = T·w + (T·₂u)·diag(−1/(p+u)²)   (W = V)
+ *   NEWTON P0-W kinds   : J = T·w + (T·₂u)·D_u w, D_u w from `chain` (egfem_interp):
+ *                         GRADPOW_P0, MINSURF_P0, RECIPROCAL with W = P0
+ * u: [N_u] (NEWTON), w: [N_f], chain: [N_f*(d+1)] (P0-W NEWTON), csr_vals: [nnz_csr].
  * NEWTON with P1_TO_P2_SQUARE returns UNSUPPORTED. */
 egfem_status egfem_jacobian(const egfem_tensor* t, egfem_jac_mode mode, egfem_interp_kind kind, double p,
                             const void* u, const void* w, const void* chain, void* csr_vals,

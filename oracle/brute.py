@@ -226,6 +226,43 @@ def sga_plap(mesh, u, p):
     return r
 
 
+def sga_minsurf(mesh, u):
+    """SGA minimal-surface residual K(a,u)u, a = (1 + ‖∇u_h‖²)^{-1/2}: with P1
+    u_h the coefficient is constant on each cell, so this is exact (and equals EGFEM-P0, L616)."""
+    r = np.zeros(mesh.n_vertices)
+    for K in range(mesh.n_cells):
+        I = mesh.cells[K]
+        G, vol = geometry(mesh.coords[I])
+        g = G.T @ u[I]
+        r[I] += vol * (G @ g) / np.sqrt(1.0 + g @ g)
+    return r
+
+
+def tensor_free_reciprocal(mesh, u, k, w_family):
+    """r_i = ∫ φ_i u_h c̃_h with c̃ = 1/(k + u) interpolated onto W, by exact
+    polynomial integration, no tensor: W = P1 → c̃_h = Σ_v c̃(u_v) φ_v (GFEM); W = P0 → c̃_h|_K =
+    c̃(u_h(centroid of K))."""
+    d = mesh.dim
+    r = np.zeros(mesh.n_vertices)
+    phis = local_basis(P1, d)
+    for K in range(mesh.n_cells):
+        I = mesh.cells[K]
+        G, vol = geometry(mesh.coords[I])
+        uh = {}
+        for a in range(d + 1):
+            uh = padd(uh, pscale(phis[a], u[I[a]]))
+        if w_family == "P1":
+            ch = {}
+            for a in range(d + 1):
+                ch = padd(ch, pscale(phis[a], 1.0 / (k + u[I[a]])))
+        else:
+            ch = pscale(mono(d), 1.0 / (k + peval(uh, [1.0 / (d + 1)] * (d + 1))))
+        f = pmul(uh, ch)
+        for a in range(d + 1):
+            r[I[a]] += pint(pmul(phis[a], f), vol, d)
+    return r
+
+
 def sga_cubic_mass(mesh, u):
     """r_i = ∫ φ_i u_h³ dx exactly (Case-1 target, PAPER.md L338 / L456)."""
     d = mesh.dim

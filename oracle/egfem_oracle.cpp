@@ -33,7 +33,7 @@ namespace {
 
 enum { OF_P0 = 0, OF_P1 = 1, OF_P2 = 2 };
 enum { OFORM_CONV_K = 0, OFORM_CONV_J = 1, OFORM_PLAP = 2, OFORM_MASS3 = 3, OFORM_CONV_I = 4 };
-enum { OK_IDENTITY = 0, OK_SQUARE = 1, OK_GRADPOW_P0 = 2, OK_P1_TO_P2_SQUARE = 3 };
+enum { OK_IDENTITY = 0, OK_SQUARE = 1, OK_GRADPOW_P0 = 2, OK_P1_TO_P2_SQUARE = 3, OK_MINSURF_P0 = 4, OK_RECIPROCAL = 5 };
 enum { OJ_PICARD = 0, OJ_NEWTON = 1 };
 
 // Slot operators: which functional of a basis function enters a slot.
@@ -443,12 +443,43 @@ int oracle_export(const void* h, int64_t* t_row_ptr, int32_t* t_j, int32_t* t_k,
 //   SQUARE:          f(u) = u², W = V  (L336 with Π = identity)
 //   GRADPOW_P0:      f(∇u) = ‖∇u‖^{p-2} at the P0 DOF of each cell (L574, L582)
 //   P1_TO_P2_SQUARE: f(u) = u² at the P2 DOFs, w = (Π_u u) ⊙ (Π_u u) (L336)
+//   MINSURF_P0:      a(∇u) = (1 + ‖∇u‖²)^{-1/2} at the P0 DOF of each cell (minimal surface, L605, L609)
+//   RECIPROCAL:      c̃(u) = σ/(k + u) with σ = 1, k = p (biochemical, L520–535) at the W-DOFs:
+//                    the nodes (W = V) or the cell centroid (W = P0, V = P1: u_h(x_K) = Σ_a u_a λ_a(x_K))
 int oracle_interp(const void* h, int kind, double p, const double* u, double* w) {
   const OTensor* T = static_cast<const OTensor*>(h);
   const int d = T->dim;
   if (kind == OK_IDENTITY || kind == OK_SQUARE) {
     if (T->W.n_dofs != T->V.n_dofs) return -1;
     for (int64_t k = 0; k < T->W.n_dofs; ++k) w[k] = (kind == OK_IDENTITY) ? u[k] : u[k] * u[k];
+    return 0;
+  }
+  if (kind == OK_RECIPROCAL) {
+    if (T->W.family == T->V.family && T->W.n_dofs == T->V.n_dofs) {
+      for (int64_t k = 0; k < T->W.n_dofs; ++k) w[k] = 1.0 / (p + u[k]);
+      return 0;
+    }
+    if (T->W.family != OF_P0 || T->V.family != OF_P1) return -2;
+    for (int64_t K = 0; K < T->n_cells; ++K) {
+      const int32_t* I = &T->V.cell_dofs[K * T->V.n_loc];
+      double uc = 0;  // u_h at the centroid: λ_a = 1/(d+1)
+      for (int a = 0; a <= d; ++a) uc += u[I[a]] / (d + 1);
+      w[T->W.cell_dofs[K]] = 1.0 / (p + uc);
+    }
+    return 0;
+  }
+  if (kind == OK_MINSURF_P0) {
+    if (T->W.family != OF_P0 || T->V.family != OF_P1) return -2;
+    for (int64_t K = 0; K < T->n_cells; ++K) {
+      Geo g = geometry(*T, K);
+      const int32_t* I = &T->V.cell_dofs[K * T->V.n_loc];
+      double gu[3] = {0, 0, 0};  // (Π_∇u ·₂ u) at the cell's DOF
+      for (int a = 0; a <= d; ++a)
+        for (int x = 0; x < d; ++x) gu[x] += u[I[a]] * g.grad[a][x];
+      double gg = 0;
+      for (int x = 0; x < d; ++x) gg += gu[x] * gu[x];
+      w[T->W.cell_dofs[K]] = 1.0 / std::sqrt(1.0 + gg);
+    }
     return 0;
   }
   if (kind == OK_GRADPOW_P0) {
@@ -535,6 +566,40 @@ static int build_Duw(const OTensor* T, int kind, double p, const double* u, std:
         for (int x = 0; x < d; ++x) gdot += gu[x] * g.grad[a][x];
         D.push_back({(int64_t)T->W.cell_dofs[K], I[a], fac * gdot});
       }
+    }
+    return 0;
+  }
+  if (kind == OK_MINSURF_P0) {
+    // a_K = (1 + |g|²)^{-1/2}, g = Σ_a u_a ∇λ_a  ⇒  ∂a_K/∂u_a = −(1 + |g|²)^{-3/2} (g·∇λ_a)
+    for (int64_t K = 0; K < T->n_cells; ++K) {
+      Geo g = geometry(*T, K);
+      const int32_t* I = &T->V.cell_dofs[K * T->V.n_loc];
+      double gu[3] = {0, 0, 0};
+      for (int a = 0; a <= d; ++a)
+        for (int x = 0; x < d; ++x) gu[x] += u[I[a]] * g.grad[a][x];
+      double gg = 0;
+      for (int x = 0; x < d; ++x) gg += gu[x] * gu[x];
+      const double fac = -std::pow(1.0 + gg, -1.5);
+      for (int a = 0; a <= d; ++a) {
+        double gdot = 0;
+        for (int x = 0; x < d; ++x) gdot += gu[x] * g.grad[a][x];
+        D.push_back({(int64_t)T->W.cell_dofs[K], I[a], fac * gdot});
+      }
+    }
+    return 0;
+  }
+  if (kind == OK_RECIPROCAL) {
+    // c̃ = 1/(k + u_h(x))  ⇒  ∂c̃/∂u_a = −λ_a(x)/(k + u_h(x))²  (x the W-DOF; λ_a = δ at nodes, 1/(d+1) at centroids)
+    if (T->W.family == T->V.family && T->W.n_dofs == T->V.n_dofs) {
+      for (int64_t k = 0; k < T->W.n_dofs; ++k) D.push_back({k, (int32_t)k, -1.0 / ((p + u[k]) * (p + u[k]))});
+      return 0;
+    }
+    for (int64_t K = 0; K < T->n_cells; ++K) {
+      const int32_t* I = &T->V.cell_dofs[K * T->V.n_loc];
+      double uc = 0;
+      for (int a = 0; a <= d; ++a) uc += u[I[a]] / (d + 1);
+      for (int a = 0; a <= d; ++a)
+        D.push_back({(int64_t)T->W.cell_dofs[K], I[a], -1.0 / ((d + 1) * (p + uc) * (p + uc))});
     }
     return 0;
   }

@@ -28,6 +28,7 @@ F64, F32 = 0, 1
 P0, P1, P2 = 0, 1, 2
 FORM_CONV_K, FORM_CONV_J, FORM_PLAP, FORM_MASS3, FORM_CONV_I = 0, 1, 2, 3, 4
 INTERP_IDENTITY, INTERP_SQUARE, INTERP_GRADPOW_P0, INTERP_P1_TO_P2_SQUARE = 0, 1, 2, 3
+INTERP_MINSURF_P0, INTERP_RECIPROCAL = 4, 5
 JAC_PICARD, JAC_NEWTON = 0, 1
 LAYOUT_NODE_MAJOR, LAYOUT_PAIR_MAJOR = 0, 1
 STATUS = {0: "EGFEM_OK", 1: "EGFEM_ERR_INVALID_ARGUMENT", 2: "EGFEM_ERR_DIMENSION_MISMATCH",

@@ -1,6 +1,7 @@
 // C ABI of libegfem.so: validation, handle lifetime, dispatch, multi-GPU
 // partitioning.  See include/egfem.h for the contract of every entry point.
 #include <algorithm>
+#include <cmath>
 #include <atomic>
 #include <cstring>
 #include <numeric>
@@ -278,7 +279,7 @@ egfem_status egfem_tensor_export(const egfem_tensor* t, int64_t* t_row_ptr, int3
 egfem_status egfem_interp(const egfem_tensor* t, egfem_interp_kind kind, double p, const void* u, void* w,
                           void* chain, egfem_stream_t stream) {
   if (!t) return fail(EGFEM_ERR_INVALID_ARGUMENT, "tensor is NULL");
-  if (kind < EGFEM_INTERP_IDENTITY || kind > EGFEM_INTERP_P1_TO_P2_SQUARE)
+  if (kind < EGFEM_INTERP_IDENTITY || kind > EGFEM_INTERP_RECIPROCAL)
     return fail(EGFEM_ERR_INVALID_ARGUMENT, "bad interp kind");
   egfem_status st;
   if ((st = check_dev_ptr(t, u, "u", true)) || (st = check_dev_ptr(t, w, "w", true)) ||
@@ -294,6 +295,18 @@ egfem_status egfem_interp(const egfem_tensor* t, egfem_interp_kind kind, double 
       if (!t->has_mesh || !t->w_p0 || t->vfam != EGFEM_P1)
         return fail(EGFEM_ERR_UNSUPPORTED, "GRADPOW_P0 needs V = P1, W = P0 and a mesh");
       if (!(p > 1.0)) return fail(EGFEM_ERR_INVALID_ARGUMENT, "GRADPOW_P0 needs p > 1");
+      break;
+    case EGFEM_INTERP_MINSURF_P0:
+      if (!t->has_mesh || !t->w_p0 || t->vfam != EGFEM_P1)
+        return fail(EGFEM_ERR_UNSUPPORTED, "MINSURF_P0 needs V = P1, W = P0 and a mesh");
+      break;
+    case EGFEM_INTERP_RECIPROCAL:
+      if (t->w_is_v) {
+        if (chain) return fail(EGFEM_ERR_INVALID_ARGUMENT, "chain is only produced for P0 W");
+      } else if (!t->has_mesh || !t->w_p0 || t->vfam != EGFEM_P1) {
+        return fail(EGFEM_ERR_UNSUPPORTED, "RECIPROCAL needs W = V, or V = P1 and W = P0 with a mesh");
+      }
+      if (!std::isfinite(p)) return fail(EGFEM_ERR_INVALID_ARGUMENT, "RECIPROCAL needs a finite p (= k)");
       break;
     default:
       if (!t->has_mesh || t->vfam != EGFEM_P1 || t->wfam != EGFEM_P2 || t->dim != 2)
@@ -311,7 +324,7 @@ egfem_status egfem_apply(const egfem_tensor* t, const void* u, const void* w, vo
       (st = check_dev_ptr(t, r, "r", true)))
     return st;
   DeviceGuard g(t->device);
-  return launch_tile(t, true, 0, EGFEM_INTERP_IDENTITY, u, w, nullptr, r, nullptr, (cudaStream_t)stream);
+  return launch_tile(t, true, 0, EGFEM_INTERP_IDENTITY, 0.0, u, w, nullptr, r, nullptr, (cudaStream_t)stream);
 }
 
 egfem_status egfem_apply_batched(const egfem_tensor* t, int32_t batch, egfem_layout layout, const void* U,
@@ -348,9 +361,23 @@ static egfem_status jac_mode_code(const egfem_tensor* t, egfem_jac_mode mode, eg
       *code = 2;
       return EGFEM_OK;
     case EGFEM_INTERP_GRADPOW_P0:
+    case EGFEM_INTERP_MINSURF_P0:
       if (!t->has_mesh || !t->w_p0 || t->vfam != EGFEM_P1)
-        return fail(EGFEM_ERR_UNSUPPORTED, "GRADPOW_P0 Newton needs V = P1, W = P0");
-      if (!(p > 1.0)) return fail(EGFEM_ERR_INVALID_ARGUMENT, "GRADPOW_P0 needs p > 1");
+        return fail(EGFEM_ERR_UNSUPPORTED, "P0-W Newton needs V = P1, W = P0");
+      if (kind == EGFEM_INTERP_GRADPOW_P0 && !(p > 1.0))
+        return fail(EGFEM_ERR_INVALID_ARGUMENT, "GRADPOW_P0 needs p > 1");
+      if ((st = check_dev_ptr(t, chain, "chain", true))) return st;
+      *code = 3;
+      return EGFEM_OK;
+    case EGFEM_INTERP_RECIPROCAL:
+      if (t->w_is_v) {
+        if (!t->newton_wv_ok)
+          return fail(EGFEM_ERR_UNSUPPORTED, "T·₂u has entries outside the CSR pattern (from_coo tensor)");
+        *code = 2;
+        return EGFEM_OK;
+      }
+      if (!t->has_mesh || !t->w_p0 || t->vfam != EGFEM_P1)
+        return fail(EGFEM_ERR_UNSUPPORTED, "RECIPROCAL Newton needs W = V, or V = P1 and W = P0");
       if ((st = check_dev_ptr(t, chain, "chain", true))) return st;
       *code = 3;
       return EGFEM_OK;
@@ -369,7 +396,7 @@ egfem_status egfem_jacobian(const egfem_tensor* t, egfem_jac_mode mode, egfem_in
   int code = 0;
   if ((st = jac_mode_code(t, mode, kind, p, u, chain, &code))) return st;
   DeviceGuard g(t->device);
-  return launch_tile(t, false, code, kind, u, w, chain, nullptr, csr_vals, (cudaStream_t)stream);
+  return launch_tile(t, false, code, kind, p, u, w, chain, nullptr, csr_vals, (cudaStream_t)stream);
 }
 
 egfem_status egfem_apply_jacobian(const egfem_tensor* t, egfem_jac_mode mode, egfem_interp_kind kind, double p,
@@ -383,7 +410,7 @@ egfem_status egfem_apply_jacobian(const egfem_tensor* t, egfem_jac_mode mode, eg
   int code = 0;
   if ((st = jac_mode_code(t, mode, kind, p, u, chain, &code))) return st;
   DeviceGuard g(t->device);
-  return launch_tile(t, true, code, kind, u, w, chain, r, csr_vals, (cudaStream_t)stream);
+  return launch_tile(t, true, code, kind, p, u, w, chain, r, csr_vals, (cudaStream_t)stream);
 }
 
 egfem_status egfem_halo_pack(const egfem_tensor* local, const int32_t* d_idx, int64_t n, const void* u_local,

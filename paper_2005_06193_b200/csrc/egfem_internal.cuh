@@ -112,9 +112,9 @@ cudaError_t dmalloc_padded(void** p, size_t bytes);
 // compute kernels (egfem_kernels.cu)
 egfem_status launch_interp(const egfem_tensor* t, egfem_interp_kind kind, double p, const void* u, void* w,
                            void* chain, cudaStream_t s);
-egfem_status launch_tile(const egfem_tensor* t, bool do_r, int jac, egfem_interp_kind kind, const void* u,
+egfem_status launch_tile(const egfem_tensor* t, bool do_r, int jac, egfem_interp_kind kind, double p, const void* u,
                          const void* w, const void* chain, void* r, void* csr_vals, cudaStream_t s);
-egfem_status launch_rows(const egfem_tensor* t, bool do_r, int jac, egfem_interp_kind kind, const void* u,
+egfem_status launch_rows(const egfem_tensor* t, bool do_r, int jac, egfem_interp_kind kind, double p, const void* u,
                          const void* w, const void* chain, void* r, void* csr_vals, cudaStream_t s);
 bool rows_path_ok(const egfem_tensor* t, int jac);
 egfem_status make_wv_aux(egfem_tensor* t);

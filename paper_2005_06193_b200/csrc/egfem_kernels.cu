@@ -33,12 +33,12 @@ __device__ __forceinline__ S ld_ro(const S* p) {
 
 // ------------------------------------------------------------------ interp
 template <typename S>
-__global__ void k_interp_copy(const S* __restrict__ u, S* __restrict__ w, int64_t n, bool square) {
+__global__ void k_interp_copy(const S* __restrict__ u, S* __restrict__ w, int64_t n, int mode, double pk) {
   int64_t i = (int64_t)blockIdx.x * blockDim.x + threadIdx.x;
   const int64_t stride = (int64_t)gridDim.x * blockDim.x;
   for (; i < n; i += stride) {
     S x = u[i];
-    w[i] = square ? x * x : x;
+    w[i] = mode == 0 ? x : (mode == 1 ? x * x : S(1) / (S(pk) + x));  // IDENTITY, SQUARE, RECIPROCAL
   }
 }
 
@@ -69,7 +69,8 @@ __device__ __forceinline__ CellIdx<D> load_cell(const int32_t* __restrict__ t, i
 template <typename S, int D, bool SAME, bool IOTA>
 __global__ void __launch_bounds__(128) k_interp_gradpow(const double* __restrict__ coords, const int32_t* __restrict__ cells,
                                  const int32_t* __restrict__ vdofs, const int32_t* __restrict__ wdofs, int64_t n_cells,
-                                 const S* __restrict__ u, S* __restrict__ w, S* __restrict__ chain, double p) {
+                                 const S* __restrict__ u, S* __restrict__ w, S* __restrict__ chain, double p,
+                                 bool minsurf) {
   int64_t c = (int64_t)blockIdx.x * blockDim.x + threadIdx.x;
   if (c >= n_cells) return;
   const CellIdx<D> cv = load_cell<D>(cells, c);
@@ -144,7 +145,10 @@ __global__ void __launch_bounds__(128) k_interp_gradpow(const double* __restrict
 #pragma unroll
   for (int q = 0; q < D; ++q) gg += gu[q] * gu[q];
   double wk, fac;
-  if (p == 4.0) {
+  if (minsurf) {  // a = (1 + ‖g‖²)^{−1/2}, ∂a/∂u_m = −(1 + ‖g‖²)^{−3/2} g·∇λ_m
+    wk = 1.0 / sqrt(1.0 + gg);
+    fac = -(wk * wk * wk);
+  } else if (p == 4.0) {
     wk = gg;
     fac = 2.0;
   } else if (p == 3.0) {
@@ -179,6 +183,25 @@ __global__ void __launch_bounds__(128) k_interp_gradpow(const double* __restrict
 #pragma unroll
       for (int a = 0; a <= D; ++a) chain[K * (D + 1) + a] = dm[a];
     }
+  }
+}
+
+// RECIPROCAL with W = P0 (V = P1): w_K = 1/(k + u_h(x_K)), u_h(x_K) = mean of the vertex values
+// (λ_a = 1/(d+1) at the centroid), chain[K][m] = ∂w_K/∂u_{v_m} = −w_K²/(d+1).
+template <typename S>
+__global__ void k_interp_recip_p0(const int32_t* __restrict__ vdofs, const int32_t* __restrict__ wdofs,
+                                  int64_t n_cells, int d1, const S* __restrict__ u, S* __restrict__ w,
+                                  S* __restrict__ chain, double pk) {
+  const int64_t c = (int64_t)blockIdx.x * blockDim.x + threadIdx.x;
+  if (c >= n_cells) return;
+  double s = 0.0;
+  for (int a = 0; a < d1; ++a) s += (double)__ldg(u + vdofs[c * d1 + a]);
+  const double wk = 1.0 / (pk + s / d1);
+  const int64_t K = wdofs[c];
+  w[K] = (S)wk;
+  if (chain) {
+    const S dm = (S)(-(wk * wk) / d1);
+    for (int a = 0; a < d1; ++a) chain[K * d1 + a] = dm;
   }
 }
 
@@ -225,7 +248,8 @@ struct TileArgs {
   S* r;
   S* csr;
   int d1;       // d+1 (GRADPOW chain stride)
-  bool square;  // SQUARE Newton factor 2u_k
+  int dmode;    // W = V Newton factor ∂w_m/∂u_m: 0 → 1, 1 → 2u_m (SQUARE), 2 → −1/(pk+u_m)² (RECIPROCAL)
+  double pk;
   uint32_t kmask;  // kKMask for P0 W (loc bits), ~0 otherwise
 };
 
@@ -497,7 +521,13 @@ __global__ void __launch_bounds__(kThreads) k_tile(const TileArgs<S> A) {
             for (int y = ya; y < yb; ++y)
               if ((v.k[y] & A.kmask) == m) acc += v.val[y] * uj;
           }
-          const S cm = A.square ? S(2) * ld_ro(A.u + m) : S(1);
+          const S um = A.dmode ? ld_ro(A.u + m) : S(0);
+          S cm = S(1);
+          if (A.dmode == 1) cm = S(2) * um;
+          if (A.dmode == 2) {
+            const S iv = S(1) / (S(A.pk) + um);
+            cm = -(iv * iv);
+          }
           A.csr[g.f0 + x] = areg[c] + cm * acc;
         }
       }
@@ -553,7 +583,7 @@ egfem_status run_tile(const egfem_tensor* t, const TileArgs<S>& A, cudaStream_t 
 }
 
 template <typename S>
-egfem_status tile_dispatch(const egfem_tensor* t, bool do_r, int jac, egfem_interp_kind kind, const void* u,
+egfem_status tile_dispatch(const egfem_tensor* t, bool do_r, int jac, egfem_interp_kind kind, double p, const void* u,
                            const void* w, const void* chain, void* r, void* csr, cudaStream_t s) {
   TileArgs<S> A;
   A.tile_row = t->tile_row;
@@ -572,7 +602,8 @@ egfem_status tile_dispatch(const egfem_tensor* t, bool do_r, int jac, egfem_inte
   A.r = static_cast<S*>(r);
   A.csr = static_cast<S*>(csr);
   A.d1 = t->dim + 1;
-  A.square = (kind == EGFEM_INTERP_SQUARE);
+  A.dmode = kind == EGFEM_INTERP_SQUARE ? 1 : (kind == EGFEM_INTERP_RECIPROCAL ? 2 : 0);
+  A.pk = p;
   A.kmask = t->kmask();
   if (do_r) {
     switch (jac) {
@@ -665,20 +696,33 @@ __global__ void k_halo(const int32_t* __restrict__ idx, int64_t n, const S* __re
 egfem_status launch_interp(const egfem_tensor* t, egfem_interp_kind kind, double p, const void* u, void* w,
                            void* chain, cudaStream_t s) {
   const bool f64 = t->dtype == EGFEM_F64;
-  if (kind == EGFEM_INTERP_IDENTITY || kind == EGFEM_INTERP_SQUARE) {
+  if (kind == EGFEM_INTERP_IDENTITY || kind == EGFEM_INTERP_SQUARE ||
+      (kind == EGFEM_INTERP_RECIPROCAL && t->w_is_v)) {
     const int64_t n = t->n_f;
     const int grid = std::max(1, std::min(nblk(n), 148 * 16));
+    const int mode = kind == EGFEM_INTERP_IDENTITY ? 0 : (kind == EGFEM_INTERP_SQUARE ? 1 : 2);
     if (f64)
-      k_interp_copy<double><<<grid, 256, 0, s>>>((const double*)u, (double*)w, n, kind == EGFEM_INTERP_SQUARE);
+      k_interp_copy<double><<<grid, 256, 0, s>>>((const double*)u, (double*)w, n, mode, p);
     else
-      k_interp_copy<float><<<grid, 256, 0, s>>>((const float*)u, (float*)w, n, kind == EGFEM_INTERP_SQUARE);
+      k_interp_copy<float><<<grid, 256, 0, s>>>((const float*)u, (float*)w, n, mode, p);
     count_launch();
-  } else if (kind == EGFEM_INTERP_GRADPOW_P0) {
+  } else if (kind == EGFEM_INTERP_RECIPROCAL) {  // W = P0, V = P1: at the centroid
+    if (t->n_cells > 0) {
+      if (f64)
+        k_interp_recip_p0<double><<<nblk(t->n_cells), 256, 0, s>>>(t->vdofs, t->wdofs, t->n_cells, t->dim + 1,
+                                                                   (const double*)u, (double*)w, (double*)chain, p);
+      else
+        k_interp_recip_p0<float><<<nblk(t->n_cells), 256, 0, s>>>(t->vdofs, t->wdofs, t->n_cells, t->dim + 1,
+                                                                  (const float*)u, (float*)w, (float*)chain, p);
+      count_launch();
+    }
+  } else if (kind == EGFEM_INTERP_GRADPOW_P0 || kind == EGFEM_INTERP_MINSURF_P0) {
     const int grid = nblk(t->n_cells, 128);
     if (t->n_cells > 0) {
 #define EGFEM_GP3(S, D, SA, IO)                                                                       \
   k_interp_gradpow<S, D, SA, IO><<<grid, 128, 0, s>>>(D == 3 ? t->coords4 : t->coords, t->cells, t->vdofs,   \
-                                                      t->wdofs, t->n_cells, (const S*)u, (S*)w, (S*)chain, p)
+                                                      t->wdofs, t->n_cells, (const S*)u, (S*)w, (S*)chain, p, \
+                                                      kind == EGFEM_INTERP_MINSURF_P0)
 #define EGFEM_GP(S, D)                                                          \
   do {                                                                          \
     if (t->vdofs_is_cells && t->wdofs_is_iota) EGFEM_GP3(S, D, true, true);     \
@@ -708,7 +752,7 @@ egfem_status launch_interp(const egfem_tensor* t, egfem_interp_kind kind, double
   return EGFEM_OK;
 }
 
-egfem_status launch_tile(const egfem_tensor* t, bool do_r, int jac, egfem_interp_kind kind, const void* u,
+egfem_status launch_tile(const egfem_tensor* t, bool do_r, int jac, egfem_interp_kind kind, double p, const void* u,
                          const void* w, const void* chain, void* r, void* csr_vals, cudaStream_t s) {
   // Row-group kernels (egfem_rows.cu) unless a row is too long or EGFEM_PATH=tile forces the
   // TMA-pipelined tile kernel (kept as the general path and as a cross-check in the tests).
@@ -718,9 +762,9 @@ egfem_status launch_tile(const egfem_tensor* t, bool do_r, int jac, egfem_interp
   const bool rows_only = force && force[0] == 'r';
   if (!tile && !rows_only && cells_path_ok(t, jac))
     return launch_cells(t, do_r, jac, u, w, chain, r, csr_vals, s);
-  if (!tile && rows_path_ok(t, jac)) return launch_rows(t, do_r, jac, kind, u, w, chain, r, csr_vals, s);
-  if (t->dtype == EGFEM_F64) return tile_dispatch<double>(t, do_r, jac, kind, u, w, chain, r, csr_vals, s);
-  return tile_dispatch<float>(t, do_r, jac, kind, u, w, chain, r, csr_vals, s);
+  if (!tile && rows_path_ok(t, jac)) return launch_rows(t, do_r, jac, kind, p, u, w, chain, r, csr_vals, s);
+  if (t->dtype == EGFEM_F64) return tile_dispatch<double>(t, do_r, jac, kind, p, u, w, chain, r, csr_vals, s);
+  return tile_dispatch<float>(t, do_r, jac, kind, p, u, w, chain, r, csr_vals, s);
 }
 
 egfem_status launch_batched(const egfem_tensor* t, int32_t batch, egfem_layout layout, const void* U, const void* W,

@@ -44,7 +44,8 @@ struct RowArgs {
   S* r;
   S* csr;
   int d1;
-  bool square;
+  int dmode;   // W = V Newton factor: 0 → 1, 1 → 2u (SQUARE), 2 → −1/(pk+u)² (RECIPROCAL)
+  double pk;
   uint32_t kmask;
   int64_t diag_off;  // column of row i's diagonal = i + diag_off (local tensors)
 };
@@ -279,7 +280,13 @@ __global__ void __launch_bounds__(256, (JAC == kJacNewtonP0 || JAC == kJacNewton
             const int b = (f + 1 < nf) ? (int)__ldg(A.fib_kr + cur.f0 + f + 1) : ne;
             S x = S(0);
             for (int y = a; y < b; ++y) x = add_(x, s_x[y]);
-            s_b[f] = A.square ? mul_(mul_(S(2), uj_cur[q]), x) : x;
+            S cm = S(1);
+            if (A.dmode == 1) cm = mul_(S(2), uj_cur[q]);
+            if (A.dmode == 2) {
+              const S iv = S(1) / (S(A.pk) + uj_cur[q]);
+              cm = -mul_(iv, iv);
+            }
+            s_b[f] = A.dmode ? mul_(cm, x) : x;
           }
         }
         __syncwarp();
@@ -440,7 +447,7 @@ void rows_config(const egfem_tensor* t, int* G, int* NCH) {
 }
 
 template <typename S>
-egfem_status rows_dispatch(const egfem_tensor* t, bool do_r, int jac, egfem_interp_kind kind, const void* u,
+egfem_status rows_dispatch(const egfem_tensor* t, bool do_r, int jac, egfem_interp_kind kind, double p, const void* u,
                            const void* w, const void* chain, void* r, void* csr, cudaStream_t s) {
   RowArgs<S> A;
   A.n_u = t->n_u;
@@ -457,7 +464,8 @@ egfem_status rows_dispatch(const egfem_tensor* t, bool do_r, int jac, egfem_inte
   A.r = static_cast<S*>(r);
   A.csr = static_cast<S*>(csr);
   A.d1 = t->dim + 1;
-  A.square = kind == EGFEM_INTERP_SQUARE;
+  A.dmode = kind == EGFEM_INTERP_SQUARE ? 1 : (kind == EGFEM_INTERP_RECIPROCAL ? 2 : 0);
+  A.pk = p;
   A.kmask = t->kmask();
   A.diag_off = t->row_begin - t->col_begin;
   int G = 0, NCH = 0;
@@ -490,11 +498,11 @@ bool rows_path_ok(const egfem_tensor* t, int jac) {
   return G > 0 && G * NCH >= t->max_row_nnz && t->max_row_fib <= (G < 32 ? 2 * G : G);
 }
 
-egfem_status launch_rows(const egfem_tensor* t, bool do_r, int jac, egfem_interp_kind kind, const void* u,
+egfem_status launch_rows(const egfem_tensor* t, bool do_r, int jac, egfem_interp_kind kind, double p, const void* u,
                          const void* w, const void* chain, void* r, void* csr_vals, cudaStream_t s) {
   if (t->n_u <= 0) return EGFEM_OK;
-  if (t->dtype == EGFEM_F64) return rows_dispatch<double>(t, do_r, jac, kind, u, w, chain, r, csr_vals, s);
-  return rows_dispatch<float>(t, do_r, jac, kind, u, w, chain, r, csr_vals, s);
+  if (t->dtype == EGFEM_F64) return rows_dispatch<double>(t, do_r, jac, kind, p, u, w, chain, r, csr_vals, s);
+  return rows_dispatch<float>(t, do_r, jac, kind, p, u, w, chain, r, csr_vals, s);
 }
 
 // Offline W = V Newton data for the row kernels (rows of at most kRowsMaxNnz nonzeros).

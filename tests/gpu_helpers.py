@@ -14,7 +14,7 @@ def gpu_pass(eg, t, pr, u_np, newton=True, fused=False, dtype=None):
     u = torch.tensor(u_np, dtype=td, device=dev)
     w = torch.empty(t.n_f, dtype=td, device=dev)
     chain = None
-    if pr.interp == I.INTERP_GRADPOW_P0:
+    if pr.W.family == I.P0 and pr.interp in (I.INTERP_GRADPOW_P0, I.INTERP_MINSURF_P0, I.INTERP_RECIPROCAL):
         chain = torch.empty(t.n_f * (pr.mesh.dim + 1), dtype=td, device=dev)
     eg.egfem_interp(t, pr.interp, pr.p, u, w, chain)
     r = torch.empty(t.n_u, dtype=td, device=dev)

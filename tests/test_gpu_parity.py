@@ -51,7 +51,9 @@ def _maps_kw(pr):
 
 
 SMALL = [("cfg1", None), ("cfg2", None), ("cfg3", None), ("cfg4", None), ("cfg5", None),
-         ("cfg2", 7), ("cfg3", 5), ("cfg4", 3), ("cfg4", 1), ("cfg3", 1), ("cfg1", 1), ("cfg5", 1)]
+         ("cfg2", 7), ("cfg3", 5), ("cfg4", 3), ("cfg4", 1), ("cfg3", 1), ("cfg1", 1), ("cfg5", 1),
+         # SURVEY §8(f) F1 pointwise kinds: minimal surface (P0 W) and biochemical σ/(k+u) (W = P1, P0)
+         ("minsurf2d", None), ("minsurf3d", None), ("minsurf3d", 2), ("biochem_p1", None), ("biochem_p0", None)]
 
 
 @pytest.mark.parametrize("name,n", SMALL)

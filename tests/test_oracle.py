@@ -550,3 +550,70 @@ def test_row_range_build_matches_full(oracle_mod):
     assert np.array_equal(part["t_j"], full["t_j"][a:b])
     assert np.array_equal(part["t_k"], full["t_k"][a:b])
     assert np.array_equal(part["t_val"], full["t_val"][a:b])
+
+
+# ----------------------------------------------------------------------------- F1 pointwise kinds
+@pytest.mark.parametrize("dim", [2, 3])
+def test_minsurf_linear_field(oracle_mod, dim):
+    """u = interpolant of α·x + β ⇒ ∇u_h ≡ α ⇒ a_K = (1 + |α|²)^{-1/2} on every cell."""
+    m = jitter(I.mesh_square(5) if dim == 2 else I.mesh_cube(3), 0.2, 8)
+    T = oracle_mod.OracleTensor(m, I.space_p1(m), I.space_p0(m), I.FORM_PLAP)
+    alpha = np.array([0.7, -1.3, 0.4][:dim])
+    w = T.interp(I.INTERP_MINSURF_P0, 0.0, m.coords @ alpha + 0.25)
+    assert np.abs(w - 1.0 / np.sqrt(1.0 + alpha @ alpha)).max() < 1e-15
+
+
+@pytest.mark.parametrize("dim", [2, 3])
+def test_minsurf_egfem_p0_equals_sga(oracle_mod, dim):
+    """a(∇u_h) is constant per cell for P1 u_h, so EGFEM-P0 reproduces the SGA
+    minimal-surface residual (tensor-free brute force)."""
+    m = jitter(I.mesh_square(5) if dim == 2 else I.mesh_cube(2), 0.2, 11)
+    T = oracle_mod.OracleTensor(m, I.space_p1(m), I.space_p0(m), I.FORM_PLAP)
+    u = np.random.default_rng(12).standard_normal(m.n_vertices)
+    r = T.apply(u, T.interp(I.INTERP_MINSURF_P0, 0.0, u))
+    assert rel_l2(r, brute.sga_minsurf(m, u)) < 1e-13
+
+
+@pytest.mark.parametrize("wfam", ["P1", "P0"])
+def test_reciprocal_tensor_free(oracle_mod, wfam):
+    """M_c̃:(u⊗c̃) with c̃ = 1/(k+u) interpolated onto W equals ∫ φ_i u_h c̃_h
+    integrated exactly without the tensor (W = P1: nodal GFEM; W = P0: centroid value)."""
+    m = jitter(I.mesh_square(4), 0.2, 13)
+    V = I.space_p1(m)
+    W = V if wfam == "P1" else I.space_p0(m)
+    T = oracle_mod.OracleTensor(m, V, W, I.FORM_MASS3)
+    u = 0.5 + np.random.default_rng(14).uniform(0.0, 1.0, V.n_dofs)
+    k = 1.0
+    r = T.apply(u, T.interp(I.INTERP_RECIPROCAL, k, u))
+    assert rel_l2(r, brute.tensor_free_reciprocal(m, u, k, wfam)) < 1e-13
+
+
+def test_reciprocal_closed_forms(oracle_mod):
+    """Constant u = c ⇒ c̃ ≡ 1/(k+c) at the nodes; linear u ⇒ c̃_K = 1/(k + u(x̄_K)) at the centroid
+    x̄_K = mean of the cell's vertices (u_h is exact for linear u)."""
+    m = jitter(I.mesh_square(4), 0.2, 15)
+    V = I.space_p1(m)
+    T1 = oracle_mod.OracleTensor(m, V, V, I.FORM_MASS3)
+    assert np.abs(T1.interp(I.INTERP_RECIPROCAL, 2.0, np.full(V.n_dofs, 0.5)) - 0.4).max() < 1e-16
+    T0 = oracle_mod.OracleTensor(m, V, I.space_p0(m), I.FORM_MASS3)
+    alpha = np.array([0.3, -0.2])
+    u = m.coords @ alpha + 1.0
+    xc = m.coords[m.cells].mean(axis=1)
+    w = T0.interp(I.INTERP_RECIPROCAL, 1.0, u)
+    assert np.abs(w - 1.0 / (1.0 + xc @ alpha + 1.0)).max() < 1e-15
+
+
+@pytest.mark.parametrize("case", ["minsurf2d", "minsurf3d", "biochem_p1", "biochem_p0"])
+def test_f1_newton_vs_finite_differences(oracle_mod, case):
+    """J = T·w + (T·₂u)·D_u w for the F1 kinds equals central differences of r(u) = T:(u⊗w(u));
+    the minimal-surface Newton matrix is symmetric (like p-Laplace)."""
+    pr = I.make_problem(case, n={"minsurf2d": 4, "minsurf3d": 2, "biochem_p1": 3, "biochem_p0": 3}[case])
+    m = jitter(pr.mesh, 0.15, 2)
+    T = oracle_mod.OracleTensor(m, pr.V, pr.W, pr.form)
+    u = pr.u
+    w = T.interp(pr.interp, pr.p, u)
+    J = _csr_dense(T, T.jacobian(I.JAC_NEWTON, pr.interp, pr.p, u, w))
+    Jfd = _fd_jacobian(T, pr.interp, pr.p, u, 1e-5)
+    assert rel_l2(J, Jfd) < 1e-8
+    if pr.interp == I.INTERP_MINSURF_P0:
+        assert rel_l2(J, J.T) < 1e-14
