@@ -175,7 +175,8 @@ def run_ours(args):
         return run_batched(args, eg, t, pr, dev, td, s, build_s, world, rank)
     u = torch.tensor(u_np, dtype=td, device=dev)
     w = torch.empty(t.n_f, dtype=td, device=dev)
-    gp = pr.W.family == I.P0 and pr.interp in (I.INTERP_GRADPOW_P0, I.INTERP_MINSURF_P0, I.INTERP_RECIPROCAL)
+    gp = pr.W.family in (I.P0, I.QUAD) and pr.interp in (I.INTERP_GRADPOW_P0, I.INTERP_MINSURF_P0,
+                                                         I.INTERP_RECIPROCAL, I.INTERP_SQUARE)
     chain = torch.empty(t.n_f * (pr.mesh.dim + 1), dtype=td, device=dev) if gp else None
     r = torch.empty(t.n_u, dtype=td, device=dev)
     J = torch.empty(t.nnz_csr, dtype=td, device=dev)

@@ -21,7 +21,7 @@ from typing import Optional
 import numpy as np
 
 # Space family codes (must match include/egfem.h egfem_family and oracle/).
-P0, P1, P2 = 0, 1, 2
+P0, P1, P2, QUAD = 0, 1, 2, 3
 # Form codes (include/egfem.h egfem_form).
 FORM_CONV_K, FORM_CONV_J, FORM_PLAP, FORM_MASS3, FORM_CONV_I = 0, 1, 2, 3, 4
 # Interp kinds (include/egfem.h egfem_interp_kind).
@@ -126,6 +126,14 @@ def space_p0(mesh: Mesh) -> Space:
     return Space(P0, mesh.n_cells, cd, None)
 
 
+def space_quad(mesh: Mesh, nq: int) -> Space:
+    """The quadrature-embedded space I_k: N_q DOFs per cell numbered
+    K·N_q + ℓ (N_f = N_q·N_el, L139).  Only the count is an input; each side (GPU builder,
+    oracle) uses its own rule with N_q points (2D: 1, 3, 6; 3D: 1, 4)."""
+    cd = np.arange(mesh.n_cells * nq, dtype=np.int32).reshape(-1, nq)
+    return Space(QUAD, mesh.n_cells * nq, cd, None)
+
+
 def space_p2_square(n: int) -> Space:
     """P2 on mesh_square(n) with lattice numbering on the (2n+1)² grid.
 
@@ -218,14 +226,21 @@ def _u_paper_bc(x, seed):
 # Full BASELINE.json sizes; "small" variants use the same recipe at a size the
 # oracle finishes in seconds but that still spans many kernel tiles.
 FULL_N = {"cfg1": 256, "cfg2": 512, "cfg3": 1024, "cfg4": 128, "cfg5": 256,
-          "minsurf2d": 1024, "minsurf3d": 64, "biochem_p1": 512, "biochem_p0": 512}
+          "minsurf2d": 1024, "minsurf3d": 64, "biochem_p1": 512, "biochem_p0": 512,
+          "quadratic_i4": 512, "biochem_i2": 512, "plap_i1": 1024, "plap3d_i2": 32}
 SMALL_N = {"cfg1": 256, "cfg2": 40, "cfg3": 48, "cfg4": 10, "cfg5": 24,
-           "minsurf2d": 40, "minsurf3d": 8, "biochem_p1": 32, "biochem_p0": 32}
+           "minsurf2d": 40, "minsurf3d": 8, "biochem_p1": 32, "biochem_p0": 32,
+           "quadratic_i4": 24, "biochem_i2": 32, "plap_i1": 40, "plap3d_i2": 5}
 CONFIG_NAMES = ("cfg1", "cfg2", "cfg3", "cfg4", "cfg5")
 # SURVEY §8(f) F1 pointwise kinds (not BASELINE configs): minimal surface a = (1+|∇u|²)^{-1/2}
 # with P0 W (§5.6) and the biochemical c̃ = σ/(k+u), σ = 1 = k, on the
 # trilinear mass tensor M_c̃ with W = P1 (GFEM) or P0 (§5.4).
-EXTRA_NAMES = ("minsurf2d", "minsurf3d", "biochem_p1", "biochem_p0")
+# F2 quadrature-embedded W = I_k (Case 3): the §5.1 quadratic term M:(u⊗w),
+# w = u² at the points of the 6-point rule (I_4, Table 1's "EGFEM (I4)", L492); the biochemical
+# term on I_2 (3 points, L541–550); the p-Laplace K_a on I_1 (centroid, L143–149, L616) and on the
+# 4-point tetrahedral I_2 (3D).
+EXTRA_NAMES = ("minsurf2d", "minsurf3d", "biochem_p1", "biochem_p0", "quadratic_i4", "biochem_i2", "plap_i1",
+               "plap3d_i2")
 
 
 def make_problem(name: str, n: Optional[int] = None, batch: Optional[int] = None) -> Problem:
@@ -272,6 +287,22 @@ def make_problem(name: str, n: Optional[int] = None, batch: Optional[int] = None
         W = V if name == "biochem_p1" else space_p0(mesh)
         return Problem(name, mesh, V, W, FORM_MASS3, INTERP_RECIPROCAL, 1.0, ("f64",),
                        _u_paper_bc(mesh.coords, 8), description=f"2D biochemical sigma/(k+u), W={name[-2:]}, {n}x{n}")
+    if name == "quadratic_i4":
+        mesh = mesh_square(n)
+        return Problem(name, mesh, space_p1(mesh), space_quad(mesh, 6), FORM_MASS3, INTERP_SQUARE, 0.0, ("f64",),
+                       _u_paper_bc(mesh.coords, 9), description=f"2D quadratic u^2 on I4 (6-pt), {n}x{n}")
+    if name == "biochem_i2":
+        mesh = mesh_square(n)
+        return Problem(name, mesh, space_p1(mesh), space_quad(mesh, 3), FORM_MASS3, INTERP_RECIPROCAL, 1.0,
+                       ("f64",), _u_paper_bc(mesh.coords, 10), description=f"2D biochemical on I2 (3-pt), {n}x{n}")
+    if name == "plap_i1":
+        mesh = mesh_square(n)
+        return Problem(name, mesh, space_p1(mesh), space_quad(mesh, 1), FORM_PLAP, INTERP_GRADPOW_P0, 4.0,
+                       ("f64",), _u_cfg3(mesh.coords), description=f"2D p-Laplace p=4 on I1 (centroid), {n}x{n}")
+    if name == "plap3d_i2":
+        mesh = mesh_cube(n)
+        return Problem(name, mesh, space_p1(mesh), space_quad(mesh, 4), FORM_PLAP, INTERP_GRADPOW_P0, 3.0,
+                       ("f64",), _u_cfg4(mesh.coords), description=f"3D p-Laplace p=3 on I2 (4-pt), {n}^3x6")
     raise KeyError(name)
 
 

@@ -53,8 +53,16 @@ typedef enum {
 
 typedef enum { EGFEM_F64 = 0, EGFEM_F32 = 1 } egfem_dtype;
 
-/* Lagrange families (P0 for gradient nonlinearities L584). */
-typedef enum { EGFEM_P0 = 0, EGFEM_P1 = 1, EGFEM_P2 = 2 } egfem_family;
+/* Families.  P0/P1/P2: Lagrange (P0 for gradient nonlinearities
+ * L584).  QUAD: the quadrature-embedded space I_k of Case 3 (L117–139, eq.
+ * (quadrature_basis)), W only: its DOFs are the N_q points x_ℓ^K of the rule used for
+ * the assembly in every cell (N_f = N_q·N_el, L139), basis η_ℓ^K = w_ℓ^K δ_{x_ℓ^K}, so
+ * T_ijk for k = (K, ℓ) is w_ℓ|K| (slot φ_i)(x_ℓ)(slot φ_j)(x_ℓ) — the discrete SGA term
+ * with that rule is reproduced exactly.  N_q = n_dofs / n_cells; the rule is the
+ * `quad` argument of egfem_tensor_build (n_points must equal N_q) or the default rule
+ * with N_q points (2D: 1, 3, 6; 3D: 1, 4; 1D: 3).  The k-slot must be a value slot
+ * (every form but CONV_K). */
+typedef enum { EGFEM_P0 = 0, EGFEM_P1 = 1, EGFEM_P2 = 2, EGFEM_QUAD = 3 } egfem_family;
 
 /* Trilinear forms, slot order (i = test, j = u-slot, k = w-slot):
  *   CONV_K : ∫ φ_i φ_j ∂x φ_k                 (BASELINE cfg1, 1D Burgers)
@@ -79,7 +87,10 @@ typedef enum {
  *   MINSURF_P0      : w_K = (1 + ‖∇u_h|_K‖²)^{−1/2}  (V = P1, W = P0, minimal surface a(·), L605–611)
  *   RECIPROCAL      : w_k = 1 / (p + u_h(x_k))  (the biochemical c̃ = σ/(k+u) with σ = 1, k = p,
  *                     L520–535; W = V: at the nodes; W = P0 with V = P1: at the centroid,
- *                     u_h(x_K) = mean of the cell's vertex values) */
+ *                     u_h(x_K) = mean of the cell's vertex values)
+ * With W = QUAD (V = P1) every kind but IDENTITY / P1_TO_P2_SQUARE is evaluated at the
+ * quadrature points (Case 3, L133): GRADPOW_P0 / MINSURF_P0 (∇u_h is constant per cell),
+ * RECIPROCAL and SQUARE (w = u_h(x_ℓ)²) at u_h(x_ℓ) = Σ_a λ_a(x_ℓ) u_a. */
 typedef enum {
   EGFEM_INTERP_IDENTITY = 0,
   EGFEM_INTERP_SQUARE = 1,
@@ -105,9 +116,9 @@ typedef struct {
   const int32_t* cells;   /* host, n_cells*(dim+1) vertex ids */
 } egfem_mesh;
 
-/* A DOF numbering of a Lagrange space on the mesh.  cell_dofs == NULL means the
- * canonical numbering: P0 -> cell id, P1 -> vertex id (mesh cells).  P2 (2D only)
- * needs an explicit table with local order (v0, v1, v2, m01, m12, m20). */
+/* A DOF numbering of a space on the mesh.  cell_dofs == NULL means the canonical
+ * numbering: P0 -> cell id, P1 -> vertex id (mesh cells), QUAD -> K·N_q + ℓ.  P2 (2D
+ * only) needs an explicit table with local order (v0, v1, v2, m01, m12, m20). */
 typedef struct {
   egfem_family family;
   int64_t n_dofs;
@@ -173,10 +184,9 @@ egfem_status egfem_tensor_export(const egfem_tensor* t, int64_t* t_row_ptr, int3
 
 /* ---------------------------------------------------------------- per iteration
  * (1) w = f(Π_u u, Π_∇u ·₂ u) at every W-DOF.
- * u: device [N_u]; w: device [N_f].  chain (nullable; P0-W kinds only: GRADPOW_P0,
- * MINSURF_P0, RECIPROCAL with W = P0): device [N_f*(d+1)], chain[K*(d+1)+m] =
- * ∂w_K/∂u_{v_m(K)} (the pointwise D_u w of PAPER.md L292), consumed by egfem_jacobian
- * NEWTON.  p > 1 required for GRADPOW_P0; p is k of RECIPROCAL (any value; p + u = 0
+ * u: device [N_u]; w: device [N_f].  chain (nullable; cell-wise W = P0 or QUAD only):
+ * device [N_f*(d+1)], chain[k*(d+1)+m] = ∂w_k/∂u_{v_m} for the cell K owning W-DOF k (the
+ * pointwise D_u w of PAPER.md L292), consumed by egfem_jacobian NEWTON.  p > 1 required for GRADPOW_P0; p is k of RECIPROCAL (any value; p + u = 0
  * gives ±inf); p ignored otherwise.  At ∇u_h|_K = 0 and p < 4 the GRADPOW derivative is
  * taken as 0 (reading C11). */
 egfem_status egfem_interp(const egfem_tensor* t, egfem_interp_kind kind, double p, const void* u,
@@ -198,8 +208,8 @@ egfem_status egfem_apply_batched(const egfem_tensor* t, int32_t batch, egfem_lay
  *   NEWTON IDENTITY     : J = T·w + T·₂u                (∂w_k/∂u_m = δ_km)
  *   NEWTON SQUARE       : J = T·w + (T·₂u)·diag(2u)
  *   NEWTON RECIPROCAL   : J = T·w + (T·₂u)·diag(−1/(p+u)²)   (W = V)
- *   NEWTON P0-W kinds   : J = T·w + (T·₂u)·D_u w, D_u w from `chain` (egfem_interp):
- *                         GRADPOW_P0, MINSURF_P0, RECIPROCAL with W = P0
+ *   NEWTON cell-wise W  : J = T·w + (T·₂u)·D_u w, D_u w from `chain` (egfem_interp):
+ *                         W = P0 or QUAD with GRADPOW_P0, MINSURF_P0, RECIPROCAL, (QUAD) SQUARE
  * u: [N_u] (NEWTON), w: [N_f], chain: [N_f*(d+1)] (P0-W NEWTON), csr_vals: [nnz_csr].
  * NEWTON with P1_TO_P2_SQUARE returns UNSUPPORTED. */
 egfem_status egfem_jacobian(const egfem_tensor* t, egfem_jac_mode mode, egfem_interp_kind kind, double p,

@@ -263,6 +263,21 @@ def tensor_free_reciprocal(mesh, u, k, w_family):
     return r
 
 
+def sga_rule_mass(mesh, u, f, bary, weights):
+    """SGA of the term ∫ φ_i u f(u) with a quadrature rule: Σ_K Σ_ℓ w_ℓ|K| φ_i(x_ℓ)
+    u_h(x_ℓ) f(u_h(x_ℓ)) — what EGFEM with W = I_k must reproduce exactly (Case 3, L133–139)."""
+    d = mesh.dim
+    r = np.zeros(mesh.n_vertices)
+    bary = np.asarray(bary, dtype=np.float64).reshape(len(weights), d + 1)
+    for K in range(mesh.n_cells):
+        I = mesh.cells[K]
+        _, vol = geometry(mesh.coords[I])
+        for lam, wq in zip(bary, weights):
+            uh = lam @ u[I]
+            r[I] += wq * vol * lam * uh * f(uh)
+    return r
+
+
 def sga_cubic_mass(mesh, u):
     """r_i = ∫ φ_i u_h³ dx exactly (Case-1 target, PAPER.md L338 / L456)."""
     d = mesh.dim

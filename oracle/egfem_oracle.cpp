@@ -31,7 +31,7 @@
 
 namespace {
 
-enum { OF_P0 = 0, OF_P1 = 1, OF_P2 = 2 };
+enum { OF_P0 = 0, OF_P1 = 1, OF_P2 = 2, OF_QUAD = 3 };  // QUAD: I_k of PAPER.md L117–139
 enum { OFORM_CONV_K = 0, OFORM_CONV_J = 1, OFORM_PLAP = 2, OFORM_MASS3 = 3, OFORM_CONV_I = 4 };
 enum { OK_IDENTITY = 0, OK_SQUARE = 1, OK_GRADPOW_P0 = 2, OK_P1_TO_P2_SQUARE = 3, OK_MINSURF_P0 = 4, OK_RECIPROCAL = 5 };
 enum { OJ_PICARD = 0, OJ_NEWTON = 1 };
@@ -62,6 +62,8 @@ struct OTensor {
   // CSR pattern (union of element cliques over V-DOFs)
   std::vector<int64_t> csr_row_ptr;
   std::vector<int32_t> csr_col;
+  // W = QUAD: barycentric coordinates of the quadrature points (the W DOFs of each cell)
+  std::vector<double> wbary;
 };
 
 // ---------------------------------------------------------------- geometry
@@ -150,7 +152,7 @@ static void basis(int family, int d, const double* lam, const Geo& g, int n_loc,
   }
 }
 
-static int family_degree(int f) { return f == OF_P0 ? 0 : (f == OF_P1 ? 1 : 2); }
+static int family_degree(int f) { return (f == OF_P0 || f == OF_QUAD) ? 0 : (f == OF_P1 ? 1 : 2); }
 
 // ---------------------------------------------------------------- quadrature
 // Reference rules in barycentric coordinates, weights summing to 1 (physical
@@ -283,10 +285,32 @@ int oracle_build(int dim, int64_t n_vertices, const double* coords, int64_t n_ce
     R.nq = nq;
     R.bary.assign(qbary, qbary + nq * (dim + 1));
     R.w.assign(qw, qw + nq);
+  } else if (w_family == OF_QUAD) {
+    // I_k: the W DOFs are the points of the assembly rule itself; take the
+    // default rule with exactly w_nloc points.
+    bool found = false;
+    for (int deg : {1, 2, 4, 5}) {
+      R = default_rule(dim, deg);
+      if (R.nq == w_nloc) {
+        found = true;
+        break;
+      }
+    }
+    if (!found) {
+      delete T;
+      return -4;
+    }
   } else {
     int deg = op_degree(opA, v_family) + op_degree(opB, v_family) + op_degree(opC, w_family);
     if (opA == OP_GRAD) deg = 2 * op_degree(OP_GRAD, v_family) + op_degree(opC, w_family);
     R = default_rule(dim, deg);
+  }
+  if (w_family == OF_QUAD) {
+    if (R.nq != w_nloc || opC != OP_VALUE) {
+      delete T;
+      return -5;
+    }
+    T->wbary = R.bary;
   }
 
   // ---- emit every local triple, cell-major then (a,b,c) lexicographic
@@ -306,7 +330,14 @@ int oracle_build(int dim, int64_t n_vertices, const double* coords, int64_t n_ce
     for (int q = 0; q < R.nq; ++q) {
       const double* lam = &R.bary[q * (dim + 1)];
       basis(v_family, dim, lam, g, nA, vv.data(), reinterpret_cast<double(*)[3]>(vg.data()));
-      basis(w_family, dim, lam, g, nC, wv.data(), reinterpret_cast<double(*)[3]>(wg.data()));
+      if (w_family == OF_QUAD) {  // η_ℓ = w_ℓ δ_{x_ℓ}: ∫ v η_ℓ = w_ℓ v(x_ℓ)
+        for (int c = 0; c < nC; ++c) {
+          wv[c] = (c == q) ? 1.0 : 0.0;
+          wg[c * 3] = wg[c * 3 + 1] = wg[c * 3 + 2] = 0.0;
+        }
+      } else {
+        basis(w_family, dim, lam, g, nC, wv.data(), reinterpret_cast<double(*)[3]>(wg.data()));
+      }
       double wq = R.w[q] * g.vol;
       for (int a = 0; a < nA; ++a)
         for (int b = 0; b < nA; ++b)
@@ -409,6 +440,12 @@ int oracle_export(const void* h, int64_t* t_row_ptr, int32_t* t_j, int32_t* t_k,
   if (t_val) std::copy(T->t_val.begin(), T->t_val.end(), t_val);
   if (csr_row_ptr) std::copy(T->csr_row_ptr.begin(), T->csr_row_ptr.end(), csr_row_ptr);
   if (csr_col) std::copy(T->csr_col.begin(), T->csr_col.end(), csr_col);
+  std::vector<int64_t> wcell;  // cell-wise W (P0: one DOF per cell; QUAD: N_q per cell)
+  if (loc) {
+    wcell.assign(T->W.n_dofs, -1);
+    for (int64_t K = 0; K < T->n_cells; ++K)
+      for (int l = 0; l < T->W.n_loc; ++l) wcell[T->W.cell_dofs[K * T->W.n_loc + l]] = K;
+  }
   for (int64_t i = 0; i < T->V.n_dofs; ++i) {
     for (int64_t e = T->t_row_ptr[i]; e < T->t_row_ptr[i + 1]; ++e) {
       if (slot_ij) {
@@ -422,7 +459,9 @@ int oracle_export(const void* h, int64_t* t_row_ptr, int32_t* t_j, int32_t* t_k,
         slot_ik[e] = (int32_t)s;
       }
       if (loc) {
-        const int32_t* cv = &T->V.cell_dofs[(int64_t)T->t_k[e] * T->V.n_loc];
+        const int64_t cell = wcell[T->t_k[e]];  // the cell owning W-DOF t_k[e]
+        if (cell < 0) return -5;
+        const int32_t* cv = &T->V.cell_dofs[cell * T->V.n_loc];
         int li = -1, lj = -1;
         for (int a = 0; a < T->V.n_loc; ++a) {
           if (cv[a] == i) li = a;
@@ -449,6 +488,20 @@ int oracle_export(const void* h, int64_t* t_row_ptr, int32_t* t_j, int32_t* t_k,
 int oracle_interp(const void* h, int kind, double p, const double* u, double* w) {
   const OTensor* T = static_cast<const OTensor*>(h);
   const int d = T->dim;
+  if (T->W.family == OF_QUAD && (kind == OK_SQUARE || kind == OK_RECIPROCAL)) {
+    // Case 3: f evaluated at the quadrature points, u_h(x_ℓ) = Σ_a λ_a(x_ℓ) u_a
+    if (T->V.family != OF_P1) return -2;
+    const int nq = T->W.n_loc;
+    for (int64_t K = 0; K < T->n_cells; ++K) {
+      const int32_t* I = &T->V.cell_dofs[K * T->V.n_loc];
+      for (int l = 0; l < nq; ++l) {
+        double uh = 0;
+        for (int a = 0; a <= d; ++a) uh += T->wbary[l * (d + 1) + a] * u[I[a]];
+        w[T->W.cell_dofs[K * nq + l]] = (kind == OK_SQUARE) ? uh * uh : 1.0 / (p + uh);
+      }
+    }
+    return 0;
+  }
   if (kind == OK_IDENTITY || kind == OK_SQUARE) {
     if (T->W.n_dofs != T->V.n_dofs) return -1;
     for (int64_t k = 0; k < T->W.n_dofs; ++k) w[k] = (kind == OK_IDENTITY) ? u[k] : u[k] * u[k];
@@ -469,7 +522,7 @@ int oracle_interp(const void* h, int kind, double p, const double* u, double* w)
     return 0;
   }
   if (kind == OK_MINSURF_P0) {
-    if (T->W.family != OF_P0 || T->V.family != OF_P1) return -2;
+    if ((T->W.family != OF_P0 && T->W.family != OF_QUAD) || T->V.family != OF_P1) return -2;
     for (int64_t K = 0; K < T->n_cells; ++K) {
       Geo g = geometry(*T, K);
       const int32_t* I = &T->V.cell_dofs[K * T->V.n_loc];
@@ -478,12 +531,13 @@ int oracle_interp(const void* h, int kind, double p, const double* u, double* w)
         for (int x = 0; x < d; ++x) gu[x] += u[I[a]] * g.grad[a][x];
       double gg = 0;
       for (int x = 0; x < d; ++x) gg += gu[x] * gu[x];
-      w[T->W.cell_dofs[K]] = 1.0 / std::sqrt(1.0 + gg);
+      for (int l = 0; l < T->W.n_loc; ++l) w[T->W.cell_dofs[K * T->W.n_loc + l]] = 1.0 / std::sqrt(1.0 + gg);
     }
     return 0;
   }
   if (kind == OK_GRADPOW_P0) {
-    if (T->W.family != OF_P0 || T->V.family != OF_P1) return -2;
+    // W = P0, or QUAD (∇u_h of P1 is the same at every quadrature point of the cell)
+    if ((T->W.family != OF_P0 && T->W.family != OF_QUAD) || T->V.family != OF_P1) return -2;
     for (int64_t K = 0; K < T->n_cells; ++K) {
       Geo g = geometry(*T, K);
       const int32_t* I = &T->V.cell_dofs[K * T->V.n_loc];
@@ -493,7 +547,7 @@ int oracle_interp(const void* h, int kind, double p, const double* u, double* w)
       double nrm = 0;
       for (int x = 0; x < d; ++x) nrm += gu[x] * gu[x];
       nrm = std::sqrt(nrm);
-      w[T->W.cell_dofs[K]] = std::pow(nrm, p - 2.0);
+      for (int l = 0; l < T->W.n_loc; ++l) w[T->W.cell_dofs[K * T->W.n_loc + l]] = std::pow(nrm, p - 2.0);
     }
     return 0;
   }
@@ -541,6 +595,21 @@ struct DEntry { int64_t k; int32_t m; double v; };
 
 static int build_Duw(const OTensor* T, int kind, double p, const double* u, std::vector<DEntry>& D) {
   const int d = T->dim;
+  if (T->W.family == OF_QUAD && (kind == OK_SQUARE || kind == OK_RECIPROCAL)) {
+    // w_ℓ = f(u_h(x_ℓ)), u_h(x_ℓ) = Σ_a λ_a(x_ℓ) u_a  ⇒  ∂w_ℓ/∂u_a = f'(u_h(x_ℓ)) λ_a(x_ℓ)
+    const int nq = T->W.n_loc;
+    for (int64_t K = 0; K < T->n_cells; ++K) {
+      const int32_t* I = &T->V.cell_dofs[K * T->V.n_loc];
+      for (int l = 0; l < nq; ++l) {
+        double uh = 0;
+        for (int a = 0; a <= d; ++a) uh += T->wbary[l * (d + 1) + a] * u[I[a]];
+        const double df = (kind == OK_SQUARE) ? 2.0 * uh : -1.0 / ((p + uh) * (p + uh));
+        for (int a = 0; a <= d; ++a)
+          D.push_back({(int64_t)T->W.cell_dofs[K * nq + l], I[a], df * T->wbary[l * (d + 1) + a]});
+      }
+    }
+    return 0;
+  }
   if (kind == OK_IDENTITY) {
     for (int64_t k = 0; k < T->W.n_dofs; ++k) D.push_back({k, (int32_t)k, 1.0});
     return 0;
@@ -551,7 +620,7 @@ static int build_Duw(const OTensor* T, int kind, double p, const double* u, std:
   }
   if (kind == OK_GRADPOW_P0) {
     // w_K = |g|^{p-2}, g = Σ_a u_a ∇λ_a  ⇒  ∂w_K/∂u_a = (p-2)|g|^{p-4} (g·∇λ_a);
-    // at g = 0 the value 0 is used (reading C11).
+    // at g = 0 the value 0 is used (reading C11).  W = QUAD: the same for every point of K.
     for (int64_t K = 0; K < T->n_cells; ++K) {
       Geo g = geometry(*T, K);
       const int32_t* I = &T->V.cell_dofs[K * T->V.n_loc];
@@ -561,11 +630,12 @@ static int build_Duw(const OTensor* T, int kind, double p, const double* u, std:
       double gg = 0;
       for (int x = 0; x < d; ++x) gg += gu[x] * gu[x];
       double fac = (gg == 0.0) ? 0.0 : (p - 2.0) * std::pow(std::sqrt(gg), p - 4.0);
-      for (int a = 0; a <= d; ++a) {
-        double gdot = 0;
-        for (int x = 0; x < d; ++x) gdot += gu[x] * g.grad[a][x];
-        D.push_back({(int64_t)T->W.cell_dofs[K], I[a], fac * gdot});
-      }
+      for (int l = 0; l < T->W.n_loc; ++l)
+        for (int a = 0; a <= d; ++a) {
+          double gdot = 0;
+          for (int x = 0; x < d; ++x) gdot += gu[x] * g.grad[a][x];
+          D.push_back({(int64_t)T->W.cell_dofs[K * T->W.n_loc + l], I[a], fac * gdot});
+        }
     }
     return 0;
   }
@@ -580,11 +650,12 @@ static int build_Duw(const OTensor* T, int kind, double p, const double* u, std:
       double gg = 0;
       for (int x = 0; x < d; ++x) gg += gu[x] * gu[x];
       const double fac = -std::pow(1.0 + gg, -1.5);
-      for (int a = 0; a <= d; ++a) {
-        double gdot = 0;
-        for (int x = 0; x < d; ++x) gdot += gu[x] * g.grad[a][x];
-        D.push_back({(int64_t)T->W.cell_dofs[K], I[a], fac * gdot});
-      }
+      for (int l = 0; l < T->W.n_loc; ++l)
+        for (int a = 0; a <= d; ++a) {
+          double gdot = 0;
+          for (int x = 0; x < d; ++x) gdot += gu[x] * g.grad[a][x];
+          D.push_back({(int64_t)T->W.cell_dofs[K * T->W.n_loc + l], I[a], fac * gdot});
+        }
     }
     return 0;
   }

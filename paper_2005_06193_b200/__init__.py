@@ -25,7 +25,7 @@ LIB_PATH = os.path.join(_HERE, "lib", "libegfem.so")
 
 # enums (include/egfem.h)
 F64, F32 = 0, 1
-P0, P1, P2 = 0, 1, 2
+P0, P1, P2, QUAD = 0, 1, 2, 3
 FORM_CONV_K, FORM_CONV_J, FORM_PLAP, FORM_MASS3, FORM_CONV_I = 0, 1, 2, 3, 4
 INTERP_IDENTITY, INTERP_SQUARE, INTERP_GRADPOW_P0, INTERP_P1_TO_P2_SQUARE = 0, 1, 2, 3
 INTERP_MINSURF_P0, INTERP_RECIPROCAL = 4, 5

@@ -54,8 +54,22 @@ egfem_status check_dev_ptr(const egfem_tensor* t, const void* p, const char* nam
 
 egfem_status validate_space(const egfem_mesh* m, const egfem_space* S, const char* name) {
   if (!S) return fail(EGFEM_ERR_INVALID_ARGUMENT, std::string(name) + " is NULL");
-  if (S->family < EGFEM_P0 || S->family > EGFEM_P2)
+  if (S->family < EGFEM_P0 || S->family > EGFEM_QUAD)
     return fail(EGFEM_ERR_INVALID_ARGUMENT, std::string(name) + ": bad family");
+  if (S->family == EGFEM_QUAD) {  // N_q points per cell, each DOF used once
+    if (S->n_dofs <= 0 || S->n_dofs % m->n_cells != 0 || S->n_dofs / m->n_cells > kMaxQuad)
+      return fail(EGFEM_ERR_DIMENSION_MISMATCH, std::string(name) + ": QUAD needs n_dofs = N_q·n_cells, N_q <= 16");
+    if (S->n_dofs >= (int64_t(1) << 31)) return fail(EGFEM_ERR_INDEX_OVERFLOW, std::string(name) + ": n_dofs");
+    if (S->cell_dofs) {
+      std::vector<uint8_t> seen(S->n_dofs, 0);
+      for (int64_t q = 0; q < S->n_dofs; ++q) {
+        if (S->cell_dofs[q] < 0 || S->cell_dofs[q] >= S->n_dofs || seen[S->cell_dofs[q]])
+          return fail(EGFEM_ERR_INVALID_ARGUMENT, "QUAD cell_dofs is not a permutation");
+        seen[S->cell_dofs[q]] = 1;
+      }
+    }
+    return EGFEM_OK;
+  }
   if (S->family == EGFEM_P2 && m->dim != 2) return fail(EGFEM_ERR_UNSUPPORTED, "P2 is implemented in 2D only");
   if (S->family == EGFEM_P2 && !S->cell_dofs) return fail(EGFEM_ERR_INVALID_ARGUMENT, "P2 needs cell_dofs");
   if (S->n_dofs <= 0 || S->n_dofs >= (int64_t(1) << 31))
@@ -133,13 +147,21 @@ egfem_status egfem_tensor_build(const egfem_mesh* mesh, const egfem_space* V, co
   egfem_status st = validate_space(mesh, V, "V");
   if (st) return st;
   if ((st = validate_space(mesh, W, "W"))) return st;
-  if (V->family == EGFEM_P0) return fail(EGFEM_ERR_UNSUPPORTED, "V = P0 has no gradients/test functions here");
+  if (V->family == EGFEM_P0 || V->family == EGFEM_QUAD)
+    return fail(EGFEM_ERR_UNSUPPORTED, "V must be P1 or P2");
+  if (W->family == EGFEM_QUAD && form == EGFEM_FORM_CONV_K)
+    return fail(EGFEM_ERR_UNSUPPORTED, "QUAD W needs a value k-slot (CONV_K differentiates k)");
+  if (W->family == EGFEM_QUAD && quad && quad->n_points > 0 && quad->n_points != W->n_dofs / mesh->n_cells)
+    return fail(EGFEM_ERR_DIMENSION_MISMATCH, "QUAD W: quad->n_points != n_dofs / n_cells");
   if (form == EGFEM_FORM_PLAP && W->family == EGFEM_P2)
     ;  // allowed: quadrature definition
   if (quad && quad->n_points > 0 && (!quad->bary || !quad->weights))
     return fail(EGFEM_ERR_INVALID_ARGUMENT, "quadrature arrays are NULL");
   const int nV = V->family == EGFEM_P1 ? mesh->dim + 1 : 6;
-  const int nW = W->family == EGFEM_P0 ? 1 : (W->family == EGFEM_P1 ? mesh->dim + 1 : 6);
+  const int nW = W->family == EGFEM_P0 ? 1
+                 : W->family == EGFEM_P1 ? mesh->dim + 1
+                 : W->family == EGFEM_QUAD ? (int)(W->n_dofs / mesh->n_cells) : 6;
+  if (nV * nV * nW > 256) return fail(EGFEM_ERR_UNSUPPORTED, "local tensor larger than 256 entries");
   if ((int64_t)nV * nV * nW * mesh->n_cells >= (int64_t(1) << 32))
     return fail(EGFEM_ERR_INDEX_OVERFLOW, "more than 2^32 element triples");
   int ndev = 0;
@@ -288,8 +310,12 @@ egfem_status egfem_interp(const egfem_tensor* t, egfem_interp_kind kind, double 
   switch (kind) {
     case EGFEM_INTERP_IDENTITY:
     case EGFEM_INTERP_SQUARE:
-      if (!t->w_is_v) return fail(EGFEM_ERR_DIMENSION_MISMATCH, "IDENTITY/SQUARE need W = V");
-      if (chain) return fail(EGFEM_ERR_INVALID_ARGUMENT, "chain is only produced by GRADPOW_P0");
+      if (kind == EGFEM_INTERP_SQUARE && t->wfam == EGFEM_QUAD) {  // u_h(x_ℓ)² at the quadrature points
+        if (t->vfam != EGFEM_P1) return fail(EGFEM_ERR_UNSUPPORTED, "SQUARE on QUAD W needs V = P1");
+        break;
+      }
+      if (!t->w_is_v) return fail(EGFEM_ERR_DIMENSION_MISMATCH, "IDENTITY/SQUARE need W = V (SQUARE: or QUAD)");
+      if (chain) return fail(EGFEM_ERR_INVALID_ARGUMENT, "chain is only produced for cell-wise W");
       break;
     case EGFEM_INTERP_GRADPOW_P0:
       if (!t->has_mesh || !t->w_p0 || t->vfam != EGFEM_P1)
@@ -355,6 +381,11 @@ static egfem_status jac_mode_code(const egfem_tensor* t, egfem_jac_mode mode, eg
   switch (kind) {
     case EGFEM_INTERP_IDENTITY:
     case EGFEM_INTERP_SQUARE:
+      if (kind == EGFEM_INTERP_SQUARE && t->wfam == EGFEM_QUAD && t->vfam == EGFEM_P1) {
+        if ((st = check_dev_ptr(t, chain, "chain", true))) return st;
+        *code = 3;
+        return EGFEM_OK;
+      }
       if (!t->w_is_v) return fail(EGFEM_ERR_DIMENSION_MISMATCH, "IDENTITY/SQUARE Newton needs W = V");
       if (!t->newton_wv_ok)
         return fail(EGFEM_ERR_UNSUPPORTED, "T·₂u has entries outside the CSR pattern (from_coo tensor)");
@@ -466,6 +497,7 @@ egfem_status egfem_partition(const egfem_tensor* G, int32_t nranks, int32_t rank
   if (device != G->device) return fail(EGFEM_ERR_UNSUPPORTED, "partition onto another device");
   if (G->has_mesh && !G->w_p0 && !G->w_is_v)
     return fail(EGFEM_ERR_UNSUPPORTED, "row partition needs W = V or W = P0");
+  if (G->wfam == EGFEM_QUAD) return fail(EGFEM_ERR_UNSUPPORTED, "row partition of QUAD W is not implemented");
   DeviceGuard g(G->device);
   // host copies of the integer structure (offline)
   std::vector<int64_t> row_fib(G->n_u + 1);
@@ -593,6 +625,10 @@ egfem_status egfem_partition(const egfem_tensor* G, int32_t nranks, int32_t rank
       return bail(fail(EGFEM_ERR_OUT_OF_MEMORY, "cudaMalloc failed"));
     t->vdofs_is_cells = G->vdofs_is_cells;
     t->wdofs_is_iota = true;
+    t->nwc = 1;
+    if (cudaMalloc(&t->wpts, sizeof(double) * d1) ||
+        cudaMemcpy(t->wpts, G->wpts, sizeof(double) * d1, cudaMemcpyDeviceToDevice))
+      return bail(fail(EGFEM_ERR_CUDA, "wpts copy failed"));
     if (G->dim == 3 && (cudaMalloc(&t->coords4, 32 * std::max<int64_t>(n_local, 1)) ||
                         cudaMemcpy(t->coords4, G->coords4 + cb * 4, 32 * n_local, cudaMemcpyDeviceToDevice)))
       return bail(fail(EGFEM_ERR_CUDA, "coords4 copy failed"));

@@ -129,13 +129,20 @@ __global__ void k_element_triples(const ElemParams P) {
   }
   double g[4][3];
   double vol = simplex_gradients(d, x, g);
-  double Tl[216];
+  double Tl[256];
   for (int l = 0; l < L; ++l) Tl[l] = 0.0;
-  double fv[6], gv[6][3], fw[6], gw[6][3];
+  double fv[6], gv[6][3], fw[kMaxQuad], gw[kMaxQuad][3];
   for (int q = 0; q < P.nq; ++q) {
     const double* lam = &P.bary[q * (d + 1)];
     eval_basis(P.vfam, d, lam, g, fv, gv);
-    eval_basis(P.wfam, d, lam, g, fw, gw);
+    if (P.wfam == EGFEM_QUAD) {  // η_ℓ = w_ℓ δ_{x_ℓ}: the ℓ-th DOF "evaluates" to δ_{ℓq}
+      for (int c = 0; c < nW; ++c) {
+        fw[c] = (c == q) ? 1.0 : 0.0;
+        gw[c][0] = gw[c][1] = gw[c][2] = 0.0;
+      }
+    } else {
+      eval_basis(P.wfam, d, lam, g, fw, gw);
+    }
     const double wq = P.wq[q] * vol;
     for (int a = 0; a < nV; ++a)
       for (int b = 0; b < nV; ++b) {
@@ -285,9 +292,10 @@ __global__ void k_to_f32(const double* a, float* b, int64_t n) {
   if (e < n) b[e] = (float)a[e];
 }
 
-__global__ void k_wcell(const int32_t* wdofs, int32_t* wcell, int64_t n_cells) {
+__global__ void k_wcell(const int32_t* wdofs, int nw, int32_t* wcell, int64_t n_cells) {
   int64_t c = (int64_t)blockIdx.x * blockDim.x + threadIdx.x;
-  if (c < n_cells) wcell[wdofs[c]] = (int32_t)c;
+  if (c < n_cells)
+    for (int l = 0; l < nw; ++l) wcell[wdofs[c * nw + l]] = (int32_t)c;
 }
 
 inline int nblk(int64_t n, int t = 256) { return (int)((n + t - 1) / t); }
@@ -359,7 +367,17 @@ void default_rule(int d, int degree, int* nq, double* bary, double* wq) {
   }
 }
 
-int fam_degree(int f) { return f == EGFEM_P0 ? 0 : (f == EGFEM_P1 ? 1 : 2); }
+// The default rule with exactly n points (QUAD W without an explicit rule); false if none.
+bool default_rule_points(int d, int n, int* nq, double* bary, double* wq) {
+  const int deg = d == 1 ? (n == 3 ? 5 : -1)
+                  : d == 2 ? (n == 1 ? 1 : n == 3 ? 2 : n == 6 ? 4 : -1)
+                           : (n == 1 ? 1 : n == 4 ? 2 : -1);
+  if (deg < 0) return false;
+  default_rule(d, deg, nq, bary, wq);
+  return *nq == n;
+}
+
+int fam_degree(int f) { return (f == EGFEM_P0 || f == EGFEM_QUAD) ? 0 : (f == EGFEM_P1 ? 1 : 2); }
 int op_degree(int op, int fam) {
   int p = fam_degree(fam);
   return op == kValue ? p : (p > 0 ? p - 1 : 0);
@@ -375,7 +393,10 @@ egfem_status upload_mesh(egfem_tensor* t, const egfem_mesh* mesh, const egfem_sp
   t->n_cells = mesh->n_cells;
   t->vfam = V->family;
   t->wfam = W->family;
-  auto nloc = [d](egfem_family f) { return f == EGFEM_P0 ? 1 : (f == EGFEM_P1 ? d + 1 : 6); };
+  const int64_t nq = W->family == EGFEM_QUAD ? W->n_dofs / mesh->n_cells : 0;
+  auto nloc = [d, nq](egfem_family f) {
+    return f == EGFEM_P0 ? 1 : f == EGFEM_P1 ? d + 1 : f == EGFEM_QUAD ? (int)nq : 6;
+  };
   t->nV = nloc(V->family);
   t->nW = nloc(W->family);
   t->n_u = V->n_dofs;
@@ -386,7 +407,10 @@ egfem_status upload_mesh(egfem_tensor* t, const egfem_mesh* mesh, const egfem_sp
     if (S->cell_dofs) return S->cell_dofs;
     tmp.resize((size_t)nc * nl);
     for (int64_t c = 0; c < nc; ++c)
-      for (int a = 0; a < nl; ++a) tmp[c * nl + a] = (S->family == EGFEM_P0) ? (int32_t)c : mesh->cells[c * (d + 1) + a];
+      for (int a = 0; a < nl; ++a)
+        tmp[c * nl + a] = S->family == EGFEM_P0     ? (int32_t)c
+                          : S->family == EGFEM_QUAD ? (int32_t)(c * nl + a)
+                                                    : mesh->cells[c * (d + 1) + a];
     return tmp.data();
   };
   EGFEM_CUDA_TRY(cudaMalloc(&t->coords, sizeof(double) * mesh->n_vertices * d));
@@ -414,11 +438,12 @@ egfem_status upload_mesh(egfem_tensor* t, const egfem_mesh* mesh, const egfem_sp
   }
   t->w_is_v = (V->family == W->family) && (V->n_dofs == W->n_dofs) &&
               std::equal(hvcopy.begin(), hvcopy.end(), hw);
-  t->w_p0 = (W->family == EGFEM_P0);
+  t->w_p0 = (W->family == EGFEM_P0 || W->family == EGFEM_QUAD);
+  t->nwc = t->w_p0 ? t->nW : 1;
   t->newton_wv_ok = t->w_is_v;  // k and j of a cell share it: (i, k) is an element-clique pair
   if (t->w_p0) {
     EGFEM_CUDA_TRY(cudaMalloc(&t->wcell, sizeof(int32_t) * std::max<int64_t>(t->n_f, 1)));
-    k_wcell<<<nblk(nc), 256>>>(t->wdofs, t->wcell, nc);
+    k_wcell<<<nblk(nc), 256>>>(t->wdofs, t->nW, t->wcell, nc);
     count_launch();
     EGFEM_CUDA_TRY(cudaGetLastError());
   }
@@ -450,10 +475,25 @@ egfem_status emit_element_triples(egfem_tensor* t, egfem_form form, const egfem_
       for (int a = 0; a <= t->dim; ++a) P.bary[q * (t->dim + 1) + a] = quad->bary[q * (t->dim + 1) + a];
       P.wq[q] = quad->weights[q];
     }
+  } else if (t->wfam == EGFEM_QUAD) {  // I_k: the default rule with N_q = nW points
+    if (!default_rule_points(t->dim, t->nW, &P.nq, P.bary, P.wq)) {
+      set_error("QUAD W: no default rule with " + std::to_string(t->nW) + " points in " + std::to_string(t->dim) +
+                "D (pass egfem_quad)");
+      return EGFEM_ERR_UNSUPPORTED;
+    }
   } else {
     int deg = (P.opA == kGrad) ? 2 * op_degree(kDx, t->vfam) + op_degree(kValue, t->wfam)
                                : op_degree(P.opA, t->vfam) + op_degree(P.opB, t->vfam) + op_degree(P.opC, t->wfam);
     default_rule(t->dim, deg, &P.nq, P.bary, P.wq);
+  }
+  // cell-wise W: barycentric coordinates of each cell's W DOFs (P0: centroid; QUAD: the rule)
+  if (t->w_p0) {
+    std::vector<double> pts((size_t)t->nwc * (t->dim + 1));
+    for (int l = 0; l < t->nwc; ++l)
+      for (int a = 0; a <= t->dim; ++a)
+        pts[l * (t->dim + 1) + a] = t->wfam == EGFEM_QUAD ? P.bary[l * (t->dim + 1) + a] : 1.0 / (t->dim + 1);
+    EGFEM_CUDA_TRY(cudaMalloc(&t->wpts, sizeof(double) * pts.size()));
+    EGFEM_CUDA_TRY(cudaMemcpy(t->wpts, pts.data(), sizeof(double) * pts.size(), cudaMemcpyHostToDevice));
   }
   P.n_cells = t->n_cells;
   P.n_u = t->n_u;
@@ -847,7 +887,7 @@ egfem_status export_arrays(const egfem_tensor* t, int64_t* t_row_ptr, int32_t* t
 
 void free_tensor(egfem_tensor* t) {
   void* ptrs[] = {t->row_fib, t->row_nz, t->fib_j, t->fib_nz, t->nz_k, t->nz_val, t->nz_aux, t->nz_kpos, t->fib_kr, t->ck_k, t->ck_val, t->ck_b, t->blk_off, t->blk,
-                  t->tile_row, t->tile_fib, t->tile_nz, t->coords, t->coords4, t->cells, t->vdofs, t->wdofs, t->wcell};
+                  t->tile_row, t->tile_fib, t->tile_nz, t->coords, t->coords4, t->cells, t->vdofs, t->wdofs, t->wcell, t->wpts};
   for (void* p : ptrs)
     if (p) cudaFree(p);
 }

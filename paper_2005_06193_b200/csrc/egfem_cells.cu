@@ -491,7 +491,7 @@ egfem_status cells_mode(const egfem_tensor* t, const CellArgs<S>& A, bool do_r, 
 struct CellCfg {
   int d1, G, CPL, FREG;
 };
-constexpr CellCfg kCellCfgs[] = {{3, 2, 3, 4}, {3, 4, 4, 8}, {4, 8, 3, 2}, {4, 16, 3, 2}, {4, 16, 4, 4}};
+constexpr CellCfg kCellCfgs[] = {{3, 2, 3, 4}, {3, 4, 4, 8}, {3, 16, 3, 1}, {4, 8, 3, 2}, {4, 16, 3, 2}, {4, 16, 4, 4}};
 
 bool pick_cells(const egfem_tensor* t, CellCfg* out) {
   static int envG = -1, envC = -1;
@@ -539,6 +539,7 @@ egfem_status cells_dispatch(const egfem_tensor* t, bool do_r, int jac, const voi
   if (c.d1 == D_ && c.G == G_ && c.CPL == C_) return cells_mode<S, D_, G_, C_, F_>(t, A, do_r, jac, s);
   EGFEM_CC(3, 2, 3, 4)
   EGFEM_CC(3, 4, 4, 8)
+  EGFEM_CC(3, 16, 3, 1)
   EGFEM_CC(4, 8, 3, 2)
   EGFEM_CC(4, 16, 3, 2)
   EGFEM_CC(4, 16, 4, 4)

@@ -52,7 +52,9 @@ struct egfem_tensor {
   egfem_form form = EGFEM_FORM_CONV_J;
   int64_t nnz = 0, n_fib = 0;
   bool w_is_v = false;   // W numbering identical to V numbering (IDENTITY/SQUARE allowed)
-  bool w_p0 = false;     // W = P0 (loc packed into nz_k)
+  bool w_p0 = false;     // cell-wise W (P0 or QUAD): every W DOF lies in one cell (loc packed into nz_k)
+  int nwc = 1;           // W DOFs per cell of a cell-wise W (P0: 1, QUAD: N_q)
+  double* wpts = nullptr;  // cell-wise W: barycentric coordinates of a cell's W DOFs, nwc*(dim+1) (device)
   bool newton_wv_ok = false;  // every (i, k) of T is an (i, j) fiber (T·₂u fits the CSR pattern)
   int max_row_nnz = 0, max_row_fib = 0;
   uint32_t kmask() const { return (has_mesh && w_p0) ? egfem::kKMask : egfem::kKMaskAny; }

@@ -70,7 +70,7 @@ template <typename S, int D, bool SAME, bool IOTA>
 __global__ void __launch_bounds__(128) k_interp_gradpow(const double* __restrict__ coords, const int32_t* __restrict__ cells,
                                  const int32_t* __restrict__ vdofs, const int32_t* __restrict__ wdofs, int64_t n_cells,
                                  const S* __restrict__ u, S* __restrict__ w, S* __restrict__ chain, double p,
-                                 bool minsurf) {
+                                 bool minsurf, int nw) {
   int64_t c = (int64_t)blockIdx.x * blockDim.x + threadIdx.x;
   if (c >= n_cells) return;
   const CellIdx<D> cv = load_cell<D>(cells, c);
@@ -162,10 +162,8 @@ __global__ void __launch_bounds__(128) k_interp_gradpow(const double* __restrict
     wk = pow(gg, 0.5 * (p - 2.0));
     fac = gg > 0.0 ? (p - 2.0) * pow(gg, 0.5 * (p - 4.0)) : 0.0;
   }
-  const int64_t K = IOTA ? c : (int64_t)__ldg(wdofs + c);
-  w[K] = (S)wk;
+  S dm[D + 1];
   if (chain) {
-    S dm[D + 1];
 #pragma unroll
     for (int a = 0; a <= D; ++a) {
       double s = 0.0;
@@ -173,35 +171,55 @@ __global__ void __launch_bounds__(128) k_interp_gradpow(const double* __restrict
       for (int q = 0; q < D; ++q) s += gu[q] * g[a][q];
       dm[a] = (S)(fac * s);
     }
-    if constexpr (D == 3 && sizeof(S) == 8) {
-      double2* o = reinterpret_cast<double2*>(chain + K * 4);
-      o[0] = make_double2(dm[0], dm[1]);
-      o[1] = make_double2(dm[2], dm[3]);
-    } else if constexpr (D == 3) {
-      reinterpret_cast<float4*>(chain)[K] = make_float4(dm[0], dm[1], dm[2], dm[3]);
-    } else {
+  }
+  // the cell's W DOFs (P0: one; QUAD: N_q points, ∇u_h is constant on the cell)
+  for (int l = 0; l < nw; ++l) {
+    const int64_t K = IOTA ? c * nw + l : (int64_t)__ldg(wdofs + c * nw + l);
+    w[K] = (S)wk;
+    if (chain) {
+      if constexpr (D == 3 && sizeof(S) == 8) {
+        double2* o = reinterpret_cast<double2*>(chain + K * 4);
+        o[0] = make_double2(dm[0], dm[1]);
+        o[1] = make_double2(dm[2], dm[3]);
+      } else if constexpr (D == 3) {
+        reinterpret_cast<float4*>(chain)[K] = make_float4(dm[0], dm[1], dm[2], dm[3]);
+      } else {
 #pragma unroll
-      for (int a = 0; a <= D; ++a) chain[K * (D + 1) + a] = dm[a];
+        for (int a = 0; a <= D; ++a) chain[K * (D + 1) + a] = dm[a];
+      }
     }
   }
 }
 
-// RECIPROCAL with W = P0 (V = P1): w_K = 1/(k + u_h(x_K)), u_h(x_K) = mean of the vertex values
-// (λ_a = 1/(d+1) at the centroid), chain[K][m] = ∂w_K/∂u_{v_m} = −w_K²/(d+1).
+// Value kinds at the W DOFs of a cell-wise W (V = P1): u_h(x_l) = Σ_a λ_a(x_l) u_a with λ(x_l)
+// from wpts (P0: the centroid; QUAD: the rule's points), then
+//   mode 0 RECIPROCAL: w = 1/(k + u_h), ∂w/∂u_m = −w² λ_m
+//   mode 1 SQUARE:     w = u_h²,        ∂w/∂u_m = 2 u_h λ_m
 template <typename S>
-__global__ void k_interp_recip_p0(const int32_t* __restrict__ vdofs, const int32_t* __restrict__ wdofs,
-                                  int64_t n_cells, int d1, const S* __restrict__ u, S* __restrict__ w,
-                                  S* __restrict__ chain, double pk) {
+__global__ void k_interp_points(const int32_t* __restrict__ vdofs, const int32_t* __restrict__ wdofs,
+                                const double* __restrict__ wpts, int64_t n_cells, int d1, int nw,
+                                const S* __restrict__ u, S* __restrict__ w, S* __restrict__ chain, int mode,
+                                double pk) {
   const int64_t c = (int64_t)blockIdx.x * blockDim.x + threadIdx.x;
   if (c >= n_cells) return;
-  double s = 0.0;
-  for (int a = 0; a < d1; ++a) s += (double)__ldg(u + vdofs[c * d1 + a]);
-  const double wk = 1.0 / (pk + s / d1);
-  const int64_t K = wdofs[c];
-  w[K] = (S)wk;
-  if (chain) {
-    const S dm = (S)(-(wk * wk) / d1);
-    for (int a = 0; a < d1; ++a) chain[K * d1 + a] = dm;
+  double uv[4];
+  for (int a = 0; a < d1; ++a) uv[a] = (double)__ldg(u + vdofs[c * d1 + a]);
+  for (int l = 0; l < nw; ++l) {
+    const double* lam = wpts + l * d1;
+    double uh = 0.0;
+    for (int a = 0; a < d1; ++a) uh += lam[a] * uv[a];
+    double f, df;
+    if (mode == 0) {
+      f = 1.0 / (pk + uh);
+      df = -(f * f);
+    } else {
+      f = uh * uh;
+      df = 2.0 * uh;
+    }
+    const int64_t K = wdofs[c * nw + l];
+    w[K] = (S)f;
+    if (chain)
+      for (int a = 0; a < d1; ++a) chain[K * d1 + a] = (S)(df * lam[a]);
   }
 }
 
@@ -696,7 +714,7 @@ __global__ void k_halo(const int32_t* __restrict__ idx, int64_t n, const S* __re
 egfem_status launch_interp(const egfem_tensor* t, egfem_interp_kind kind, double p, const void* u, void* w,
                            void* chain, cudaStream_t s) {
   const bool f64 = t->dtype == EGFEM_F64;
-  if (kind == EGFEM_INTERP_IDENTITY || kind == EGFEM_INTERP_SQUARE ||
+  if (kind == EGFEM_INTERP_IDENTITY || (kind == EGFEM_INTERP_SQUARE && t->w_is_v) ||
       (kind == EGFEM_INTERP_RECIPROCAL && t->w_is_v)) {
     const int64_t n = t->n_f;
     const int grid = std::max(1, std::min(nblk(n), 148 * 16));
@@ -706,14 +724,17 @@ egfem_status launch_interp(const egfem_tensor* t, egfem_interp_kind kind, double
     else
       k_interp_copy<float><<<grid, 256, 0, s>>>((const float*)u, (float*)w, n, mode, p);
     count_launch();
-  } else if (kind == EGFEM_INTERP_RECIPROCAL) {  // W = P0, V = P1: at the centroid
+  } else if (kind == EGFEM_INTERP_RECIPROCAL || kind == EGFEM_INTERP_SQUARE) {  // cell-wise W, V = P1
     if (t->n_cells > 0) {
+      const int mode = kind == EGFEM_INTERP_RECIPROCAL ? 0 : 1;
       if (f64)
-        k_interp_recip_p0<double><<<nblk(t->n_cells), 256, 0, s>>>(t->vdofs, t->wdofs, t->n_cells, t->dim + 1,
-                                                                   (const double*)u, (double*)w, (double*)chain, p);
+        k_interp_points<double><<<nblk(t->n_cells, 128), 128, 0, s>>>(t->vdofs, t->wdofs, t->wpts, t->n_cells, t->dim + 1,
+                                                                 t->nwc, (const double*)u, (double*)w, (double*)chain,
+                                                                 mode, p);
       else
-        k_interp_recip_p0<float><<<nblk(t->n_cells), 256, 0, s>>>(t->vdofs, t->wdofs, t->n_cells, t->dim + 1,
-                                                                  (const float*)u, (float*)w, (float*)chain, p);
+        k_interp_points<float><<<nblk(t->n_cells, 128), 128, 0, s>>>(t->vdofs, t->wdofs, t->wpts, t->n_cells, t->dim + 1,
+                                                                t->nwc, (const float*)u, (float*)w, (float*)chain,
+                                                                mode, p);
       count_launch();
     }
   } else if (kind == EGFEM_INTERP_GRADPOW_P0 || kind == EGFEM_INTERP_MINSURF_P0) {
@@ -722,7 +743,7 @@ egfem_status launch_interp(const egfem_tensor* t, egfem_interp_kind kind, double
 #define EGFEM_GP3(S, D, SA, IO)                                                                       \
   k_interp_gradpow<S, D, SA, IO><<<grid, 128, 0, s>>>(D == 3 ? t->coords4 : t->coords, t->cells, t->vdofs,   \
                                                       t->wdofs, t->n_cells, (const S*)u, (S*)w, (S*)chain, p, \
-                                                      kind == EGFEM_INTERP_MINSURF_P0)
+                                                      kind == EGFEM_INTERP_MINSURF_P0, t->nwc)
 #define EGFEM_GP(S, D)                                                          \
   do {                                                                          \
     if (t->vdofs_is_cells && t->wdofs_is_iota) EGFEM_GP3(S, D, true, true);     \

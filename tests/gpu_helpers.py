@@ -6,6 +6,12 @@ import egfem_inputs as I
 SIX_PT = (0.445948490915965, 0.2233815896780118, 0.091576213509770549, 0.10995174365532154)
 
 
+def needs_chain(pr):
+    """Cell-wise W (P0 or QUAD) kinds carry D_u w as per-DOF chain rows (include/egfem.h)."""
+    return pr.W.family in (I.P0, I.QUAD) and pr.interp in (I.INTERP_GRADPOW_P0, I.INTERP_MINSURF_P0,
+                                                          I.INTERP_RECIPROCAL, I.INTERP_SQUARE)
+
+
 def gpu_pass(eg, t, pr, u_np, newton=True, fused=False, dtype=None):
     """interp → apply → jacobian on the GPU for problem `pr`; returns host arrays."""
     import torch
@@ -14,7 +20,7 @@ def gpu_pass(eg, t, pr, u_np, newton=True, fused=False, dtype=None):
     u = torch.tensor(u_np, dtype=td, device=dev)
     w = torch.empty(t.n_f, dtype=td, device=dev)
     chain = None
-    if pr.W.family == I.P0 and pr.interp in (I.INTERP_GRADPOW_P0, I.INTERP_MINSURF_P0, I.INTERP_RECIPROCAL):
+    if needs_chain(pr):
         chain = torch.empty(t.n_f * (pr.mesh.dim + 1), dtype=td, device=dev)
     eg.egfem_interp(t, pr.interp, pr.p, u, w, chain)
     r = torch.empty(t.n_u, dtype=td, device=dev)

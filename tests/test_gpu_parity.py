@@ -46,14 +46,16 @@ def _build_both(eg, orc, pr, dtype=0, rows=None):
 
 
 def _maps_kw(pr):
-    p0 = pr.W.family == I.P0
+    p0 = pr.W.family in (I.P0, I.QUAD)  # cell-wise W: loc map; W = V numbering: slot_ik
     return dict(slot_ik=not p0, loc=p0)
 
 
 SMALL = [("cfg1", None), ("cfg2", None), ("cfg3", None), ("cfg4", None), ("cfg5", None),
          ("cfg2", 7), ("cfg3", 5), ("cfg4", 3), ("cfg4", 1), ("cfg3", 1), ("cfg1", 1), ("cfg5", 1),
          # SURVEY §8(f) F1 pointwise kinds: minimal surface (P0 W) and biochemical σ/(k+u) (W = P1, P0)
-         ("minsurf2d", None), ("minsurf3d", None), ("minsurf3d", 2), ("biochem_p1", None), ("biochem_p0", None)]
+         ("minsurf2d", None), ("minsurf3d", None), ("minsurf3d", 2), ("biochem_p1", None), ("biochem_p0", None),
+         # SURVEY §8(f) F2 quadrature-embedded W = I_k (Case 3)
+         ("quadratic_i4", None), ("biochem_i2", None), ("plap_i1", None), ("plap3d_i2", None), ("plap3d_i2", 2)]
 
 
 @pytest.mark.parametrize("name,n", SMALL)

@@ -617,3 +617,75 @@ def test_f1_newton_vs_finite_differences(oracle_mod, case):
     assert rel_l2(J, Jfd) < 1e-8
     if pr.interp == I.INTERP_MINSURF_P0:
         assert rel_l2(J, J.T) < 1e-14
+
+
+# ----------------------------------------------------------------------------- F2 quadrature-embedded W = I_k
+# Reference rules typed here from the literature (Strang–Fix 3-point, Dunavant 6-point degree 4,
+# the 4-point tetrahedral degree-2 rule), independent of the oracle's own tables.
+RULE_3 = ([2 / 3, 1 / 6, 1 / 6, 1 / 6, 2 / 3, 1 / 6, 1 / 6, 1 / 6, 2 / 3], [1 / 3] * 3)
+_A6, _B6 = 0.445948490915965, 0.091576213509771
+RULE_6 = ([1 - 2 * _A6, _A6, _A6, _A6, 1 - 2 * _A6, _A6, _A6, _A6, 1 - 2 * _A6,
+           1 - 2 * _B6, _B6, _B6, _B6, 1 - 2 * _B6, _B6, _B6, _B6, 1 - 2 * _B6],
+          [0.223381589678011] * 3 + [0.109951743655322] * 3)
+
+
+def test_table1_i4_space_size(oracle_mod):
+    """PAPER.md Table 1: EGFEM (I4) has 4225 + 6·8192 = 53377 unknowns on the 64×64 mesh (N_f = N_q·N_el, L139)."""
+    m = I.mesh_square(64)
+    assert I.space_p1(m).n_dofs + I.space_quad(m, 6).n_dofs == 53377
+
+
+@pytest.mark.parametrize("case", ["square_i4", "recip_i2"])
+def test_case3_equivalence_with_sga_rule(oracle_mod, case):
+    """Case 3: with W = I_k and w = f(u_h) at the rule's points, T:(u⊗w)
+    reproduces the SGA term ∫ φ_i u f(u) evaluated with that same rule, to rounding."""
+    m = jitter(I.mesh_square(4), 0.2, 21)
+    V = I.space_p1(m)
+    rule, nq, kind, k, f = {"square_i4": (RULE_6, 6, I.INTERP_SQUARE, 0.0, lambda x: x * x),
+                            "recip_i2": (RULE_3, 3, I.INTERP_RECIPROCAL, 1.0, lambda x: 1.0 / (1.0 + x))}[case]
+    T = oracle_mod.OracleTensor(m, V, I.space_quad(m, nq), I.FORM_MASS3)
+    assert T.n_f == nq * m.n_cells
+    u = 0.5 + np.random.default_rng(22).uniform(0.0, 1.0, V.n_dofs)
+    r = T.apply(u, T.interp(kind, k, u))
+    assert rel_l2(r, brute.sga_rule_mass(m, u, f, *rule)) < 1e-13
+
+
+def test_i4_quadratic_is_exact(oracle_mod):
+    """§5.1 (Table 1 'EGFEM (I4)'): the 6-point rule is exact to degree 4, so
+    M:(u⊗w) with w = u_h² at its points equals the exact integral ∫ φ_i u_h³ of the SGA."""
+    m = jitter(I.mesh_square(3), 0.2, 23)
+    V = I.space_p1(m)
+    T = oracle_mod.OracleTensor(m, V, I.space_quad(m, 6), I.FORM_MASS3)
+    u = np.random.default_rng(24).standard_normal(V.n_dofs)
+    r = T.apply(u, T.interp(I.INTERP_SQUARE, 0.0, u))
+    assert rel_l2(r, brute.sga_cubic_mass(m, u)) < 1e-13
+
+
+@pytest.mark.parametrize("dim,nq", [(2, 1), (2, 3), (3, 4)])
+def test_plap_quad_equals_p0(oracle_mod, dim, nq):
+    """PAPER.md L148/L616 (reading C20): I_1 and P0 give the same p-Laplace tensor values; for any
+    rule (weights summing to 1) the P1 gradient is constant per cell, so r(I_k) = r(P0)."""
+    m = jitter(I.mesh_square(4) if dim == 2 else I.mesh_cube(2), 0.2, 25)
+    V = I.space_p1(m)
+    Tq = oracle_mod.OracleTensor(m, V, I.space_quad(m, nq), I.FORM_PLAP)
+    T0 = oracle_mod.OracleTensor(m, V, I.space_p0(m), I.FORM_PLAP)
+    u = np.random.default_rng(26).standard_normal(V.n_dofs)
+    p = 3.0
+    rq = Tq.apply(u, Tq.interp(I.INTERP_GRADPOW_P0, p, u))
+    r0 = T0.apply(u, T0.interp(I.INTERP_GRADPOW_P0, p, u))
+    assert rel_l2(rq, r0) < 1e-14
+    if nq == 1:
+        assert np.abs(Tq.export()["t_val"] - T0.export()["t_val"]).max() < 1e-16
+
+
+@pytest.mark.parametrize("case", ["quadratic_i4", "biochem_i2", "plap_i1", "plap3d_i2"])
+def test_f2_newton_vs_finite_differences(oracle_mod, case):
+    """J = T·w + (T·₂u)·D_u w with w at the quadrature points equals central differences of r(u)."""
+    pr = I.make_problem(case, n={"quadratic_i4": 3, "biochem_i2": 3, "plap_i1": 4, "plap3d_i2": 2}[case])
+    m = jitter(pr.mesh, 0.15, 2)
+    T = oracle_mod.OracleTensor(m, pr.V, pr.W, pr.form)
+    u = pr.u
+    w = T.interp(pr.interp, pr.p, u)
+    J = _csr_dense(T, T.jacobian(I.JAC_NEWTON, pr.interp, pr.p, u, w))
+    Jfd = _fd_jacobian(T, pr.interp, pr.p, u, 1e-5)
+    assert rel_l2(J, Jfd) < (1e-6 if pr.form == I.FORM_PLAP else 1e-8)
