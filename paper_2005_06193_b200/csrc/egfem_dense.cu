@@ -93,65 +93,73 @@ __device__ __forceinline__ void cp16_dense(void* dst, const void* src) {
                : "memory");
 }
 
-constexpr int kBlkBytes = (kDenseMaxN * (kDenseMaxN + 1) * 8 + 32 + 15) & ~15;  // one staged block (+ slack)
+// One launch per stencil width N (rows grouped by N offline, `dense_rows`, and their blocks
+// stored contiguously in that order), so every instance holds exactly 2N W values per lane and
+// the narrow stencils run at high occupancy.  CTA c walks a contiguous range of its class's
+// rows (listed in row order: neighbours share most of their stencil, U/W lines are reused from
+// L1) RB rows at a time: the next RB blocks (one contiguous span) and stencil columns are
+// copied into shared memory by cp.async while this batch is used; its warps take the 64-pair
+// chunks of each row.
+template <int N, typename S>
+struct DenseTile {
+  static constexpr int NP = N + (N & 1);
+  static constexpr int RB = N > 0 ? ((2048 / (N * NP)) > 0 ? (2048 / (N * NP)) : 1) : 1;  // rows per stage
+  static constexpr int BYTES = (RB * N * NP * (int)sizeof(S) + 32 + 15) & ~15;
+};
 
-// CTA c walks the contiguous rows [c·R, (c+1)·R) in order (neighbouring rows share most of
-// their stencil: U/W lines are reused from L1); its warps take the 64-pair chunks of each
-// row.  The next row's block is copied into shared memory (cp.async) while this one is used.
-template <typename S, bool NM>
-__global__ void __launch_bounds__(128) k_dense(const DenseArgs<S> A) {
-  __shared__ __align__(16) unsigned char s_blk[2][kBlkBytes];
-  __shared__ int32_t s_cols[2][kDenseMaxN];
+template <typename S, int N, bool NM>
+__global__ void __launch_bounds__(128) k_dense(const DenseArgs<S> A, const int32_t* __restrict__ rows, int64_t nrows,
+                                              int64_t blk0) {
+  using TL = DenseTile<N, S>;
+  constexpr int NP = TL::NP, RB = TL::RB;
+  __shared__ __align__(16) unsigned char s_blk[2][N > 0 ? TL::BYTES : 16];
+  __shared__ int32_t s_cols[2][N > 0 ? RB * N : 1];
   const int warp = threadIdx.x >> 5, lane = threadIdx.x & 31;
   const int nwarps = blockDim.x >> 5;
   const int nchunks = (A.B + 63) / 64;
-  const int64_t per = (A.n_u + gridDim.x - 1) / gridDim.x;
-  const int64_t r0 = (int64_t)blockIdx.x * per;
-  const int64_t r1 = min(A.n_u, r0 + per);
-  if (r0 >= r1) return;
-  // copy row `row`'s block (16-byte aligned span) into buffer b; returns the element shift
-  auto stage = [&](int64_t row, int b) -> int {
-    if (row >= r1) return 0;
-    {  // the row's stencil columns (plain loads: at most kDenseMaxN, written before the barrier)
-      const int64_t f0 = __ldg(A.row_fib + row), f1 = __ldg(A.row_fib + row + 1);
-      for (int x = threadIdx.x; x < (int)(f1 - f0); x += blockDim.x) s_cols[b][x] = __ldg(A.fib_j + f0 + x);
-    }
-    const int64_t o0 = __ldg(A.blk_off + row), o1 = __ldg(A.blk_off + row + 1);
-    const uint64_t a0 = reinterpret_cast<uint64_t>(A.blk + o0), a1 = reinterpret_cast<uint64_t>(A.blk + o1);
-    const uint64_t lo = a0 & ~uint64_t(15);
-    const int chunks = (int)((((a1 + 15) & ~uint64_t(15)) - lo) >> 4);
-    for (int q = threadIdx.x; q < chunks; q += blockDim.x)
-      cp16_dense(&s_blk[b][16 * q], reinterpret_cast<const char*>(lo) + 16 * q);
-    return (int)((a0 - lo) / sizeof(S));
-  };
-  int sh_cur = stage(r0, 0);
-  asm volatile("cp.async.commit_group;" ::: "memory");
-  int st = 0;
-  for (int64_t row = r0; row < r1; ++row) {
-    const int sh_nxt = stage(row + 1, st ^ 1);
-    asm volatile("cp.async.commit_group;" ::: "memory");
-    asm volatile("cp.async.wait_group 1;" ::: "memory");
-    __syncthreads();  // this row's block is in s_blk[st] for every warp
-    const int n = (int)(__ldg(A.row_fib + row + 1) - __ldg(A.row_fib + row));
-    const S* M = reinterpret_cast<const S*>(s_blk[st]) + sh_cur;
-    const int32_t* cols = s_cols[st];
-    for (int ch = warp; ch < nchunks; ch += nwarps) {
-      const int p0 = ch * 64 + lane;
-      switch (n) {
-#define EGFEM_DR(N_) \
-  case N_: dense_row<S, N_, NM>(A, row, cols, M, p0); break;
-        EGFEM_DR(1) EGFEM_DR(2) EGFEM_DR(3) EGFEM_DR(4) EGFEM_DR(5) EGFEM_DR(6) EGFEM_DR(7) EGFEM_DR(8)
-        EGFEM_DR(9) EGFEM_DR(10) EGFEM_DR(11) EGFEM_DR(12) EGFEM_DR(13) EGFEM_DR(14) EGFEM_DR(15)
-        EGFEM_DR(16) EGFEM_DR(17) EGFEM_DR(18) EGFEM_DR(19) EGFEM_DR(20)
-#undef EGFEM_DR
-        default:  // empty row
-          if (p0 < A.B) A.R[at<NM>(row, p0, A.B, A.n_u)] = S(0);
-          if (p0 + 32 < A.B) A.R[at<NM>(row, p0 + 32, A.B, A.n_u)] = S(0);
+  const int64_t per = (nrows + gridDim.x - 1) / gridDim.x;
+  const int64_t q0 = (int64_t)blockIdx.x * per;
+  const int64_t q1 = min(nrows, q0 + per);
+  if (q0 >= q1) return;
+  if constexpr (N == 0) {  // empty rows
+    for (int64_t q = q0; q < q1; ++q)
+      for (int p = threadIdx.x; p < A.B; p += blockDim.x) A.R[at<NM>(rows[q], p, A.B, A.n_u)] = S(0);
+    return;
+  } else {
+    // stage entries [q, min(q + RB, q1)) of the class list into buffer b; returns the shift
+    auto stage = [&](int64_t q, int b) -> int {
+      if (q >= q1) return 0;
+      const int nr = (int)(q1 - q < (int64_t)RB ? q1 - q : (int64_t)RB);
+      for (int x = threadIdx.x; x < nr * N; x += blockDim.x) {
+        const int64_t row = __ldg(rows + q + x / N);
+        s_cols[b][x] = __ldg(A.fib_j + __ldg(A.row_fib + row) + x % N);
       }
+      const uint64_t a0 = reinterpret_cast<uint64_t>(A.blk + blk0 + q * (N * NP));
+      const uint64_t lo = a0 & ~uint64_t(15);
+      const int chunks = (int)((((a0 + (uint64_t)nr * N * NP * sizeof(S) + 15) & ~uint64_t(15)) - lo) >> 4);
+      for (int c = threadIdx.x; c < chunks; c += blockDim.x)
+        cp16_dense(&s_blk[b][16 * c], reinterpret_cast<const char*>(lo) + 16 * c);
+      return (int)((a0 - lo) / sizeof(S));
+    };
+    int sh_cur = stage(q0, 0);
+    asm volatile("cp.async.commit_group;" ::: "memory");
+    int st = 0;
+    for (int64_t q = q0; q < q1; q += RB) {
+      const int sh_nxt = stage(q + RB, st ^ 1);
+      asm volatile("cp.async.commit_group;" ::: "memory");
+      asm volatile("cp.async.wait_group 1;" ::: "memory");
+      __syncthreads();  // this batch's blocks and columns are in buffer st for every warp
+      const int nr = (int)(q1 - q < (int64_t)RB ? q1 - q : (int64_t)RB);
+      const S* M = reinterpret_cast<const S*>(s_blk[st]) + sh_cur;
+      for (int r = 0; r < nr; ++r) {
+        const int64_t row = __ldg(rows + q + r);
+        for (int ch = warp; ch < nchunks; ch += nwarps)
+          dense_row<S, N, NM>(A, row, s_cols[st] + r * N, M + r * (N * NP), ch * 64 + lane);
+      }
+      __syncthreads();  // every warp is done with buffer st before it is refilled
+      sh_cur = sh_nxt;
+      st ^= 1;
     }
-    __syncthreads();  // every warp is done with s_blk[st] before it is refilled
-    sh_cur = sh_nxt;
-    st ^= 1;
   }
 }
 
@@ -199,20 +207,39 @@ egfem_status launch_dense(const egfem_tensor* t, int32_t batch, egfem_layout lay
   const int chunks = (batch + 63) / 64;
   const int threads = 32 * std::min(4, chunks);
   const bool nm = layout == EGFEM_LAYOUT_NODE_MAJOR;
-  // one wave of resident CTAs, each walking a contiguous block of rows
-#define EGFEM_D(S_)                                                                                      \
-  {                                                                                                     \
-    DenseArgs<S_> A{t->n_u, t->n_f, batch, t->row_fib, t->fib_j, t->blk_off, (const S_*)t->blk,        \
-                    (const S_*)U, (const S_*)W, (S_*)R};                                                \
-    auto fn = nm ? k_dense<S_, true> : k_dense<S_, false>;                                              \
-    int per_sm = 0;                                                                                     \
-    EGFEM_CUDA_TRY(cudaOccupancyMaxActiveBlocksPerMultiprocessor(&per_sm, fn, threads, 0));             \
-    const int grid = (int)std::min<int64_t>(t->n_u, (int64_t)std::max(per_sm, 1) * g_sms_dense[dev]);  \
-    fn<<<grid, threads, 0, s>>>(A);                                                                     \
+  // one launch per stencil width; each a single wave of resident CTAs over its row list
+  for (const auto& cls : t->dense_classes) {
+    const int n = (int)cls[0];
+    const int64_t start = cls[1], count = cls[2];
+    const int32_t* rows = t->dense_rows + start;
+#define EGFEM_DN(S_, N_)                                                                                       \
+  case N_: {                                                                                                  \
+    DenseArgs<S_> A{t->n_u, t->n_f, batch, t->row_fib, t->fib_j, t->blk_off, (const S_*)t->blk,              \
+                    (const S_*)U, (const S_*)W, (S_*)R};                                                      \
+    auto fn = nm ? k_dense<S_, N_, true> : k_dense<S_, N_, false>;                                            \
+    int per_sm = 0;                                                                                           \
+    EGFEM_CUDA_TRY(cudaOccupancyMaxActiveBlocksPerMultiprocessor(&per_sm, fn, threads, 0));                   \
+    const int grid = (int)std::min<int64_t>(count, (int64_t)std::max(per_sm, 1) * g_sms_dense[dev]);         \
+    fn<<<grid, threads, 0, s>>>(A, rows, count, cls[3]);                                                      \
+    break;                                                                                                    \
   }
-  if (t->dtype == EGFEM_F64) EGFEM_D(double) else EGFEM_D(float)
-#undef EGFEM_D
-  count_launch();
+#define EGFEM_DALL(S_)                                                                                         \
+  switch (n) {                                                                                                \
+    EGFEM_DN(S_, 0) EGFEM_DN(S_, 1) EGFEM_DN(S_, 2) EGFEM_DN(S_, 3) EGFEM_DN(S_, 4) EGFEM_DN(S_, 5)          \
+    EGFEM_DN(S_, 6) EGFEM_DN(S_, 7) EGFEM_DN(S_, 8) EGFEM_DN(S_, 9) EGFEM_DN(S_, 10) EGFEM_DN(S_, 11)        \
+    EGFEM_DN(S_, 12) EGFEM_DN(S_, 13) EGFEM_DN(S_, 14) EGFEM_DN(S_, 15) EGFEM_DN(S_, 16) EGFEM_DN(S_, 17)   \
+    EGFEM_DN(S_, 18) EGFEM_DN(S_, 19) EGFEM_DN(S_, 20)                                                        \
+    default: set_error("dense stencil wider than 20"); return EGFEM_ERR_UNSUPPORTED;                         \
+  }
+    if (t->dtype == EGFEM_F64) {
+      EGFEM_DALL(double)
+    } else {
+      EGFEM_DALL(float)
+    }
+#undef EGFEM_DALL
+#undef EGFEM_DN
+    count_launch();
+  }
   EGFEM_CUDA_TRY(cudaGetLastError());
   return EGFEM_OK;
 }
@@ -220,11 +247,25 @@ egfem_status launch_dense(const egfem_tensor* t, int32_t batch, egfem_layout lay
 // Offline dense blocks for W = V tensors whose stencils are at most kDenseMaxN wide.
 egfem_status make_dense_blocks(egfem_tensor* t, const std::vector<int64_t>& hrf) {
   if (!t->w_is_v || t->n_u <= 0 || t->nnz <= 0 || t->max_row_fib > kDenseMaxN) return EGFEM_OK;
-  std::vector<int64_t> off(t->n_u + 1, 0);
-  for (int64_t i = 0; i < t->n_u; ++i) {
-    const int64_t n = hrf[i + 1] - hrf[i];
-    off[i + 1] = off[i] + n * (n + (n & 1));
+  // rows grouped by stencil width (stable: row order within a width); blocks stored in that order
+  std::vector<int32_t> order(t->n_u);
+  std::vector<int64_t> cnt(kDenseMaxN + 2, 0);
+  for (int64_t i = 0; i < t->n_u; ++i) cnt[hrf[i + 1] - hrf[i] + 1]++;
+  for (int n = 0; n <= kDenseMaxN; ++n) cnt[n + 1] += cnt[n];
+  std::vector<int64_t> first(cnt.begin(), cnt.end() - 1);
+  for (int64_t i = 0; i < t->n_u; ++i) order[first[hrf[i + 1] - hrf[i]]++] = (int32_t)i;
+  std::vector<int64_t> off(t->n_u + 1, 0);  // off[i]: block of row i; off[n_u]: total
+  int64_t pos = 0;
+  t->dense_classes.clear();
+  for (int n = 0; n <= kDenseMaxN; ++n) {
+    if (cnt[n + 1] == cnt[n]) continue;
+    t->dense_classes.push_back({n, cnt[n], cnt[n + 1] - cnt[n], pos});
+    for (int64_t q = cnt[n]; q < cnt[n + 1]; ++q) {
+      off[order[q]] = pos;
+      pos += (int64_t)n * (n + (n & 1));
+    }
   }
+  off[t->n_u] = pos;
   const size_t vs = t->dtype == EGFEM_F64 ? 8 : 4;
   EGFEM_CUDA_TRY(cudaMalloc(&t->blk_off, 8 * (t->n_u + 1)));
   EGFEM_CUDA_TRY(cudaMemcpy(t->blk_off, off.data(), 8 * (t->n_u + 1), cudaMemcpyHostToDevice));
@@ -249,7 +290,11 @@ egfem_status make_dense_blocks(egfem_tensor* t, const std::vector<int64_t>& hrf)
     cudaFree(t->blk);
     t->blk_off = nullptr;
     t->blk = nullptr;
+    t->dense_classes.clear();
+    return EGFEM_OK;
   }
+  EGFEM_CUDA_TRY(cudaMalloc(&t->dense_rows, sizeof(int32_t) * t->n_u));
+  EGFEM_CUDA_TRY(cudaMemcpy(t->dense_rows, order.data(), sizeof(int32_t) * t->n_u, cudaMemcpyHostToDevice));
   return EGFEM_OK;
 }
 
