@@ -11,8 +11,9 @@
 //   r_i  = Σ_K w_K B_iK
 // with one w gather per cell, and the Jacobian terms
 //   t_{i v_m K} = T_{i v_m K} w_K [+ B_iK (D_u w)_{K m}]
-// are scattered once into the row's canonical positions and summed per CSR fiber in
-// canonical order by the lane owning the fiber.  Per nonzero the stream carries the value
+// go either to the diagonal fiber (i, i) — one nonzero per cell, summed in registers and
+// reduced by a butterfly — or, scattered once into the row's canonical positions, to the short
+// off-diagonal fibers, which the lane owning the fiber sums in canonical order.  Per nonzero the stream carries the value
 // and a 16-bit (fiber, canonical position) pair; per cell the 32-bit K.
 //
 // Layout per row group (G lanes, CPL cells per lane — lane l takes cells l, l+G, l+2G, so one
@@ -46,6 +47,7 @@ struct CellArgs {
   const S* chain;          // (D_u w)_{K m}, N_f x (d+1)
   S* r;
   S* csr;
+  int64_t diag_off;        // column of row i's diagonal = i + diag_off (local tensors of a partition)
 };
 
 __device__ __forceinline__ uint32_t smem_u32(const void* p) { return (uint32_t)__cvta_generic_to_shared(p); }
@@ -129,16 +131,16 @@ __device__ __forceinline__ void load_cell(const S* p, bool vec, S* out) {
 }
 // the D1 values of one cell from global memory (16-byte read-only vector loads; D1·sizeof(S) % 16 == 0)
 template <typename S, int D1>
-__device__ __forceinline__ void load_cell_ldg(const S* p, bool ok, S* out) {
+__device__ __forceinline__ void load_cell_ldg(const S* p, S* out) {
   constexpr int NV = D1 * (int)sizeof(S) / 16;
 #pragma unroll
   for (int v = 0; v < NV; ++v) {
     if constexpr (sizeof(S) == 8) {
-      const double2 x = ok ? __ldg(reinterpret_cast<const double2*>(p) + v) : make_double2(0.0, 0.0);
+      const double2 x = __ldg(reinterpret_cast<const double2*>(p) + v);
       out[2 * v] = x.x;
       out[2 * v + 1] = x.y;
     } else {
-      const float4 x = ok ? __ldg(reinterpret_cast<const float4*>(p) + v) : make_float4(0.f, 0.f, 0.f, 0.f);
+      const float4 x = __ldg(reinterpret_cast<const float4*>(p) + v);
       out[4 * v] = x.x;
       out[4 * v + 1] = x.y;
       out[4 * v + 2] = x.z;
@@ -215,13 +217,15 @@ __global__ void __launch_bounds__(256, (JAC == kJacNone || G >= 16) ? 3 : 2) k_c
     for (int q = 0; q < FREG; ++q) {
       const int f = lane + q * G;
       const bool ok = f < (int)(m.f1 - m.f0);
-      fj[q] = (kU && ok) ? __ldg(A.fib_j + m.f0 + f) : -1;
-      fb[q] = ok ? (int)(__ldg(A.fib_nz + m.f0 + f) - m.e0) : 0;
+      fj[q] = ((kU || kJ) && ok) ? __ldg(A.fib_j + m.f0 + f) : -1;
+      fb[q] = ok ? (int)__ldg(A.fib_nz + m.f0 + f) : 0;  // raw offset: e0 is subtracted at use (no stall now)
     }
   };
+  // unconditional (clamped) loads: a select on the loaded value would stall right here; the
+  // value of a lane without a fiber is never shuffled out
   auto ucols = [&](const int* fj, S* uj) {
 #pragma unroll
-    for (int q = 0; q < FREG; ++q) uj[q] = (kU && fj[q] >= 0) ? __ldg(A.u + fj[q]) : S(0);
+    for (int q = 0; q < FREG; ++q) uj[q] = kU ? __ldg(A.u + (fj[q] >= 0 ? fj[q] : 0)) : S(0);
   };
   auto stage_in = [&](uint32_t dst, const Meta& m, int& sk, int& sv, int& sb) {
     const int n = (int)(m.e1 - m.e0);
@@ -270,16 +274,30 @@ __global__ void __launch_bounds__(256, (JAC == kJacNone || G >= 16) ? 3 : 2) k_c
       const uint32_t K = ok ? bk[q] : 0u;
       wk[c] = ok ? __ldg(A.w + K) : S(0);
       if constexpr (kN) {
-        if constexpr ((D1 * sizeof(S)) % 16 == 0) {  // the cell's D1 values: 16-byte vector loads
-          const S* src = A.chain + (size_t)K * D1;
-          load_cell_ldg<S, D1>(src, ok, dd[c]);
+        // the cell's D1 values (16-byte vector loads); a lane past the row's cells loads cell 0's
+        // row and never uses it (no select on the loaded value)
+        if constexpr ((D1 * sizeof(S)) % 16 == 0) {
+          load_cell_ldg<S, D1>(A.chain + (size_t)K * D1, dd[c]);
         } else {
 #pragma unroll
-          for (int m = 0; m < D1; ++m) dd[c][m] = ok ? __ldg(A.chain + (size_t)K * D1 + m) : S(0);
+          for (int m = 0; m < D1; ++m) dd[c][m] = __ldg(A.chain + (size_t)K * D1 + m);
         }
       }
     }
     const bool vec_v = (reinterpret_cast<uintptr_t>(bv) & 15u) == 0;
+    // the diagonal fiber (i, i): one nonzero per cell of the row — summed in registers
+    int fd = -1;
+    if constexpr (kJ) {
+      const int64_t irow = row + A.diag_off;
+      const int goff = (threadIdx.x & 31) & ~(G - 1);
+      constexpr unsigned GM = (G == 32) ? 0xffffffffu : ((1u << G) - 1u);
+#pragma unroll
+      for (int q = 0; q < FREG; ++q) {
+        const unsigned b = (__ballot_sync(FM, lane + q * G < nf && fj_cur[q] == irow) >> goff) & GM;
+        if (b) fd = q * G + __ffs(b) - 1;
+      }
+    }
+    S dacc = S(0);
     S acc = S(0);
 #pragma unroll
     for (int c = 0; c < CPL; ++c) {
@@ -327,7 +345,8 @@ __global__ void __launch_bounds__(256, (JAC == kJacNone || G >= 16) ? 3 : 2) k_c
           for (int m = 0; m < D1; ++m) {
             S t = xmul(tv[m], wk[c]);
             if constexpr (kN) t = xfma(B, dd[c][m], t);
-            s_t[bq[m] >> 8] = t;
+            if ((int)(bq[m] & 0xffu) == fd) dacc = xadd(dacc, t);
+            else s_t[bq[m] >> 8] = t;
           }
         }
       }
@@ -338,74 +357,24 @@ __global__ void __launch_bounds__(256, (JAC == kJacNone || G >= 16) ? 3 : 2) k_c
       if (lane == 0 && row < A.n_u) A.r[row] = acc;
     }
     if constexpr (kJ) {
-      // ---- fiber sums over the canonical positions: lane l owns positions l·NC .. l·NC+NC-1;
-      // the fiber heads (mask words hm) come from the fiber lanes' start positions
-      constexpr int NC = L::CE / G;
-      constexpr int NW = (L::CE + 31) / 32;
-      uint32_t hm[NW];
+      // ---- diagonal: lane partials (cell order) + butterfly; the other fibers: their lane sums
+      // the scattered terms in canonical order (a handful per fiber: the cells around an edge)
 #pragma unroll
-      for (int x = 0; x < NW; ++x) hm[x] = 0u;
+      for (int o = G / 2; o > 0; o >>= 1) dacc = xadd(dacc, __shfl_xor_sync(FM, dacc, o, G));
+      if (lane == 0 && fd >= 0) A.csr[cur.f0 + fd] = dacc;
+      __syncwarp();  // the scatter into s_t is complete
 #pragma unroll
       for (int q = 0; q < FREG; ++q) {
-        const int ya = fb_cur[q];
-        const bool h = lane + q * G < nf;
-#pragma unroll
-        for (int x = 0; x < NW; ++x) hm[x] |= (h && (ya >> 5) == x) ? (1u << (ya & 31)) : 0u;
-      }
-#pragma unroll
-      for (int x = 0; x < NW; ++x)
-#pragma unroll
-        for (int o = G / 2; o > 0; o >>= 1) hm[x] |= (uint32_t)__shfl_xor_sync(FM, (int)hm[x], o, G);
-      const int y0 = lane * NC;
-      // head bits of this lane's positions, and the heads before them
-      uint32_t hb = 0;
-      int before = 0;
-#pragma unroll
-      for (int x = 0; x < NW; ++x) {
-        const int lo = x * 32;
-        // bits of word x that fall in [y0, y0 + NC)
-        const int sh = lo - y0;
-        uint32_t part = 0u;
-        if (sh >= 0 && sh < NC) part = hm[x] << sh;
-        else if (sh < 0 && sh > -32) part = hm[x] >> (-sh);
-        hb |= part;
-        if (lo + 32 <= y0) before += __popc(hm[x]);
-        else if (lo < y0) before += __popc(hm[x] & ((1u << (y0 - lo)) - 1u));
-      }
-      const int nl = ne - y0;
-      hb &= (nl >= NC) ? (NC >= 32 ? 0xffffffffu : ((1u << NC) - 1u)) : (nl > 0 ? ((1u << nl) - 1u) : 0u);
-      __syncwarp();  // the scatter into s_t is complete
-      S tv[NC];
-      load_run<S, NC>(s_t + y0, tv);
-#pragma unroll
-      for (int c = 0; c < NC; ++c)
-        if (c >= nl) tv[c] = S(0);
-      const int fbase = before - 1;
-      S tail = S(0);
-#pragma unroll
-      for (int c = 0; c < NC; ++c) tail = ((hb >> c) & 1u) ? tv[c] : xadd(tail, tv[c]);
-      S sv = tail;
-      int fl = hb != 0;
-#pragma unroll
-      for (int o = 1; o < G; o <<= 1) {
-        const S ov = __shfl_up_sync(FM, sv, o, G);
-        const int of = __shfl_up_sync(FM, fl, o, G);
-        if (lane >= o) {
-          if (!fl) sv = xadd(ov, sv);
-          fl |= of;
+        const int f = lane + q * G;
+        const int fs = fb_cur[q] - (int)cur.e0;
+        const int nx_same = __shfl_sync(FM, fs, (lane + 1) % G, G);
+        const int nx_next = (q + 1 < FREG) ? __shfl_sync(FM, fb_cur[(q + 1) % FREG] - (int)cur.e0, 0, G) : ne;
+        if (f < nf && f != fd) {
+          const int yb = (f + 1 >= nf) ? ne : (lane + 1 < G ? nx_same : nx_next);
+          S a = S(0);
+          for (int y = fs; y < yb; ++y) a = xadd(a, s_t[y]);
+          A.csr[cur.f0 + f] = a;
         }
-      }
-      S run = __shfl_up_sync(FM, sv, 1, G);
-      if (lane == 0) run = S(0);
-      const unsigned nxh = (unsigned)__shfl_down_sync(FM, (int)(hb & 1u), 1, G);
-      // bit c: position c ends its fiber (the next position is a head or the row ends)
-      unsigned last = (hb >> 1) | (nxh << (NC - 1));
-      if (nl >= 1 && nl <= NC) last |= 1u << (nl - 1);
-      last &= (nl >= NC) ? ((1u << NC) - 1u) : (nl > 0 ? ((1u << nl) - 1u) : 0u);
-#pragma unroll
-      for (int c = 0; c < NC; ++c) {
-        run = ((hb >> c) & 1u) ? tv[c] : xadd(run, tv[c]);
-        if ((last >> c) & 1u) A.csr[cur.f0 + fbase + __popc(hb & ((2u << c) - 1u))] = run;
       }
     }
     __syncwarp();  // stage st and s_t are free for reuse
@@ -420,6 +389,7 @@ __global__ void __launch_bounds__(256, (JAC == kJacNone || G >= 16) ? 3 : 2) k_c
       uj_cur[q] = uj_nxt[q];
       fb_cur[q] = fb_nxt[q];
       fb_nxt[q] = fb_nn[q];
+      fj_cur[q] = fj_nxt[q];
       fj_nxt[q] = fj_nn[q];
     }
     st ^= 1;
@@ -528,6 +498,7 @@ egfem_status cells_dispatch(const egfem_tensor* t, bool do_r, int jac, const voi
   A.chain = static_cast<const S*>(chain);
   A.r = static_cast<S*>(r);
   A.csr = static_cast<S*>(csr);
+  A.diag_off = t->row_begin - t->col_begin;
   CellCfg c{};
   if (!pick_cells(t, &c)) {
     set_error("no cell-major configuration");

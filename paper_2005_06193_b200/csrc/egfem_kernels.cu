@@ -173,8 +173,9 @@ __global__ void __launch_bounds__(128) k_interp_gradpow(const double* __restrict
     }
   }
   // the cell's W DOFs (P0: one; QUAD: N_q points, ∇u_h is constant on the cell)
+  if (IOTA) nw = 1;  // canonical P0 (the IOTA instance is only launched for it)
   for (int l = 0; l < nw; ++l) {
-    const int64_t K = IOTA ? c * nw + l : (int64_t)__ldg(wdofs + c * nw + l);
+    const int64_t K = IOTA ? c : (int64_t)__ldg(wdofs + c * nw + l);
     w[K] = (S)wk;
     if (chain) {
       if constexpr (D == 3 && sizeof(S) == 8) {
