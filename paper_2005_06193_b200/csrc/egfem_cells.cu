@@ -18,8 +18,9 @@
 //
 // Layout per row group (G lanes, CPL cells per lane — lane l takes cells l, l+G, l+2G, so one
 // warp-wide gather touches a few neighbouring cells' lines — grid-stride rows): the next row's
-// (K, value, fiber|pos) slices are fetched with 16-byte cp.async.cg (L2 evict-first) into
-// the group's second shared-memory stage while the current row is reduced.  Every sum
+// (K, value, fiber|pos) slices are fetched into a second shared-memory stage while the current
+// row is reduced, by 16-byte cp.async.cg (L2 evict-first) or, when a warp holds >= 8 rows,
+// by three TMA bulk copies per warp (its rows are consecutive) completing on an mbarrier.  Every sum
 // runs in a fixed order: bitwise reproducible; fused and separate launches agree bitwise.
 #include <algorithm>
 #include <cstdio>
@@ -61,6 +62,40 @@ __device__ __forceinline__ void cp16(uint32_t dst, const void* src, uint64_t pol
                : "memory");
 }
 __device__ __forceinline__ void commit() { asm volatile("cp.async.commit_group;" ::: "memory"); }
+// TMA 1D bulk copies completing on an mbarrier (one lane per warp issues them)
+__device__ __forceinline__ void bar_init(uint64_t* bar) {
+  asm volatile("mbarrier.init.shared::cta.b64 [%0], 1;" ::"r"(smem_u32(bar)) : "memory");
+}
+__device__ __forceinline__ void bar_expect(uint64_t* bar, uint32_t bytes) {
+  asm volatile("mbarrier.arrive.expect_tx.shared::cta.b64 _, [%0], %1;" ::"r"(smem_u32(bar)), "r"(bytes) : "memory");
+}
+__device__ __forceinline__ void bar_wait(uint64_t* bar, uint32_t parity) {
+  asm volatile(
+      "{\n"
+      ".reg .pred p;\n"
+      "WAIT_%=:\n"
+      "mbarrier.try_wait.parity.shared::cta.b64 p, [%0], %1;\n"
+      "@!p bra WAIT_%=;\n"
+      "}\n" ::"r"(smem_u32(bar)),
+      "r"(parity)
+      : "memory");
+}
+__device__ __forceinline__ void bulk_copy(uint32_t dst, const void* src, uint32_t bytes, uint64_t* bar, uint64_t pol) {
+  asm volatile(
+      "cp.async.bulk.shared::cluster.global.mbarrier::complete_tx::bytes.L2::cache_hint [%0], [%1], %2, [%3], %4;" ::"r"(
+          dst),
+      "l"(src), "r"(bytes), "r"(smem_u32(bar)), "l"(pol)
+      : "memory");
+}
+// 16-byte-aligned span around [p, p+n): start, byte count; returns the element shift
+template <typename T>
+__device__ __forceinline__ int span16(const T* p, int n, const char** lo_out, uint32_t* bytes) {
+  const uint64_t a = reinterpret_cast<uint64_t>(p);
+  const uint64_t lo = a & ~uint64_t(15);
+  *bytes = n > 0 ? (uint32_t)(((a + (uint64_t)n * sizeof(T) + 15) & ~uint64_t(15)) - lo) : 0u;
+  *lo_out = reinterpret_cast<const char*>(lo);
+  return (int)((a - lo) / sizeof(T));
+}
 __device__ __forceinline__ void wait_prev() { asm volatile("cp.async.wait_group 1;" ::: "memory"); }
 
 // 16-byte async copies of the span around [p, p+n) to shared address dst; returns the shift.
@@ -85,6 +120,10 @@ __device__ __forceinline__ float xadd(float a, float b) { return __fadd_rn(a, b)
 __device__ __forceinline__ double xfma(double a, double b, double c) { return __fma_rn(a, b, c); }
 __device__ __forceinline__ float xfma(float a, float b, float c) { return __fmaf_rn(a, b, c); }
 
+// Shared memory per row group: two stages of (K, value, fiber|pos) slices and the Jacobian
+// scratch.  With warp-level bulk staging the 32/G groups of a warp pool their stage regions
+// into one warp stage per buffer (the warp's rows are consecutive, so their slices are one
+// contiguous span per array) and the warp's two mbarriers sit in group 0's tail.
 template <typename S, int D1, int G, int CPL, bool JT>
 struct CellSmem {
   static constexpr int CC = G * CPL;  // cells per row (max)
@@ -96,7 +135,18 @@ struct CellSmem {
   static constexpr int st_b = (st_v + CE * (int)sizeof(S) + 32 + 15) & ~15;
   static constexpr int stage = (st_b + CE * 2 + 32 + 15) & ~15;
   static constexpr int o_t = 2 * stage;  // S[CE]: Jacobian terms at canonical positions
+  // warp stage (bulk): WPG groups' slices back to back, each array with 32 B of slack
+  static constexpr int WPG = 32 / G;
+  static constexpr int w_k = 0;
+  static constexpr int w_v = (w_k + WPG * CC * 4 + 32 + 15) & ~15;
+  static constexpr int w_b = (w_v + WPG * CE * (int)sizeof(S) + 32 + 15) & ~15;
+  static constexpr int wstage = (w_b + WPG * CE * 2 + 32 + 15) & ~15;
   static constexpr int raw = (o_t + (JT ? CE * (int)sizeof(S) : 0) + 15) & ~15;  // s_t only with a Jacobian
+  // per-warp layout for bulk staging: [2 warp stages][WPG x s_t][2 mbarriers]
+  static constexpr int wo_t = 2 * wstage;
+  static constexpr int wo_bar = (wo_t + (JT ? WPG * CE * (int)sizeof(S) : 0) + 15) & ~15;
+  static constexpr int wraw = wo_bar + 16;
+  static constexpr int wbytes = wraw + ((16 - wraw % 128) + 128) % 128;
   // group stride = 16 (mod 128): the groups of a warp start on different bank quads, so
   // their same-offset accesses do not collide
   static constexpr int bytes = raw + ((16 - raw % 128) + 128) % 128;
@@ -188,7 +238,7 @@ __device__ __forceinline__ Meta meta(const CellArgs<S>& A, int64_t row) {
   return m;
 }
 
-template <typename S, int D1, int G, int CPL, int FREG, bool DO_R, int JAC>
+template <typename S, int D1, int G, int CPL, int FREG, bool DO_R, int JAC, bool WB>
 __global__ void __launch_bounds__(256, (JAC == kJacNone || G >= 16) ? 3 : 2) k_cell(const CellArgs<S> A) {
   using L = CellSmem<S, D1, G, CPL, JAC != kJacNone>;
   constexpr int GPB = 256 / G;
@@ -201,9 +251,13 @@ __global__ void __launch_bounds__(256, (JAC == kJacNone || G >= 16) ? 3 : 2) k_c
   extern __shared__ __align__(16) unsigned char smem[];
   const int lane = threadIdx.x % G;
   const int grp = threadIdx.x / G;
-  unsigned char* gs = smem + grp * L::bytes;
+  // WB: the warp's region holds its two stages, its groups' s_t and its mbarriers
+  unsigned char* gs = WB ? smem + (threadIdx.x >> 5) * L::wbytes : smem + grp * L::bytes;
   const uint32_t gs_s = smem_u32(gs);
-  S* s_t = reinterpret_cast<S*>(gs + L::o_t);
+  S* s_t = reinterpret_cast<S*>(WB ? gs + L::wo_t + (grp % L::WPG) * L::CE * (int)sizeof(S) : gs + L::o_t);
+  uint64_t* bars = reinterpret_cast<uint64_t*>(gs + L::wo_bar);
+  constexpr int STG = WB ? L::wstage : L::stage;
+  constexpr int SK = WB ? L::w_k : L::st_k, SV = WB ? L::w_v : L::st_v, SB = WB ? L::w_b : L::st_b;
   const uint64_t pol = evict_first_policy();
   const int64_t NG = (int64_t)gridDim.x * GPB;
   int64_t row = (int64_t)blockIdx.x * GPB + grp;
@@ -227,19 +281,52 @@ __global__ void __launch_bounds__(256, (JAC == kJacNone || G >= 16) ? 3 : 2) k_c
 #pragma unroll
     for (int q = 0; q < FREG; ++q) uj[q] = kU ? __ldg(A.u + (fj[q] >= 0 ? fj[q] : 0)) : S(0);
   };
-  auto stage_in = [&](uint32_t dst, const Meta& m, int& sk, int& sv, int& sb) {
-    const int n = (int)(m.e1 - m.e0);
-    sk = stage_span<uint32_t, G, L::CC>(dst + L::st_k, A.ck_k + m.e0 / D1, n / D1, lane, pol);
-    sv = stage_span<S, G, L::CE>(dst + L::st_v, A.ck_val + m.e0, n, lane, pol);
-    sb = stage_span<uint16_t, G, L::CE>(dst + L::st_b, A.ck_b + m.e0, n, lane, pol);
+  // stage buffer b <- this group's row slices.  cp.async: every lane copies 16-byte chunks of
+  // its group's row.  WB: the warp's rows are consecutive, so lane 0 of the warp copies the
+  // warp's contiguous spans with three TMA bulk copies completing on bars[b]; each group then
+  // addresses its row at its offset inside the span.
+  auto stage_in = [&](int b, const Meta& m, int& sk, int& sv, int& sb) {
+    const uint32_t dst = gs_s + b * STG;
+    if constexpr (WB) {
+      const uint32_t e0w = __shfl_sync(FM, m.e0, 0);
+      const uint32_t e1w = __reduce_max_sync(FM, m.e1);  // rows past the end have e1 = 0
+      const int n = (int)(e1w - e0w);
+      const char *lk, *lv, *lb;
+      uint32_t nk, nv, nb;
+      const int o = (int)(m.e0 - e0w);  // this group's row inside the warp span (ne = 0 past the end)
+      sk = span16(A.ck_k + e0w / D1, n / D1, &lk, &nk) + o / D1;
+      sv = span16(A.ck_val + e0w, n, &lv, &nv) + o;
+      sb = span16(A.ck_b + e0w, n, &lb, &nb) + o;
+      if ((threadIdx.x & 31) == 0) {
+        asm volatile("fence.proxy.async.shared::cta;" ::: "memory");  // earlier generic reads of the buffer
+        bar_expect(&bars[b], nk + nv + nb);
+        if (nk) bulk_copy(dst + SK, lk, nk, &bars[b], pol);
+        if (nv) bulk_copy(dst + SV, lv, nv, &bars[b], pol);
+        if (nb) bulk_copy(dst + SB, lb, nb, &bars[b], pol);
+      }
+    } else {
+      const int n = (int)(m.e1 - m.e0);
+      sk = stage_span<uint32_t, G, L::CC>(dst + SK, A.ck_k + m.e0 / D1, n / D1, lane, pol);
+      sv = stage_span<S, G, L::CE>(dst + SV, A.ck_val + m.e0, n, lane, pol);
+      sb = stage_span<uint16_t, G, L::CE>(dst + SB, A.ck_b + m.e0, n, lane, pol);
+      commit();
+    }
   };
+  if constexpr (WB) {
+    if ((threadIdx.x & 31) == 0) {
+      bar_init(&bars[0]);
+      bar_init(&bars[1]);
+      asm volatile("fence.mbarrier_init.release.cluster;" ::: "memory");
+    }
+    __syncwarp();
+  }
+  uint32_t phase = 0;  // WB: parity bit per buffer
 
   Meta cur = meta(A, row);
   Meta nxt = meta(A, row + NG);
   Meta nn = meta(A, row + 2 * NG);
   int shk, shv, shb;
-  stage_in(gs_s, cur, shk, shv, shb);
-  commit();
+  stage_in(0, cur, shk, shv, shb);
   S uj_cur[FREG], uj_nxt[FREG];
   int fb_cur[FREG], fb_nxt[FREG], fj_cur[FREG], fj_nxt[FREG];
   fibers(cur, fj_cur, fb_cur);
@@ -252,18 +339,23 @@ __global__ void __launch_bounds__(256, (JAC == kJacNone || G >= 16) ? 3 : 2) k_c
     const int nf = (int)(cur.f1 - cur.f0);
     // ---- prefetch: the next row's stream (async) and fiber data, metadata two rows ahead
     int nshk = 0, nshv = 0, nshb = 0;
-    if (row + NG < A.n_u) stage_in(gs_s + (st ^ 1) * L::stage, nxt, nshk, nshv, nshb);
-    commit();
+    if (WB || row + NG < A.n_u) stage_in(st ^ 1, nxt, nshk, nshv, nshb);  // WB: 0-byte arrive past the end
+    else commit();
     ucols(fj_nxt, uj_nxt);
     int fj_nn[FREG], fb_nn[FREG];
     fibers(nn, fj_nn, fb_nn);
     const Meta n3 = meta(A, row + 3 * NG);
-    wait_prev();
+    if constexpr (WB) {
+      bar_wait(&bars[st], (phase >> st) & 1u);
+      phase ^= 1u << st;
+    } else {
+      wait_prev();
+    }
     __syncwarp();
-    const unsigned char* cs = gs + st * L::stage;
-    const uint32_t* bk = reinterpret_cast<const uint32_t*>(cs + L::st_k) + shk;
-    const S* bv = reinterpret_cast<const S*>(cs + L::st_v) + shv;
-    const uint16_t* bb = reinterpret_cast<const uint16_t*>(cs + L::st_b) + shb;
+    const unsigned char* cs = gs + st * STG;
+    const uint32_t* bk = reinterpret_cast<const uint32_t*>(cs + SK) + shk;
+    const S* bv = reinterpret_cast<const S*>(cs + SV) + shv;
+    const uint16_t* bb = reinterpret_cast<const uint16_t*>(cs + SB) + shb;
     // ---- gathers of the lane's cells: w_K and (D_u w)_{K, 0..d}, all in flight together
     S wk[CPL];
     S dd[kN ? CPL : 1][D1];
@@ -426,11 +518,25 @@ __global__ void k_make_cells(int64_t n_u, const int64_t* __restrict__ row_fib, c
 
 int g_sm_count[64] = {0};
 
+// Row-stream staging: TMA bulk copies of each warp's consecutive rows (WB) when a warp holds
+// at least 8 rows (G <= 4: the copies are large, measured faster on cfg3: fused 0.139 ->
+// 0.107 ms), per-lane cp.async otherwise (cfg4, 4 rows per warp: 0.87 vs 0.94 ms with WB).
+// EGFEM_CELLS_STAGE=cp|bulk forces one (experiments).
+bool cells_warp_bulk(int G) {
+  static int v = -1;
+  if (v < 0) {
+    const char* e = getenv("EGFEM_CELLS_STAGE");
+    v = (e && e[0] == 'b') ? 1 : (e && e[0] == 'c') ? 0 : 2;
+  }
+  return v == 2 ? (G <= 4) : (v == 1);
+}
+
 template <typename S, int D1, int G, int CPL, int FREG, bool DO_R, int JAC>
 egfem_status run_cells(const egfem_tensor* t, const CellArgs<S>& A, cudaStream_t s) {
   using L = CellSmem<S, D1, G, CPL, JAC != kJacNone>;
-  auto fn = k_cell<S, D1, G, CPL, FREG, DO_R, JAC>;
-  const int smem = L::bytes * (256 / G);
+  const bool wb = cells_warp_bulk(G);
+  auto fn = wb ? k_cell<S, D1, G, CPL, FREG, DO_R, JAC, true> : k_cell<S, D1, G, CPL, FREG, DO_R, JAC, false>;
+  const int smem = wb ? L::wbytes * 8 : L::bytes * (256 / G);
   if (smem > 48 * 1024) EGFEM_CUDA_TRY(cudaFuncSetAttribute(fn, cudaFuncAttributeMaxDynamicSharedMemorySize, smem));
   const int dev = t->device & 63;
   if (!g_sm_count[dev])

@@ -12,4 +12,4 @@ for c in cfg1 cfg2 cfg3 cfg5; do timeout 600 python bench.py --config $c --no-cp
 timeout 600 python bench.py --dtype f32 --no-cpu-baseline > gpurun_out/bench_f32.json 2>&1
 timeout 900 python bench.py --steps 3 --warmup 3 --no-cpu-baseline > /dev/null 2>&1 && \
 timeout 900 ncu --metrics gpu__time_duration.sum --clock-control none -c 400 --csv --log-file gpurun_out/launches.csv python bench.py --steps 3 --warmup 3 --no-cpu-baseline > gpurun_out/ncu_launch.log 2>&1; echo "ncu launch rc=$?" >> gpurun_out/ncu_launch.log
-timeout 900 ncu --set full --clock-control none --import-source on -k 'regex:k_cell|k_interp' -c 6 -o gpurun_out/prof_cfg4 -f python scripts/profile_cfg4_jac.py > gpurun_out/ncu_full.log 2>&1; echo "ncu rc=$?" >> gpurun_out/ncu_full.log
+timeout 900 ncu --set full --clock-control none --import-source on -k 'regex:k_cell$|k_interp' -c 5 -o gpurun_out/prof_cfg4 -f python scripts/profile_cfg4_jac.py > gpurun_out/ncu_full.log 2>&1; echo "ncu rc=$?" >> gpurun_out/ncu_full.log
