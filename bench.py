@@ -173,6 +173,8 @@ def run_ours(args):
     batched = args.config == "cfg5"
     if batched:
         return run_batched(args, eg, t, pr, dev, td, s, build_s, world, rank)
+    if args.config == "gfem2d" and world == 1:
+        return run_gfem(args, eg, t, pr, dev, td, s, build_s)
     u = torch.tensor(u_np, dtype=td, device=dev)
     w = torch.empty(t.n_f, dtype=td, device=dev)
     gp = pr.W.family in (I.P0, I.QUAD) and pr.interp in (I.INTERP_GRADPOW_P0, I.INTERP_MINSURF_P0,
@@ -358,6 +360,64 @@ def run_batched(args, eg, t, pr, dev, td, s, build_s, world, rank):
            "gpu_launches": int(eg.launch_count() - l0), "clocks": clk.summary(), "build_s": build_s}
     if rank == 0:
         print(json.dumps(out), flush=True)
+
+
+def run_gfem(args, eg, t, pr, dev, td, s, build_s):
+    """F3: the GFEM (matrix) form of the Burgers term, r = N^f f with f = u² and J = N^f·diag(2u)
+    (PAPER.md L402–409), timed beside the tensor form T:(u⊗u) + Newton Jacobian on the same mesh
+    (the paper's tensor-vs-matrix comparison, L432).  Units: tensor nonzeros of the tensor form per
+    step (2·nnz for apply + Jacobian), so both forms are on the same scale."""
+    import torch
+    stream = torch.cuda.current_stream(dev)
+    u = torch.tensor(pr.u, dtype=td, device=dev)
+    f = torch.empty(t.n_f, dtype=td, device=dev)
+    r = torch.empty(t.n_u, dtype=td, device=dev)
+    B = torch.empty(t.nnz_csr, dtype=td, device=dev)
+    J = torch.empty(t.nnz_csr, dtype=td, device=dev)
+    eg.egfem_bilinear_build(t, B, stream)
+
+    def matrix_step():
+        eg.egfem_interp(t, pr.interp, pr.p, u, f, None, stream)
+        eg.egfem_csr_spmv(t, B, f, r, stream)
+        eg.egfem_bilinear_jacobian(t, B, pr.interp, pr.p, u, J, stream)
+
+    def tensor_step():
+        eg.egfem_apply_jacobian(t, eg.JAC_NEWTON, eg.INTERP_IDENTITY, 0.0, u, u, None, r, J, stream)
+
+    def timed(fn, K):
+        for _ in range(args.warmup):
+            fn()
+        torch.cuda.synchronize()
+        a, b = torch.cuda.Event(enable_timing=True), torch.cuda.Event(enable_timing=True)
+        a.record(stream)
+        for _ in range(K):
+            fn()
+        b.record(stream)
+        torch.cuda.synchronize()
+        return a.elapsed_time(b)
+    l0 = eg.launch_count()
+    with ClockSampler(dev.index) as clk:
+        ms = timed(matrix_step, args.steps)
+    launches = eg.launch_count() - l0
+    ms_tensor = timed(tensor_step, args.steps)
+    K = args.steps
+    units = 2 * t.nnz * K
+    # matrix step bytes: f from u (2 s N_u), B + cols (s+4) nnz_csr, row ptr, f gathered, r; J: B, cols, u, J
+    byts = 2 * s * t.n_u + (s + 4) * t.nnz_csr + 8 * (t.n_u + 1) + 2 * s * t.n_u + (2 * s + 4) * t.nnz_csr + s * t.n_u
+    peak, kind = _peaks()
+    per = ms / K
+    out = {"metric": "tensor nonzeros/s (GFEM matrix form of the same term, 2 x nnz(T) per step)",
+           "value": units / (ms * 1e-3), "unit": "nnz/s", "n_gpus": 1, "steps": K, "warmup": args.warmup,
+           "ms_per_step": per, "higher_is_better": True, "scaling": "weak", "vs_baseline": None, "dtype": args.dtype,
+           "data": "synthetic (seeded)",
+           "config": {"workload": f"{args.config}-{args.dtype}", "description": pr.description, "nnz": t.nnz,
+                      "nnz_csr": t.nnz_csr, "step": "interp(SQUARE) + CSR SpMV r = N^f f + J = N^f diag(2u)"},
+           "roofline": {"bound": "hbm", "kernel": "k_spmv + k_scale_cols (egfem_csr_spmv, egfem_bilinear_jacobian)",
+                        "achieved": byts / (per * 1e-3) / 1e9, "peak": peak, "peak_kind": kind, "unit": "GB/s",
+                        "frac": byts / (per * 1e-3) / 1e9 / peak, "algorithmic_bytes": byts, "traffic": None},
+           "kernels_ms": {"matrix_step": per, "tensor_step_fused_apply_newton": ms_tensor / K},
+           "gpu_launches": int(launches), "clocks": clk.summary(), "build_s": build_s}
+    print(json.dumps(out), flush=True)
 
 
 def cpu_baseline(pr, rows=ORACLE_SAMPLE_ROWS, steps=1):

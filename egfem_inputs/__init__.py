@@ -227,10 +227,10 @@ def _u_paper_bc(x, seed):
 # oracle finishes in seconds but that still spans many kernel tiles.
 FULL_N = {"cfg1": 256, "cfg2": 512, "cfg3": 1024, "cfg4": 128, "cfg5": 256,
           "minsurf2d": 1024, "minsurf3d": 64, "biochem_p1": 512, "biochem_p0": 512,
-          "quadratic_i4": 512, "biochem_i2": 512, "plap_i1": 1024, "plap3d_i2": 32}
+          "quadratic_i4": 512, "biochem_i2": 512, "plap_i1": 1024, "plap3d_i2": 32, "gfem2d": 512}
 SMALL_N = {"cfg1": 256, "cfg2": 40, "cfg3": 48, "cfg4": 10, "cfg5": 24,
            "minsurf2d": 40, "minsurf3d": 8, "biochem_p1": 32, "biochem_p0": 32,
-           "quadratic_i4": 24, "biochem_i2": 32, "plap_i1": 40, "plap3d_i2": 5}
+           "quadratic_i4": 24, "biochem_i2": 32, "plap_i1": 40, "plap3d_i2": 5, "gfem2d": 40}
 CONFIG_NAMES = ("cfg1", "cfg2", "cfg3", "cfg4", "cfg5")
 # SURVEY §8(f) F1 pointwise kinds (not BASELINE configs): minimal surface a = (1+|∇u|²)^{-1/2}
 # with P0 W (§5.6) and the biochemical c̃ = σ/(k+u), σ = 1 = k, on the
@@ -239,8 +239,10 @@ CONFIG_NAMES = ("cfg1", "cfg2", "cfg3", "cfg4", "cfg5")
 # w = u² at the points of the 6-point rule (I_4, Table 1's "EGFEM (I4)", L492); the biochemical
 # term on I_2 (3 points, L541–550); the p-Laplace K_a on I_1 (centroid, L143–149, L616) and on the
 # 4-point tetrahedral I_2 (3D).
+# F3 bilinear GFEM form: the paper's Burgers N^f_ik = ∫ η_k (∂x+∂y)φ_i with f = u² at the nodes
+# (PAPER.md L402–409), on cfg2's mesh and u; its tensor is the paper's N (CONV_I, L400).
 EXTRA_NAMES = ("minsurf2d", "minsurf3d", "biochem_p1", "biochem_p0", "quadratic_i4", "biochem_i2", "plap_i1",
-               "plap3d_i2")
+               "plap3d_i2", "gfem2d")
 
 
 def make_problem(name: str, n: Optional[int] = None, batch: Optional[int] = None) -> Problem:
@@ -303,6 +305,11 @@ def make_problem(name: str, n: Optional[int] = None, batch: Optional[int] = None
         mesh = mesh_cube(n)
         return Problem(name, mesh, space_p1(mesh), space_quad(mesh, 4), FORM_PLAP, INTERP_GRADPOW_P0, 3.0,
                        ("f64",), _u_cfg4(mesh.coords), description=f"3D p-Laplace p=3 on I2 (4-pt), {n}^3x6")
+    if name == "gfem2d":
+        mesh = mesh_square(n)
+        V = space_p1(mesh)
+        return Problem(name, mesh, V, V, FORM_CONV_I, INTERP_SQUARE, 0.0, ("f64",), _u_cfg2(mesh.coords),
+                       description=f"2D Burgers GFEM N^f f, f = u^2, {n}x{n}")
     raise KeyError(name)
 
 

@@ -223,6 +223,33 @@ egfem_status egfem_apply_jacobian(const egfem_tensor* t, egfem_jac_mode mode, eg
                                   double p, const void* u, const void* w, const void* chain, void* r,
                                   void* csr_vals, egfem_stream_t stream);
 
+/* ---------------------------------------------------------------- bilinear GFEM forms
+ * The matrix forms of PAPER.md L196–203 eq. (egfem_terms) and L402–409:
+ *   M^c_ik = ∫ η_k φ_i   (the MASS3 tensor's form),   N^f_ik = ∫ η_k (∂x+∂y)φ_i   (CONV_I's),
+ * the GFEM counterpart of a trilinear term in which the u-slot is absent.  For Lagrange V
+ * (Σ_j φ_j ≡ 1) such a matrix is the u-slot contraction of the trilinear tensor with all ones,
+ * B = T·₂1, and for W = V numbering its pattern is the tensor's CSR pattern (k runs over the
+ * same element cliques as j).  The hot path of a GFEM term is then
+ *   r = B f (egfem_csr_spmv),  J = B·diag(f'(u)) (egfem_bilinear_jacobian),
+ * with f = w from egfem_interp (IDENTITY, SQUARE, RECIPROCAL).
+ * egfem_bilinear_build: b_vals device [nnz_csr] ← B.  Needs W = V numbering whose T·₂u fits
+ * the pattern (else DIMENSION_MISMATCH / UNSUPPORTED) and a value u-slot (MASS3, CONV_I,
+ * CONV_K; CONV_J and PLAP differentiate it, T·₂1 = 0: UNSUPPORTED; a from_coo tensor is taken
+ * as is).  Runs T·₂1 through the Newton kernel (offline; allocates and frees two device
+ * vectors, synchronizes the stream). */
+egfem_status egfem_bilinear_build(const egfem_tensor* t, void* b_vals, egfem_stream_t stream);
+
+/* y = A x for any values `vals` [nnz_csr] on the tensor's CSR pattern (x: [N_u], y: [N_u], all
+ * device, handle dtype); per-row sums in a fixed order. */
+egfem_status egfem_csr_spmv(const egfem_tensor* t, const void* vals, const void* x, void* y,
+                            egfem_stream_t stream);
+
+/* GFEM Jacobian of r(u) = B f(u):  J_ik = B_ik f'(u_k)  (W = V; PAPER.md L290 with the
+ * pointwise D_u f of L292): IDENTITY f' = 1, SQUARE 2u, RECIPROCAL −1/(p+u)².  b_vals, u, J
+ * device ([nnz_csr], [N_u], [nnz_csr]); J is fully overwritten. */
+egfem_status egfem_bilinear_jacobian(const egfem_tensor* t, const void* b_vals, egfem_interp_kind kind,
+                                     double p, const void* u, void* csr_vals, egfem_stream_t stream);
+
 /* ---------------------------------------------------------------- multi-GPU (row partition)
  * Split the rows of `global` into `nranks` contiguous ranges balanced by nnz and
  * build rank `rank`'s local tensor on `device`.  The local tensor addresses a

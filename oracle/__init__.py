@@ -14,6 +14,7 @@ Parity status per function (DESIGN.md §4 restates it):
   interp                            pinned: linear-field closed form, brute force
   apply                             pinned: 1D closed form, brute force, Σr=0, SGA
   jacobian                          pinned: 1D closed forms, FD, Euler homogeneity
+  bilinear (F3)                     pinned: exact-integration matrices (brute), PoU Σ_j T_ijk
 """
 from __future__ import annotations
 
@@ -56,6 +57,8 @@ def lib():
         L.oracle_apply_batched.argtypes = [P, i32, P, P, P]
         L.oracle_jacobian.argtypes = [P, i32, i32, ctypes.c_double, P, P, P]
         L.oracle_jacobian.restype = i32
+        L.oracle_bilinear.argtypes = [P, P]
+        L.oracle_bilinear.restype = i32
         _lib = L
     return _lib
 
@@ -132,6 +135,14 @@ class OracleTensor:
         R = np.zeros((B, self.n_u), np.float64)
         lib().oracle_apply_batched(self.h, B, _p(U), _p(W), _p(R))
         return R
+
+    def bilinear(self):
+        """F3: B_ik = ∫ (slot φ_i)(slot η_k) on the CSR pattern (W = V), element-by-element."""
+        vals = np.zeros(self.nnz_csr, np.float64)
+        rc = lib().oracle_bilinear(self.h, _p(vals))
+        if rc != 0:
+            raise ValueError(f"oracle_bilinear failed rc={rc}")
+        return vals
 
     def jacobian(self, mode, kind, p, u, w):
         vals = np.zeros(self.nnz_csr, np.float64)

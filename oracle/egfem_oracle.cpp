@@ -694,6 +694,44 @@ static int build_Duw(const OTensor* T, int kind, double p, const double* u, std:
   return -1;
 }
 
+// ---------------------------------------------------------------- bilinear GFEM form (F3)
+// B_ik = ∫ (opA φ_i)(opC η_k): the matrix of PAPER.md L196–203 (M^c: MASS3's slots) and
+// L402–409 (N^f: CONV_I's), assembled element by element with its own quadrature (degree of
+// the bilinear integrand), into the CSR pattern (W = V numbering).  Independent of T.
+int oracle_bilinear(const void* h, double* vals) {
+  const OTensor* T = static_cast<const OTensor*>(h);
+  const int d = T->dim;
+  if (T->W.n_dofs != T->V.n_dofs || T->W.family != T->V.family) return -1;
+  int opA, opB, opC;
+  form_ops(T->form, &opA, &opB, &opC);
+  (void)opB;
+  if (opA == OP_GRAD) return -2;  // ∫ η ∇φ_i is a vector: no scalar bilinear form
+  Rule R = default_rule(d, op_degree(opA, T->V.family) + op_degree(opC, T->W.family));
+  std::fill(vals, vals + T->csr_col.size(), 0.0);
+  const int nA = T->V.n_loc, nC = T->W.n_loc;
+  std::vector<double> vv(nA), wv(nC), vg(nA * 3), wg(nC * 3);
+  for (int64_t K = 0; K < T->n_cells; ++K) {
+    Geo g = geometry(*T, K);
+    const int32_t* I = &T->V.cell_dofs[K * nA];
+    const int32_t* Wd = &T->W.cell_dofs[K * nC];
+    for (int q = 0; q < R.nq; ++q) {
+      const double* lam = &R.bary[q * (d + 1)];
+      basis(T->V.family, d, lam, g, nA, vv.data(), reinterpret_cast<double(*)[3]>(vg.data()));
+      basis(T->W.family, d, lam, g, nC, wv.data(), reinterpret_cast<double(*)[3]>(wg.data()));
+      const double wq = R.w[q] * g.vol;
+      for (int a = 0; a < nA; ++a) {
+        if (I[a] < T->row_begin || I[a] >= T->row_end) continue;
+        for (int c = 0; c < nC; ++c) {
+          const int64_t sl = csr_find(T, I[a], Wd[c]);
+          if (sl < 0) return -3;
+          vals[sl] += wq * apply_op(opA, d, vv[a], &vg[a * 3]) * apply_op(opC, d, wv[c], &wg[c * 3]);
+        }
+      }
+    }
+  }
+  return 0;
+}
+
 // csr_vals = T·w                                    (PICARD)
 // csr_vals = T·w + (T·₂u)·D_u w                     (NEWTON)
 int oracle_jacobian(const void* h, int mode, int kind, double p, const double* u, const double* w,

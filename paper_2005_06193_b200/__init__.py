@@ -40,7 +40,8 @@ EXPORTS = ("egfem_tensor_build", "egfem_tensor_from_coo", "egfem_tensor_destroy"
            "egfem_tensor_csr_pattern", "egfem_tensor_export", "egfem_interp", "egfem_apply",
            "egfem_apply_batched", "egfem_jacobian", "egfem_apply_jacobian", "egfem_partition",
            "egfem_partition_rows", "egfem_halo_pack", "egfem_halo_unpack", "egfem_launch_count",
-           "egfem_status_string", "egfem_last_error")
+           "egfem_status_string", "egfem_last_error", "egfem_bilinear_build", "egfem_csr_spmv",
+           "egfem_bilinear_jacobian")
 
 
 class EgfemError(RuntimeError):
@@ -84,6 +85,9 @@ def _load():
         "egfem_partition_rows": [i64, P, i32, P],
         "egfem_halo_pack": [P, P, i64, P, P, P],
         "egfem_halo_unpack": [P, P, i64, P, P, P],
+        "egfem_bilinear_build": [P, P, P],
+        "egfem_csr_spmv": [P, P, P, P, P],
+        "egfem_bilinear_jacobian": [P, P, st, ctypes.c_double, P, P, P],
     }
     for name, args in sig.items():
         f = getattr(L, name)
@@ -233,6 +237,22 @@ def egfem_jacobian(t: Tensor, mode, kind, p, u, w, chain, csr_vals, stream=None)
     """Step (3): A = T·w or J = T·w + (T·₂u)·D_u w into the CSR values."""
     _check("egfem_jacobian", _lib.egfem_jacobian(t.h, mode, kind, float(p), _dptr(u), _dptr(w), _dptr(chain),
                                                  _dptr(csr_vals), _stream(stream)))
+
+
+def egfem_bilinear_build(t: Tensor, b_vals, stream=None):
+    """F3: the bilinear GFEM matrix B = T·₂1 on the CSR pattern (W = V)."""
+    _check("egfem_bilinear_build", _lib.egfem_bilinear_build(t.h, _dptr(b_vals), _stream(stream)))
+
+
+def egfem_csr_spmv(t: Tensor, vals, x, y, stream=None):
+    """y = A x for values on the tensor's CSR pattern (the GFEM action r = B f)."""
+    _check("egfem_csr_spmv", _lib.egfem_csr_spmv(t.h, _dptr(vals), _dptr(x), _dptr(y), _stream(stream)))
+
+
+def egfem_bilinear_jacobian(t: Tensor, b_vals, kind, p, u, csr_vals, stream=None):
+    """J = B·diag(f'(u)) for the GFEM term r = B f(u) (W = V)."""
+    _check("egfem_bilinear_jacobian", _lib.egfem_bilinear_jacobian(t.h, _dptr(b_vals), kind, float(p), _dptr(u),
+                                                                   _dptr(csr_vals), _stream(stream)))
 
 
 def egfem_apply_jacobian(t: Tensor, mode, kind, p, u, w, chain, r, csr_vals, stream=None):

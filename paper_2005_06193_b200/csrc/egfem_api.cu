@@ -444,6 +444,46 @@ egfem_status egfem_apply_jacobian(const egfem_tensor* t, egfem_jac_mode mode, eg
   return launch_tile(t, true, code, kind, p, u, w, chain, r, csr_vals, (cudaStream_t)stream);
 }
 
+egfem_status egfem_bilinear_build(const egfem_tensor* t, void* b_vals, egfem_stream_t stream) {
+  if (!t) return fail(EGFEM_ERR_INVALID_ARGUMENT, "tensor is NULL");
+  egfem_status st;
+  if ((st = check_dev_ptr(t, b_vals, "b_vals", true))) return st;
+  if (!t->w_is_v) return fail(EGFEM_ERR_DIMENSION_MISMATCH, "bilinear form needs W = V numbering");
+  if (!t->newton_wv_ok) return fail(EGFEM_ERR_UNSUPPORTED, "T·₂1 has entries outside the CSR pattern");
+  if (t->has_mesh && (t->form == EGFEM_FORM_CONV_J || t->form == EGFEM_FORM_PLAP))
+    return fail(EGFEM_ERR_UNSUPPORTED, "the u-slot of this form is differentiated: T·₂1 = 0 (Σ_j ∇φ_j = 0)");
+  DeviceGuard g(t->device);
+  return launch_bilinear_build(t, b_vals, (cudaStream_t)stream);
+}
+
+egfem_status egfem_csr_spmv(const egfem_tensor* t, const void* vals, const void* x, void* y, egfem_stream_t stream) {
+  if (!t) return fail(EGFEM_ERR_INVALID_ARGUMENT, "tensor is NULL");
+  egfem_status st;
+  if ((st = check_dev_ptr(t, vals, "vals", true)) || (st = check_dev_ptr(t, x, "x", true)) ||
+      (st = check_dev_ptr(t, y, "y", true)))
+    return st;
+  if (x == y) return fail(EGFEM_ERR_INVALID_ARGUMENT, "x and y must not alias");
+  DeviceGuard g(t->device);
+  return launch_spmv(t, vals, x, y, (cudaStream_t)stream);
+}
+
+egfem_status egfem_bilinear_jacobian(const egfem_tensor* t, const void* b_vals, egfem_interp_kind kind, double p,
+                                     const void* u, void* csr_vals, egfem_stream_t stream) {
+  if (!t) return fail(EGFEM_ERR_INVALID_ARGUMENT, "tensor is NULL");
+  egfem_status st;
+  if ((st = check_dev_ptr(t, b_vals, "b_vals", true)) || (st = check_dev_ptr(t, u, "u", true)) ||
+      (st = check_dev_ptr(t, csr_vals, "csr_vals", true)))
+    return st;
+  if (!t->w_is_v) return fail(EGFEM_ERR_DIMENSION_MISMATCH, "bilinear Jacobian needs W = V numbering");
+  int mode = -1;
+  if (kind == EGFEM_INTERP_IDENTITY) mode = 0;
+  if (kind == EGFEM_INTERP_SQUARE) mode = 1;
+  if (kind == EGFEM_INTERP_RECIPROCAL) mode = 2;
+  if (mode < 0) return fail(EGFEM_ERR_UNSUPPORTED, "bilinear Jacobian: IDENTITY, SQUARE or RECIPROCAL");
+  DeviceGuard g(t->device);
+  return launch_scale_cols(t, b_vals, mode, p, u, csr_vals, (cudaStream_t)stream);
+}
+
 egfem_status egfem_halo_pack(const egfem_tensor* local, const int32_t* d_idx, int64_t n, const void* u_local,
                              void* send_buf, egfem_stream_t stream) {
   if (!local) return fail(EGFEM_ERR_INVALID_ARGUMENT, "tensor is NULL");

@@ -131,6 +131,10 @@ bool dense_path_ok(const egfem_tensor* t);
 egfem_status launch_dense(const egfem_tensor* t, int32_t batch, egfem_layout layout, const void* U, const void* W,
                           void* R, cudaStream_t s);
 egfem_status make_dense_blocks(egfem_tensor* t, const std::vector<int64_t>& hrf);
+egfem_status launch_spmv(const egfem_tensor* t, const void* vals, const void* x, void* y, cudaStream_t s);
+egfem_status launch_scale_cols(const egfem_tensor* t, const void* b, int mode, double p, const void* u, void* J,
+                               cudaStream_t s);
+egfem_status launch_bilinear_build(const egfem_tensor* t, void* b_vals, cudaStream_t s);
 egfem_status launch_batched(const egfem_tensor* t, int32_t batch, egfem_layout layout, const void* U,
                             const void* W, void* R, cudaStream_t s);
 egfem_status launch_halo(const egfem_tensor* t, const int32_t* idx, int64_t n, const void* src, void* dst,

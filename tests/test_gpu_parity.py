@@ -369,3 +369,37 @@ def test_kernel_paths(eg, env):
                          capture_output=True, text=True, timeout=600)
     assert res.returncode == 0, res.stdout + res.stderr
     assert "path ok" in res.stdout
+
+
+@pytest.mark.parametrize("name", ["gfem2d", "biochem_p1"])
+def test_bilinear_gfem(eg, orc, name):
+    """F3: B = T·₂1 on the CSR pattern equals the oracle's element-by-element ∫ (slot φ_i) η_k
+    (PAPER.md L196–203, L402–409); r = B f and J = B·diag(f'(u)) through the C ABI."""
+    import torch
+    pr = I.make_problem(name, n=I.SMALL_N[name])
+    t, o = _build_both(eg, orc, pr)
+    Bo = o.bilinear()
+    B = torch.empty(t.nnz_csr, dtype=torch.float64, device="cuda")
+    eg.egfem_bilinear_build(t, B)
+    assert rel_l2(B.cpu().numpy(), Bo) <= FP64_TOL
+    u = torch.tensor(pr.u, device="cuda")
+    f = torch.empty(t.n_f, dtype=torch.float64, device="cuda")
+    eg.egfem_interp(t, pr.interp, pr.p, u, f)
+    r = torch.empty(t.n_u, dtype=torch.float64, device="cuda")
+    eg.egfem_csr_spmv(t, B, f, r)
+    J = torch.empty(t.nnz_csr, dtype=torch.float64, device="cuda")
+    eg.egfem_bilinear_jacobian(t, B, pr.interp, pr.p, u, J)
+    ex = o.export()
+    rows = np.repeat(np.arange(t.n_u), np.diff(ex["csr_row_ptr"]))
+    fo = o.interp(pr.interp, pr.p, pr.u)
+    r_ref = np.zeros(t.n_u)
+    np.add.at(r_ref, rows, Bo * fo[ex["csr_col"]])
+    uc = pr.u[ex["csr_col"]]
+    dfo = 2 * uc if pr.interp == I.INTERP_SQUARE else -1.0 / (pr.p + uc) ** 2
+    assert rel_l2(r.cpu().numpy(), r_ref) <= FP64_TOL
+    assert rel_l2(J.cpu().numpy(), Bo * dfo) <= FP64_TOL
+    # the gradient u-slot form has no B = T·₂1 counterpart
+    pr2 = I.make_problem("cfg2", n=4)
+    t2 = eg.egfem_tensor_build(pr2.mesh, pr2.V, pr2.W, pr2.form, device=0)
+    with pytest.raises(eg.EgfemError):
+        eg.egfem_bilinear_build(t2, torch.empty(t2.nnz_csr, dtype=torch.float64, device="cuda"))

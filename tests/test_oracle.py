@@ -689,3 +689,43 @@ def test_f2_newton_vs_finite_differences(oracle_mod, case):
     J = _csr_dense(T, T.jacobian(I.JAC_NEWTON, pr.interp, pr.p, u, w))
     Jfd = _fd_jacobian(T, pr.interp, pr.p, u, 1e-5)
     assert rel_l2(J, Jfd) < (1e-6 if pr.form == I.FORM_PLAP else 1e-8)
+
+
+# ----------------------------------------------------------------------------- F3 bilinear GFEM forms
+@pytest.mark.parametrize("form,ops", [(I.FORM_MASS3, ("v", "v")), (I.FORM_CONV_I, ("dxdy", "v"))])
+def test_bilinear_matches_exact_and_pou(oracle_mod, form, ops):
+    """F3: the oracle's bilinear M^c / N^f equals the exactly
+    integrated matrix (brute force) and the u-slot contraction of the trilinear tensor with ones
+    (partition of unity Σ_j φ_j = 1)."""
+    m = jitter(I.mesh_square(4), 0.2, 31)
+    V = I.space_p1(m)
+    T = oracle_mod.OracleTensor(m, V, V, form)
+    b = _csr_dense(T, T.bilinear())
+    exact = brute.bilinear_matrix(m, V, *ops)
+    assert np.abs(b - exact).max() < 1e-14 * max(1.0, np.abs(exact).max())
+    ones = np.ones(T.n_u)
+    Bpou = _csr_dense(T, T.jacobian(I.JAC_NEWTON, I.INTERP_IDENTITY, 0.0, ones, np.zeros(T.n_f)))
+    assert np.abs(b - Bpou).max() < 1e-14 * max(1.0, np.abs(exact).max())
+
+
+def test_gfem_burgers_residual_and_jacobian(oracle_mod):
+    """GFEM Burgers term −½ N^f f with f = u² at the nodes: r = N^f f; its
+    Jacobian N^f diag(2u) equals central differences of r(u) (r is quadratic: exact to rounding)."""
+    m = jitter(I.mesh_square(3), 0.2, 32)
+    V = I.space_p1(m)
+    T = oracle_mod.OracleTensor(m, V, V, I.FORM_CONV_I)
+    B = _csr_dense(T, T.bilinear())
+    u = np.random.default_rng(33).standard_normal(V.n_dofs)
+    r = lambda x: B @ (x * x)
+    Jfd = np.column_stack([(r(u + e) - r(u - e)) / 2e-6 for e in np.eye(V.n_dofs) * 1e-6])
+    assert rel_l2(B * (2 * u)[None, :], Jfd) < 1e-8
+
+
+def test_gradient_u_slot_contracts_to_zero(oracle_mod):
+    """Σ_j ∇φ_j = 0: forms whose u-slot is differentiated (CONV_J, PLAP) have T·₂1 = 0, so they
+    have no bilinear GFEM counterpart of the B = T·₂1 kind (egfem_bilinear_build rejects them)."""
+    m = jitter(I.mesh_square(3), 0.2, 34)
+    V = I.space_p1(m)
+    T = oracle_mod.OracleTensor(m, V, V, I.FORM_CONV_J)
+    B = T.jacobian(I.JAC_NEWTON, I.INTERP_IDENTITY, 0.0, np.ones(T.n_u), np.zeros(T.n_f))
+    assert np.abs(B).max() < 1e-15
