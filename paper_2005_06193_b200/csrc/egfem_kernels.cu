@@ -66,34 +66,40 @@ __device__ __forceinline__ CellIdx<D> load_cell(const int32_t* __restrict__ t, i
   return r;
 }
 
-template <typename S, int D, bool SAME, bool IOTA>
-__global__ void __launch_bounds__(128) k_interp_gradpow(const double* __restrict__ coords, const int32_t* __restrict__ cells,
-                                 const int32_t* __restrict__ vdofs, const int32_t* __restrict__ wdofs, int64_t n_cells,
-                                 const S* __restrict__ u, S* __restrict__ w, S* __restrict__ chain, double p,
-                                 bool minsurf, int nw) {
-  int64_t c = (int64_t)blockIdx.x * blockDim.x + threadIdx.x;
-  if (c >= n_cells) return;
-  const CellIdx<D> cv = load_cell<D>(cells, c);
-  const CellIdx<D> dv = SAME ? cv : load_cell<D>(vdofs, c);
+// One cell's gathered inputs: vertex coordinates and u at its V DOFs.
+template <typename S, int D>
+struct CellIn {
   double x[D + 1][D];
   double uv[D + 1];
+};
+template <typename S, int D, bool SAME>
+__device__ __forceinline__ void gather_cell(const double* __restrict__ coords, const CellIdx<D>& cv,
+                                            const CellIdx<D>& dv, const S* __restrict__ u, CellIn<S, D>& in) {
 #pragma unroll
   for (int a = 0; a <= D; ++a) {
     const int64_t v = cv.v[a];
     if constexpr (D == 3) {
       const double2 xy = __ldg(reinterpret_cast<const double2*>(coords + v * 4));
-      x[a][0] = xy.x;
-      x[a][1] = xy.y;
-      x[a][2] = __ldg(coords + v * 4 + 2);
+      in.x[a][0] = xy.x;
+      in.x[a][1] = xy.y;
+      in.x[a][2] = __ldg(coords + v * 4 + 2);
     } else if constexpr (D == 2) {
       const double2 xy = __ldg(reinterpret_cast<const double2*>(coords + v * 2));
-      x[a][0] = xy.x;
-      x[a][1] = xy.y;
+      in.x[a][0] = xy.x;
+      in.x[a][1] = xy.y;
     } else {
-      x[a][0] = __ldg(coords + v);
+      in.x[a][0] = __ldg(coords + v);
     }
-    uv[a] = (double)__ldg(u + dv.v[a]);
+    in.uv[a] = (double)__ldg(u + dv.v[a]);
   }
+}
+
+template <typename S, int D, bool IOTA>
+__device__ __forceinline__ void gradpow_cell(const CellIn<S, D>& in, int64_t c, const int32_t* __restrict__ wdofs,
+                                             S* __restrict__ w, S* __restrict__ chain, double p, bool minsurf,
+                                             int nw) {
+  const auto& x = in.x;
+  const auto& uv = in.uv;
   // barycentric gradients of vertices 1..D from the edge vectors e_a = x_a − x_0
   double g[D + 1][D];
   if constexpr (D == 1) {
@@ -189,6 +195,36 @@ __global__ void __launch_bounds__(128) k_interp_gradpow(const double* __restrict
         for (int a = 0; a <= D; ++a) chain[K * (D + 1) + a] = dm[a];
       }
     }
+  }
+}
+
+// Grid-stride and software-pipelined: the cell record is loaded two cells ahead and the next
+// cell's vertex coordinates and u one cell ahead, so the dependent record → coordinates
+// gather chain overlaps the current cell's arithmetic instead of stalling every thread.
+template <typename S, int D, bool SAME, bool IOTA>
+__global__ void __launch_bounds__(128) k_interp_gradpow(const double* __restrict__ coords, const int32_t* __restrict__ cells,
+                                 const int32_t* __restrict__ vdofs, const int32_t* __restrict__ wdofs, int64_t n_cells,
+                                 const S* __restrict__ u, S* __restrict__ w, S* __restrict__ chain, double p,
+                                 bool minsurf, int nw) {
+  const int64_t stride = (int64_t)gridDim.x * blockDim.x;
+  int64_t c = (int64_t)blockIdx.x * blockDim.x + threadIdx.x;
+  if (c >= n_cells) return;
+  auto idx = [&](int64_t cc, CellIdx<D>& cv, CellIdx<D>& dv) {
+    const int64_t q = cc < n_cells ? cc : c;  // clamped: a valid record, never used
+    cv = load_cell<D>(cells, q);
+    dv = SAME ? cv : load_cell<D>(vdofs, q);
+  };
+  CellIdx<D> cv1, dv1, cv2, dv2;
+  idx(c, cv1, dv1);
+  CellIn<S, D> cur;
+  gather_cell<S, D, SAME>(coords, cv1, dv1, u, cur);
+  idx(c + stride, cv2, dv2);
+  for (; c < n_cells; c += stride) {
+    CellIn<S, D> nxt;
+    gather_cell<S, D, SAME>(coords, cv2, dv2, u, nxt);  // next cell's gathers in flight
+    idx(c + 2 * stride, cv2, dv2);                      // record two cells ahead
+    gradpow_cell<S, D, IOTA>(cur, c, wdofs, w, chain, p, minsurf, nw);
+    cur = nxt;
   }
 }
 
@@ -739,12 +775,17 @@ egfem_status launch_interp(const egfem_tensor* t, egfem_interp_kind kind, double
       count_launch();
     }
   } else if (kind == EGFEM_INTERP_GRADPOW_P0 || kind == EGFEM_INTERP_MINSURF_P0) {
-    const int grid = nblk(t->n_cells, 128);
+    const int grid = std::max(1, nblk(t->n_cells, 128));  // capped at one resident wave below
     if (t->n_cells > 0) {
 #define EGFEM_GP3(S, D, SA, IO)                                                                       \
-  k_interp_gradpow<S, D, SA, IO><<<grid, 128, 0, s>>>(D == 3 ? t->coords4 : t->coords, t->cells, t->vdofs,   \
-                                                      t->wdofs, t->n_cells, (const S*)u, (S*)w, (S*)chain, p, \
-                                                      kind == EGFEM_INTERP_MINSURF_P0, t->nwc)
+  do {                                                                                                \
+    int per_sm = 0;                                                                                   \
+    cudaOccupancyMaxActiveBlocksPerMultiprocessor(&per_sm, k_interp_gradpow<S, D, SA, IO>, 128, 0);   \
+    const int g = (int)std::min<int64_t>(grid, (int64_t)std::max(per_sm, 1) * 148);                   \
+    k_interp_gradpow<S, D, SA, IO><<<g, 128, 0, s>>>(D == 3 ? t->coords4 : t->coords, t->cells, t->vdofs, \
+                                                     t->wdofs, t->n_cells, (const S*)u, (S*)w, (S*)chain, p, \
+                                                     kind == EGFEM_INTERP_MINSURF_P0, t->nwc);         \
+  } while (0)
 #define EGFEM_GP(S, D)                                                          \
   do {                                                                          \
     if (t->vdofs_is_cells && t->wdofs_is_iota) EGFEM_GP3(S, D, true, true);     \
