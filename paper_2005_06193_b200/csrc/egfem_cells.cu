@@ -463,8 +463,16 @@ __global__ void __launch_bounds__(256, (JAC == kJacNone || G >= 16) ? 3 : 2) k_c
         const int nx_next = (q + 1 < FREG) ? __shfl_sync(FM, fb_cur[(q + 1) % FREG] - (int)cur.e0, 0, G) : ne;
         if (f < nf && f != fd) {
           const int yb = (f + 1 >= nf) ? ne : (lane + 1 < G ? nx_same : nx_next);
+          // the first 8 terms loaded together (independent shared loads), summed in order; a
+          // longer fiber (unstructured meshes) continues serially
+          S v[8];
+#pragma unroll
+          for (int x = 0; x < 8; ++x) v[x] = (fs + x < yb) ? s_t[fs + x] : S(0);
           S a = S(0);
-          for (int y = fs; y < yb; ++y) a = xadd(a, s_t[y]);
+#pragma unroll
+          for (int x = 0; x < 8; ++x)
+            if (fs + x < yb) a = xadd(a, v[x]);
+          for (int y = fs + 8; y < yb; ++y) a = xadd(a, s_t[y]);
           A.csr[cur.f0 + f] = a;
         }
       }
