@@ -5,11 +5,12 @@
 // For W = V forms every nonzero of row i has j and k in the row's CSR stencil
 // N(i) = {j : (i, j) fiber} (the cell cliques around i), so row i of T is a small dense
 // |N|×|N| block M_i[a][b] = T_{i, N_a, N_b} (zero where T has no nonzero).  The builder keeps
-// that block per row (row-major, stride |N| rounded up to even).  A warp owns 64 pairs
-// (lane, lane+32) of one row at a time: it loads W at the stencil into registers, then
+// that block per row (row-major, stride |N| rounded up to even).  A warp owns 32·PPT pairs
+// (lane, lane+32, …; PPT = 2) of one row at a time: it loads
+// W at the stencil into registers, then
 //   R_{i,p} = Σ_a U_{N_a,p} Σ_b M_i[a][b] W_{N_b,p}
 // is pure FP64 FMAs with register operands and warp-uniform (broadcast) block loads, so
-// each W value fetched is reused |N| times and each block value 2× per lane — the batched
+// each W value fetched is reused |N| times and each block value PPT times per lane — the batched
 // action is FP64-bound instead of L1-gather-bound.  The per-row stencil size is a template
 // parameter (dispatched per row, warp-uniform).  Fixed summation order: bitwise reproducible.
 #include <algorithm>
@@ -51,41 +52,49 @@ struct Vec2<float> {
   using T = float2;
 };
 
-template <typename S, int N, bool NM>
+// PPT pairs per lane (lane, lane+32, ...): each staged block value feeds PPT FMAs and each W
+// value N; even and odd b accumulate in separate chains.
+template <typename S, int N, bool NM, int PPT>
 __device__ __forceinline__ void dense_row(const DenseArgs<S>& A, int64_t row, const int32_t* cols, const S* M, int p0) {
   constexpr int NP = N + (N & 1);
-  const int p1 = p0 + 32;
-  const bool ok0 = p0 < A.B, ok1 = p1 < A.B;
-  S w0[N], w1[N];
+  bool ok[PPT];
+#pragma unroll
+  for (int q = 0; q < PPT; ++q) ok[q] = p0 + 32 * q < A.B;
+  S wv[PPT][N];
 #pragma unroll
   for (int b = 0; b < N; ++b) {
     const int64_t k = cols[b];  // smem broadcast
-    w0[b] = ok0 ? __ldg(A.W + at<NM>(k, p0, A.B, A.n_f)) : S(0);
-    w1[b] = ok1 ? __ldg(A.W + at<NM>(k, p1, A.B, A.n_f)) : S(0);
+#pragma unroll
+    for (int q = 0; q < PPT; ++q) wv[q][b] = ok[q] ? __ldg(A.W + at<NM>(k, p0 + 32 * q, A.B, A.n_f)) : S(0);
   }
-  S r0 = S(0), r1 = S(0);
+  S r[PPT];
+#pragma unroll
+  for (int q = 0; q < PPT; ++q) r[q] = S(0);
 #pragma unroll
   for (int a = 0; a < N; ++a) {
     const int64_t j = cols[a];
-    const S u0 = ok0 ? __ldg(A.U + at<NM>(j, p0, A.B, A.n_u)) : S(0);
-    const S u1 = ok1 ? __ldg(A.U + at<NM>(j, p1, A.B, A.n_u)) : S(0);
-    // even and odd b in separate chains: four independent FMA chains per lane
-    S s0 = S(0), s1 = S(0), t0 = S(0), t1 = S(0);
+    S uu[PPT], se[PPT], so[PPT];
+#pragma unroll
+    for (int q = 0; q < PPT; ++q) {
+      uu[q] = ok[q] ? __ldg(A.U + at<NM>(j, p0 + 32 * q, A.B, A.n_u)) : S(0);
+      se[q] = S(0);
+      so[q] = S(0);
+    }
 #pragma unroll
     for (int b = 0; b < N; b += 2) {
       const typename Vec2<S>::T m = *reinterpret_cast<const typename Vec2<S>::T*>(M + a * NP + b);  // smem broadcast
-      s0 = fma(m.x, w0[b], s0);
-      s1 = fma(m.x, w1[b], s1);
-      if (b + 1 < N) {
-        t0 = fma(m.y, w0[b + 1], t0);
-        t1 = fma(m.y, w1[b + 1], t1);
+#pragma unroll
+      for (int q = 0; q < PPT; ++q) {
+        se[q] = fma(m.x, wv[q][b], se[q]);
+        if (b + 1 < N) so[q] = fma(m.y, wv[q][b + 1], so[q]);
       }
     }
-    r0 = fma(u0, s0 + t0, r0);
-    r1 = fma(u1, s1 + t1, r1);
+#pragma unroll
+    for (int q = 0; q < PPT; ++q) r[q] = fma(uu[q], se[q] + so[q], r[q]);
   }
-  if (ok0) A.R[at<NM>(row, p0, A.B, A.n_u)] = r0;
-  if (ok1) A.R[at<NM>(row, p1, A.B, A.n_u)] = r1;
+#pragma unroll
+  for (int q = 0; q < PPT; ++q)
+    if (ok[q]) A.R[at<NM>(row, p0 + 32 * q, A.B, A.n_u)] = r[q];
 }
 
 __device__ __forceinline__ void cp16_dense(void* dst, const void* src) {
@@ -107,16 +116,22 @@ struct DenseTile {
   static constexpr int BYTES = (RB * N * NP * (int)sizeof(S) + 32 + 15) & ~15;
 };
 
+template <int N>
+struct DensePPT {  // pairs per lane (4 for N <= 12 measured slower on cfg5: 1.73 vs 1.53 ms)
+  static constexpr int value = 2;
+};
+
 template <typename S, int N, bool NM>
 __global__ void __launch_bounds__(128) k_dense(const DenseArgs<S> A, const int32_t* __restrict__ rows, int64_t nrows,
                                               int64_t blk0) {
   using TL = DenseTile<N, S>;
+  constexpr int PPT = DensePPT<N>::value;
   constexpr int NP = TL::NP, RB = TL::RB;
   __shared__ __align__(16) unsigned char s_blk[2][N > 0 ? TL::BYTES : 16];
   __shared__ int32_t s_cols[2][N > 0 ? RB * N : 1];
   const int warp = threadIdx.x >> 5, lane = threadIdx.x & 31;
   const int nwarps = blockDim.x >> 5;
-  const int nchunks = (A.B + 63) / 64;
+  const int nchunks = (A.B + 32 * PPT - 1) / (32 * PPT);
   const int64_t per = (nrows + gridDim.x - 1) / gridDim.x;
   const int64_t q0 = (int64_t)blockIdx.x * per;
   const int64_t q1 = min(nrows, q0 + per);
@@ -154,7 +169,7 @@ __global__ void __launch_bounds__(128) k_dense(const DenseArgs<S> A, const int32
       for (int r = 0; r < nr; ++r) {
         const int64_t row = __ldg(rows + q + r);
         for (int ch = warp; ch < nchunks; ch += nwarps)
-          dense_row<S, N, NM>(A, row, s_cols[st] + r * N, M + r * (N * NP), ch * 64 + lane);
+          dense_row<S, N, NM, PPT>(A, row, s_cols[st] + r * N, M + r * (N * NP), ch * 32 * PPT + lane);
       }
       __syncthreads();  // every warp is done with buffer st before it is refilled
       sh_cur = sh_nxt;
@@ -204,8 +219,6 @@ egfem_status launch_dense(const egfem_tensor* t, int32_t batch, egfem_layout lay
   const int dev = t->device & 63;
   if (!g_sms_dense[dev])
     EGFEM_CUDA_TRY(cudaDeviceGetAttribute(&g_sms_dense[dev], cudaDevAttrMultiProcessorCount, t->device));
-  const int chunks = (batch + 63) / 64;
-  const int threads = 32 * std::min(4, chunks);
   const bool nm = layout == EGFEM_LAYOUT_NODE_MAJOR;
   // one launch per stencil width; each a single wave of resident CTAs over its row list
   for (const auto& cls : t->dense_classes) {
@@ -217,6 +230,7 @@ egfem_status launch_dense(const egfem_tensor* t, int32_t batch, egfem_layout lay
     DenseArgs<S_> A{t->n_u, t->n_f, batch, t->row_fib, t->fib_j, t->blk_off, (const S_*)t->blk,              \
                     (const S_*)U, (const S_*)W, (S_*)R};                                                      \
     auto fn = nm ? k_dense<S_, N_, true> : k_dense<S_, N_, false>;                                            \
+    const int threads = 32 * std::min(4, (batch + 32 * DensePPT<N_>::value - 1) / (32 * DensePPT<N_>::value)); \
     int per_sm = 0;                                                                                           \
     EGFEM_CUDA_TRY(cudaOccupancyMaxActiveBlocksPerMultiprocessor(&per_sm, fn, threads, 0));                   \
     const int grid = (int)std::min<int64_t>(count, (int64_t)std::max(per_sm, 1) * g_sms_dense[dev]);         \
