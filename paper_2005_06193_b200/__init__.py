@@ -191,11 +191,12 @@ def egfem_tensor_build(mesh, V, W, form, quad=None, dtype=F64, device=0) -> Tens
     """Assemble T on `device` (egfem_tensor_build)."""
     coords = np.ascontiguousarray(mesh.coords, np.float64)
     cells = np.ascontiguousarray(mesh.cells, np.int32)
-    vd = np.ascontiguousarray(V.cell_dofs, np.int32)
-    wd = np.ascontiguousarray(W.cell_dofs, np.int32)
+    # cell_dofs None -> NULL: the canonical numbering (include/egfem.h egfem_space)
+    vd = None if V.cell_dofs is None else np.ascontiguousarray(V.cell_dofs, np.int32)
+    wd = None if W.cell_dofs is None else np.ascontiguousarray(W.cell_dofs, np.int32)
     m = _Mesh(mesh.dim, coords.shape[0], coords.ctypes.data, cells.shape[0], cells.ctypes.data)
-    sv = _Space(V.family, V.n_dofs, vd.ctypes.data)
-    sw = _Space(W.family, W.n_dofs, wd.ctypes.data)
+    sv = _Space(V.family, V.n_dofs, None if vd is None else vd.ctypes.data)
+    sw = _Space(W.family, W.n_dofs, None if wd is None else wd.ctypes.data)
     q = None
     if quad is not None:
         qb = np.ascontiguousarray(quad[0], np.float64)

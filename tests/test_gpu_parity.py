@@ -327,6 +327,26 @@ def test_validation_errors(eg):
     with pytest.raises(eg.EgfemError) as e:
         eg.egfem_tensor_build(bad, pr.V, pr.W, pr.form, device=0)
     assert e.value.status == 1
+    # F1/F2/F3 entry points
+    with pytest.raises(eg.EgfemError) as e:
+        eg.egfem_interp(t, I.INTERP_RECIPROCAL, float("nan"), u, w)  # k must be finite
+    assert e.value.status == 1
+    with pytest.raises(eg.EgfemError) as e:
+        eg.egfem_interp(t, 6, 0.0, u, w)  # no such kind
+    assert e.value.status == 1
+    with pytest.raises(eg.EgfemError) as e:  # bilinear form needs W = V
+        eg.egfem_bilinear_build(t, torch.zeros(t.nnz_csr, dtype=torch.float64, device="cuda"))
+    assert e.value.status == 2
+    with pytest.raises(eg.EgfemError) as e:  # x and y alias
+        eg.egfem_csr_spmv(t, torch.zeros(t.nnz_csr, dtype=torch.float64, device="cuda"), u, u)
+    assert e.value.status == 1
+    with pytest.raises(eg.EgfemError) as e:  # QUAD with N_f not a multiple of the cell count
+        eg.egfem_tensor_build(pr.mesh, pr.V, I.Space(I.QUAD, pr.mesh.n_cells * 3 + 1, None, None), pr.form, device=0)
+    assert e.value.status == 2
+    with pytest.raises(eg.EgfemError) as e:  # QUAD W cannot carry a differentiated k-slot
+        m1 = I.mesh_interval(4)
+        eg.egfem_tensor_build(m1, I.space_p1(m1), I.space_quad(m1, 3), I.FORM_CONV_K, device=0)
+    assert e.value.status == 3
 
 
 @pytest.mark.parametrize("name,nranks", [("cfg4", 2), ("cfg4", 3), ("cfg3", 4), ("cfg2", 3), ("cfg1", 5)])
