@@ -217,6 +217,26 @@ def run_ours(args):
     for _ in range(Wm):
         step()
     torch.cuda.synchronize()
+    # Single GPU: the step (interp + fused apply/Jacobian) is captured once into a CUDA graph and
+    # replayed (no per-step launch overhead; matters for the small configs).  N>1 keeps eager
+    # launches around the NCCL halo exchange.
+    graph = None
+    if world == 1 and not args.no_graph:
+        side = torch.cuda.Stream(dev)
+        side.wait_stream(stream)
+        with torch.cuda.stream(side):
+            step()  # warm-up on the capture stream's family
+        stream.wait_stream(side)
+        torch.cuda.synchronize()
+        graph = torch.cuda.CUDAGraph()
+        with torch.cuda.graph(graph):
+            cs = torch.cuda.current_stream(dev)
+            eg.egfem_interp(t, pr.interp, pr.p, u, w, chain, cs)
+            eg.egfem_apply_jacobian(t, eg.JAC_NEWTON, pr.interp, pr.p, u, w, chain, r, J, cs)
+        torch.cuda.synchronize()
+        for _ in range(Wm):
+            graph.replay()
+        torch.cuda.synchronize()
     if world > 1:
         dist.barrier()
     torch.cuda.synchronize()
@@ -227,17 +247,23 @@ def run_ours(args):
         for k in range(K):
             if flush:
                 scratch.zero_()
-            step(ev[k])
+            if graph is not None:
+                ev[k][0].record(stream)
+                graph.replay()
+                ev[k][3].record(stream)
+            else:
+                step(ev[k])
         stop.record(stream)
         torch.cuda.synchronize()
     if world > 1:
         dist.barrier()
     torch.cuda.synchronize()
-    launches = eg.launch_count() - l0
+    launches = eg.launch_count() - l0 if graph is None else 2 * K  # graph replays launch interp + fused
     ms = sum(e[0].elapsed_time(e[3]) for e in ev) if flush else start.elapsed_time(stop)
-    t_ex = np.mean([e[0].elapsed_time(e[1]) for e in ev])
-    t_interp = np.mean([e[1].elapsed_time(e[2]) for e in ev])
-    t_fused = np.mean([e[2].elapsed_time(e[3]) for e in ev])
+    if graph is None:
+        t_ex = np.mean([e[0].elapsed_time(e[1]) for e in ev])
+        t_interp = np.mean([e[1].elapsed_time(e[2]) for e in ev])
+        t_fused = np.mean([e[2].elapsed_time(e[3]) for e in ev])
     if world > 1:
         m = torch.tensor([ms], dtype=torch.float64, device=dev)
         dist.all_reduce(m, op=dist.ReduceOp.MAX)
@@ -256,6 +282,11 @@ def run_ours(args):
         b.record(stream)
         torch.cuda.synchronize()
         return a.elapsed_time(b) / n
+    if graph is not None:  # per-kernel times of the graphed step, from separate eager launches
+        t_ex = 0.0
+        t_interp = avg_ms(lambda: eg.egfem_interp(t, pr.interp, pr.p, u, w, chain, stream))
+        t_fused = avg_ms(lambda: eg.egfem_apply_jacobian(t, eg.JAC_NEWTON, pr.interp, pr.p, u, w, chain, r, J,
+                                                         stream))
     t_apply = avg_ms(lambda: eg.egfem_apply(t, u, w, r, stream))
     t_jac = avg_ms(lambda: eg.egfem_jacobian(t, eg.JAC_NEWTON, pr.interp, pr.p, u, w, chain, J, stream))
     t_pic = avg_ms(lambda: eg.egfem_jacobian(t, eg.JAC_PICARD, pr.interp, pr.p, None, w, None, J, stream))
@@ -323,7 +354,8 @@ def run_ours(args):
                    "l2": (f"working set {ws_bytes / 1e9:.2f} GB < 4 x L2 ({l2_bytes >> 20} MB): 512 MB write "
                           "between timed steps, step time = sum of per-step intervals") if flush else
                          f"working set {ws_bytes / 1e9:.2f} GB >= 4 x L2 ({l2_bytes >> 20} MB); no flush",
-                   "parallelism": f"row-partition x{world}" if world > 1 else "single GPU"},
+                   "parallelism": f"row-partition x{world}" if world > 1 else "single GPU",
+                   "launch": "CUDA graph (interp + fused) replayed per step" if graph is not None else "eager"},
         "roofline": {"bound": "hbm", "kernel": "k_cell<S,D1,G,CPL,FREG,DO_R=1,NewtonP0> (egfem_apply_jacobian, cell-major P0 path)",
                      "achieved": achieved, "peak": peak, "peak_kind": peak_kind, "unit": "GB/s",
                      "frac": achieved / peak, "algorithmic_bytes": fused_bytes,
@@ -543,6 +575,7 @@ def main():
     ap.add_argument("--dtype", default="f64", choices=["f64", "f32"])
     ap.add_argument("--batch", type=int, default=None)
     ap.add_argument("--no-cpu-baseline", action="store_true")
+    ap.add_argument("--no-graph", action="store_true", help="eager launches instead of a CUDA graph (N=1)")
     args = ap.parse_args()
     if args.impl == "reference":
         run_reference(args)
