@@ -423,3 +423,33 @@ def test_bilinear_gfem(eg, orc, name):
     t2 = eg.egfem_tensor_build(pr2.mesh, pr2.V, pr2.W, pr2.form, device=0)
     with pytest.raises(eg.EgfemError):
         eg.egfem_bilinear_build(t2, torch.empty(t2.nnz_csr, dtype=torch.float64, device="cuda"))
+
+
+@pytest.mark.parametrize("name", ["cfg4", "cfg3", "cfg2"])
+def test_cuda_graph_replay_bitwise(eg, name):
+    """The bench step (interp + fused apply/Newton) captured into a CUDA graph and replayed gives
+    bitwise the eager results (no host work in the launch path is stream-ordered)."""
+    import torch
+    pr = I.make_problem(name, n=I.SMALL_N[name])
+    t = eg.egfem_tensor_build(pr.mesh, pr.V, pr.W, pr.form, device=0)
+    from gpu_helpers import needs_chain
+    u = torch.tensor(pr.u, device="cuda")
+    w = torch.empty(t.n_f, dtype=torch.float64, device="cuda")
+    chain = torch.empty(t.n_f * (pr.mesh.dim + 1), dtype=torch.float64, device="cuda") if needs_chain(pr) else None
+    r = torch.empty(t.n_u, dtype=torch.float64, device="cuda")
+    J = torch.empty(t.nnz_csr, dtype=torch.float64, device="cuda")
+
+    def step(s):
+        eg.egfem_interp(t, pr.interp, pr.p, u, w, chain, s)
+        eg.egfem_apply_jacobian(t, eg.JAC_NEWTON, pr.interp, pr.p, u, w, chain, r, J, s)
+    step(torch.cuda.current_stream())
+    torch.cuda.synchronize()
+    r0, J0 = r.clone(), J.clone()
+    r.zero_()
+    J.zero_()
+    g = torch.cuda.CUDAGraph()
+    with torch.cuda.graph(g):
+        step(torch.cuda.current_stream())
+    g.replay()
+    torch.cuda.synchronize()
+    assert torch.equal(r, r0) and torch.equal(J, J0)
