@@ -53,20 +53,26 @@ struct Vec2<float> {
 };
 
 // PPT pairs per lane (lane, lane+32, ...): each staged block value feeds PPT FMAs and each W
-// value N; even and odd b accumulate in separate chains.
+// value N; even and odd b accumulate in separate chains.  W at the row's stencil is loaded by
+// load_w (one row ahead of its use, see k_dense).
 template <typename S, int N, bool NM, int PPT>
-__device__ __forceinline__ void dense_row(const DenseArgs<S>& A, int64_t row, const int32_t* cols, const S* M, int p0) {
-  constexpr int NP = N + (N & 1);
-  bool ok[PPT];
-#pragma unroll
-  for (int q = 0; q < PPT; ++q) ok[q] = p0 + 32 * q < A.B;
-  S wv[PPT][N];
+__device__ __forceinline__ void load_w(const DenseArgs<S>& A, const int32_t* cols, int p0, S (&wv)[PPT][N]) {
 #pragma unroll
   for (int b = 0; b < N; ++b) {
     const int64_t k = cols[b];  // smem broadcast
 #pragma unroll
-    for (int q = 0; q < PPT; ++q) wv[q][b] = ok[q] ? __ldg(A.W + at<NM>(k, p0 + 32 * q, A.B, A.n_f)) : S(0);
+    for (int q = 0; q < PPT; ++q)
+      wv[q][b] = (p0 + 32 * q < A.B) ? __ldg(A.W + at<NM>(k, p0 + 32 * q, A.B, A.n_f)) : S(0);
   }
+}
+
+template <typename S, int N, bool NM, int PPT>
+__device__ __forceinline__ void dense_row(const DenseArgs<S>& A, int64_t row, const int32_t* cols, const S* M, int p0,
+                                          const S (&wv)[PPT][N]) {
+  constexpr int NP = N + (N & 1);
+  bool ok[PPT];
+#pragma unroll
+  for (int q = 0; q < PPT; ++q) ok[q] = p0 + 32 * q < A.B;
   S r[PPT];
 #pragma unroll
   for (int q = 0; q < PPT; ++q) r[q] = S(0);
@@ -166,10 +172,27 @@ __global__ void __launch_bounds__(128) k_dense(const DenseArgs<S> A, const int32
       __syncthreads();  // this batch's blocks and columns are in buffer st for every warp
       const int nr = (int)(q1 - q < (int64_t)RB ? q1 - q : (int64_t)RB);
       const S* M = reinterpret_cast<const S*>(s_blk[st]) + sh_cur;
-      for (int r = 0; r < nr; ++r) {
-        const int64_t row = __ldg(rows + q + r);
-        for (int ch = warp; ch < nchunks; ch += nwarps)
-          dense_row<S, N, NM, PPT>(A, row, s_cols[st] + r * N, M + r * (N * NP), ch * 32 * PPT + lane);
+      for (int ch = warp; ch < nchunks; ch += nwarps) {
+        const int p0 = ch * 32 * PPT + lane;
+        if constexpr (N > 12) {  // wide stencils: no register room for a second W set
+          for (int r = 0; r < nr; ++r) {
+            S wa[PPT][N];
+            load_w<S, N, NM, PPT>(A, s_cols[st] + r * N, p0, wa);
+            dense_row<S, N, NM, PPT>(A, __ldg(rows + q + r), s_cols[st] + r * N, M + r * (N * NP), p0, wa);
+          }
+          continue;
+        }
+        S wa[PPT][N], wb[PPT][N];  // W of row r (in use) and row r + 1 (in flight)
+        load_w<S, N, NM, PPT>(A, s_cols[st], p0, wa);
+        for (int r = 0; r < nr; r += 2) {
+          if (r + 1 < nr) load_w<S, N, NM, PPT>(A, s_cols[st] + (r + 1) * N, p0, wb);
+          dense_row<S, N, NM, PPT>(A, __ldg(rows + q + r), s_cols[st] + r * N, M + r * (N * NP), p0, wa);
+          if (r + 1 < nr) {
+            if (r + 2 < nr) load_w<S, N, NM, PPT>(A, s_cols[st] + (r + 2) * N, p0, wa);
+            dense_row<S, N, NM, PPT>(A, __ldg(rows + q + r + 1), s_cols[st] + (r + 1) * N, M + (r + 1) * (N * NP), p0,
+                                     wb);
+          }
+        }
       }
       __syncthreads();  // every warp is done with buffer st before it is refilled
       sh_cur = sh_nxt;
