@@ -268,6 +268,41 @@ egfem_status egfem_partition(const egfem_tensor* global, int32_t nranks, int32_t
 egfem_status egfem_partition_rows(int64_t n_rows, const int64_t* row_nnz_prefix, int32_t nranks,
                                   int64_t* out_bounds);
 
+/* Interior / boundary split of a tensor's work, for overlapping the u-halo exchange with
+ * compute (§8(e); the step is PAPER.md L251/L290 restricted to a row range).  Rows
+ * [row_lo, row_hi) read only owned u (columns, and for W = V the k indices, inside the
+ * owned window [row_begin − col_begin, row_end − col_begin)), and interp work items
+ * [w_lo, w_hi) read only owned u and cover every w those rows read.  So a rank can run
+ *   interp_range(w_lo, w_hi) ; apply_jacobian_rows(row_lo, row_hi)      while u's halo is in flight,
+ *   interp_range over the rest ; apply_jacobian_rows over the rest       after it has arrived,
+ * and obtain bitwise the results of the whole-range calls.  Interp work items are W DOFs for
+ * W = V and mesh cells for cell-wise W (P0 / QUAD / P2).  A global (unpartitioned) tensor
+ * has no halo: its interior is everything.  An empty interior is returned as lo = hi = 0.
+ * Outputs are host scalars (any may be NULL). */
+egfem_status egfem_interior(const egfem_tensor* t, int64_t* row_lo, int64_t* row_hi, int64_t* w_lo,
+                            int64_t* w_hi);
+
+/* egfem_interp restricted to interp work items [lo, hi) (units as in egfem_interior; the
+ * buffers are the whole-tensor u, w, chain).  0 <= lo <= hi <= n_items, else
+ * INVALID_ARGUMENT. */
+egfem_status egfem_interp_range(const egfem_tensor* t, egfem_interp_kind kind, double p, const void* u,
+                                void* w, void* chain, int64_t lo, int64_t hi, egfem_stream_t stream);
+
+/* egfem_apply_jacobian restricted to rows [row_lo, row_hi) (r and csr_vals are the
+ * whole-tensor buffers; only those rows' entries are written).  A proper sub-range needs
+ * one of the row-group kernels (rows of at most 256 nonzeros); the general tile path
+ * returns UNSUPPORTED for it. */
+egfem_status egfem_apply_jacobian_rows(const egfem_tensor* t, egfem_jac_mode mode, egfem_interp_kind kind,
+                                       double p, const void* u, const void* w, const void* chain, void* r,
+                                       void* csr_vals, int64_t row_lo, int64_t row_hi,
+                                       egfem_stream_t stream);
+
+/* Pure host helper behind egfem_interior: the longest run [lo, hi) of consecutive rows of a
+ * CSR pattern (host int64 row_ptr[n_rows+1], int32 col) whose columns all lie in
+ * [own_lo, own_hi); the first such run on ties, lo = hi = 0 when there is none. */
+egfem_status egfem_interior_rows(int64_t n_rows, const int64_t* row_ptr, const int32_t* col, int64_t own_lo,
+                                 int64_t own_hi, int64_t* lo, int64_t* hi);
+
 /* Halo gather/scatter for non-contiguous exchanges: send_buf[q] = u_local[idx[q]],
  * u_local[idx[q]] = recv_buf[q] (device arrays, n entries, handle's dtype). */
 egfem_status egfem_halo_pack(const egfem_tensor* local, const int32_t* d_idx, int64_t n,

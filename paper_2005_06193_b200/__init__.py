@@ -41,7 +41,8 @@ EXPORTS = ("egfem_tensor_build", "egfem_tensor_from_coo", "egfem_tensor_destroy"
            "egfem_apply_batched", "egfem_jacobian", "egfem_apply_jacobian", "egfem_partition",
            "egfem_partition_rows", "egfem_halo_pack", "egfem_halo_unpack", "egfem_launch_count",
            "egfem_status_string", "egfem_last_error", "egfem_bilinear_build", "egfem_csr_spmv",
-           "egfem_bilinear_jacobian")
+           "egfem_bilinear_jacobian", "egfem_interior", "egfem_interp_range", "egfem_apply_jacobian_rows",
+           "egfem_interior_rows")
 
 
 class EgfemError(RuntimeError):
@@ -88,6 +89,10 @@ def _load():
         "egfem_bilinear_build": [P, P, P],
         "egfem_csr_spmv": [P, P, P, P, P],
         "egfem_bilinear_jacobian": [P, P, st, ctypes.c_double, P, P, P],
+        "egfem_interior": [P, P, P, P, P],
+        "egfem_interp_range": [P, st, ctypes.c_double, P, P, P, i64, i64, P],
+        "egfem_apply_jacobian_rows": [P, st, st, ctypes.c_double, P, P, P, P, P, i64, i64, P],
+        "egfem_interior_rows": [i64, P, P, i64, i64, P, P],
     }
     for name, args in sig.items():
         f = getattr(L, name)
@@ -260,6 +265,34 @@ def egfem_apply_jacobian(t: Tensor, mode, kind, p, u, w, chain, r, csr_vals, str
     _check("egfem_apply_jacobian", _lib.egfem_apply_jacobian(t.h, mode, kind, float(p), _dptr(u), _dptr(w),
                                                              _dptr(chain), _dptr(r), _dptr(csr_vals),
                                                              _stream(stream)))
+
+
+def egfem_interp_range(t: Tensor, kind, p, u, w, chain, lo, hi, stream=None):
+    _check("egfem_interp_range", _lib.egfem_interp_range(t.h, kind, float(p), _dptr(u), _dptr(w), _dptr(chain),
+                                                         int(lo), int(hi), _stream(stream)))
+
+
+def egfem_apply_jacobian_rows(t: Tensor, mode, kind, p, u, w, chain, r, csr_vals, row_lo, row_hi, stream=None):
+    _check("egfem_apply_jacobian_rows",
+           _lib.egfem_apply_jacobian_rows(t.h, mode, kind, float(p), _dptr(u), _dptr(w), _dptr(chain), _dptr(r),
+                                          _dptr(csr_vals), int(row_lo), int(row_hi), _stream(stream)))
+
+
+def egfem_interior(t: Tensor):
+    """(row_lo, row_hi, w_lo, w_hi): the rows / interp items that read only owned u."""
+    b = [np.zeros(1, np.int64) for _ in range(4)]
+    _check("egfem_interior", _lib.egfem_interior(t.h, *[_np_ptr(x) for x in b]))
+    return tuple(int(x[0]) for x in b)
+
+
+def egfem_interior_rows(row_ptr, col, own_lo, own_hi):
+    """Host helper: longest run of rows whose columns all lie in [own_lo, own_hi)."""
+    rp = np.ascontiguousarray(row_ptr, dtype=np.int64)
+    c = np.ascontiguousarray(col, dtype=np.int32)
+    lo, hi = np.zeros(1, np.int64), np.zeros(1, np.int64)
+    _check("egfem_interior_rows", _lib.egfem_interior_rows(len(rp) - 1, _np_ptr(rp), _np_ptr(c), int(own_lo),
+                                                           int(own_hi), _np_ptr(lo), _np_ptr(hi)))
+    return int(lo[0]), int(hi[0])
 
 
 def egfem_partition_rows(prefix, nranks):

@@ -298,8 +298,8 @@ egfem_status egfem_tensor_export(const egfem_tensor* t, int64_t* t_row_ptr, int3
   return export_arrays(t, t_row_ptr, t_j, t_k, t_val, csr_row_ptr, csr_col, slot_ij, slot_ik, loc);
 }
 
-egfem_status egfem_interp(const egfem_tensor* t, egfem_interp_kind kind, double p, const void* u, void* w,
-                          void* chain, egfem_stream_t stream) {
+static egfem_status interp_check(const egfem_tensor* t, egfem_interp_kind kind, double p, const void* u,
+                                 const void* w, const void* chain) {
   if (!t) return fail(EGFEM_ERR_INVALID_ARGUMENT, "tensor is NULL");
   if (kind < EGFEM_INTERP_IDENTITY || kind > EGFEM_INTERP_RECIPROCAL)
     return fail(EGFEM_ERR_INVALID_ARGUMENT, "bad interp kind");
@@ -339,8 +339,25 @@ egfem_status egfem_interp(const egfem_tensor* t, egfem_interp_kind kind, double 
         return fail(EGFEM_ERR_UNSUPPORTED, "P1_TO_P2_SQUARE needs V = P1, W = P2 (2D)");
       if (chain) return fail(EGFEM_ERR_INVALID_ARGUMENT, "chain is only produced by GRADPOW_P0");
   }
+  return EGFEM_OK;
+}
+
+egfem_status egfem_interp(const egfem_tensor* t, egfem_interp_kind kind, double p, const void* u, void* w,
+                          void* chain, egfem_stream_t stream) {
+  egfem_status st = interp_check(t, kind, p, u, w, chain);
+  if (st) return st;
   DeviceGuard g(t->device);
-  return launch_interp(t, kind, p, u, w, chain, (cudaStream_t)stream);
+  return launch_interp(t, kind, p, u, w, chain, 0, interp_items(t, kind), (cudaStream_t)stream);
+}
+
+egfem_status egfem_interp_range(const egfem_tensor* t, egfem_interp_kind kind, double p, const void* u, void* w,
+                                void* chain, int64_t lo, int64_t hi, egfem_stream_t stream) {
+  egfem_status st = interp_check(t, kind, p, u, w, chain);
+  if (st) return st;
+  if (lo < 0 || hi < lo || hi > interp_items(t, kind))
+    return fail(EGFEM_ERR_INVALID_ARGUMENT, "interp range outside [0, n_items]");
+  DeviceGuard g(t->device);
+  return launch_interp(t, kind, p, u, w, chain, lo, hi, (cudaStream_t)stream);
 }
 
 egfem_status egfem_apply(const egfem_tensor* t, const void* u, const void* w, void* r, egfem_stream_t stream) {
@@ -442,6 +459,60 @@ egfem_status egfem_apply_jacobian(const egfem_tensor* t, egfem_jac_mode mode, eg
   if ((st = jac_mode_code(t, mode, kind, p, u, chain, &code))) return st;
   DeviceGuard g(t->device);
   return launch_tile(t, true, code, kind, p, u, w, chain, r, csr_vals, (cudaStream_t)stream);
+}
+
+egfem_status egfem_apply_jacobian_rows(const egfem_tensor* t, egfem_jac_mode mode, egfem_interp_kind kind, double p,
+                                       const void* u, const void* w, const void* chain, void* r, void* csr_vals,
+                                       int64_t row_lo, int64_t row_hi, egfem_stream_t stream) {
+  if (!t) return fail(EGFEM_ERR_INVALID_ARGUMENT, "tensor is NULL");
+  egfem_status st;
+  if ((st = check_dev_ptr(t, u, "u", true)) || (st = check_dev_ptr(t, w, "w", true)) ||
+      (st = check_dev_ptr(t, r, "r", true)) || (st = check_dev_ptr(t, csr_vals, "csr_vals", true)))
+    return st;
+  if (row_lo < 0 || row_hi < row_lo || row_hi > t->n_u)
+    return fail(EGFEM_ERR_INVALID_ARGUMENT, "row range outside [0, n_u]");
+  int code = 0;
+  if ((st = jac_mode_code(t, mode, kind, p, u, chain, &code))) return st;
+  DeviceGuard g(t->device);
+  return launch_tile_rows(t, row_lo, row_hi, true, code, kind, p, u, w, chain, r, csr_vals, (cudaStream_t)stream);
+}
+
+egfem_status egfem_interior(const egfem_tensor* t, int64_t* row_lo, int64_t* row_hi, int64_t* w_lo, int64_t* w_hi) {
+  if (!t) return fail(EGFEM_ERR_INVALID_ARGUMENT, "tensor is NULL");
+  const bool all = t->int_row_lo < 0;  // global tensor: no halo
+  const int64_t items = t->w_is_v ? t->n_f : t->n_cells;
+  if (row_lo) *row_lo = all ? 0 : t->int_row_lo;
+  if (row_hi) *row_hi = all ? t->n_u : t->int_row_hi;
+  if (w_lo) *w_lo = all ? 0 : t->int_w_lo;
+  if (w_hi) *w_hi = all ? items : t->int_w_hi;
+  return EGFEM_OK;
+}
+
+egfem_status egfem_interior_rows(int64_t n_rows, const int64_t* row_ptr, const int32_t* col, int64_t own_lo,
+                                 int64_t own_hi, int64_t* lo, int64_t* hi) {
+  if (n_rows < 0 || !row_ptr || (!col && n_rows > 0 && row_ptr[n_rows] > 0) || !lo || !hi)
+    return fail(EGFEM_ERR_INVALID_ARGUMENT, "bad arguments");
+  int64_t best_lo = 0, best_hi = 0, run = -1;
+  for (int64_t i = 0; i <= n_rows; ++i) {
+    bool ok = i < n_rows;
+    if (ok)
+      for (int64_t e = row_ptr[i]; e < row_ptr[i + 1]; ++e)
+        if (col[e] < own_lo || col[e] >= own_hi) {
+          ok = false;
+          break;
+        }
+    if (ok && run < 0) run = i;
+    if (!ok && run >= 0) {
+      if (i - run > best_hi - best_lo) {
+        best_lo = run;
+        best_hi = i;
+      }
+      run = -1;
+    }
+  }
+  *lo = best_lo;
+  *hi = best_hi;
+  return EGFEM_OK;
 }
 
 egfem_status egfem_bilinear_build(const egfem_tensor* t, void* b_vals, egfem_stream_t stream) {
@@ -678,6 +749,51 @@ egfem_status egfem_partition(const egfem_tensor* G, int32_t nranks, int32_t rank
         (ncl && cudaMemcpy(t->wdofs, lw.data(), 4 * lw.size(), cudaMemcpyHostToDevice)) ||
         (ncl && cudaMemcpy(t->wcell, lw.data(), 4 * lw.size(), cudaMemcpyHostToDevice)))
       return bail(fail(EGFEM_ERR_CUDA, "cudaMemcpy failed"));
+  }
+  // interior / boundary split (egfem_interior): rows reading only owned u, and the interp
+  // items covering their w that read only owned u
+  {
+    const int64_t olo = rb - cb, ohi = re - cb;
+    std::vector<int32_t> kcol;  // per nonzero: the u index its w depends on (W = V: k), for the run test
+    int64_t ia = 0, ib = 0;
+    egfem_interior_rows(nr, lrf.data(), fj.data(), olo, ohi, &ia, &ib);
+    if (!p0) {
+      // W = V: the k of every nonzero of a run row must be owned too; shrink the run to its
+      // longest sub-run with that property
+      std::vector<int64_t> rp(ib - ia + 1);
+      for (int64_t i = ia; i <= ib; ++i) rp[i - ia] = lfn[lrf[i]] - lfn[lrf[ia]];
+      kcol.resize(rp.back());
+      for (int64_t e = 0; e < (int64_t)kcol.size(); ++e) kcol[e] = (int32_t)(nk[lfn[lrf[ia]] + e] & kKMaskAny);
+      int64_t a = 0, b = 0;
+      egfem_interior_rows(ib - ia, rp.data(), kcol.data(), olo, ohi, &a, &b);
+      ib = ia + b;
+      ia = ia + a;
+      t->int_w_lo = ia < ib ? olo : 0;
+      t->int_w_hi = ia < ib ? ohi : 0;
+    } else if (ia < ib) {
+      // P0: the cells of rows [ia, ib) (local cell ids ascend with the global ones) must read
+      // owned vertices only, and so must every cell between them (one contiguous item range)
+      int64_t ca = INT64_MAX, cz = -1;
+      for (int64_t e = lfn[lrf[ia]]; e < (int64_t)lfn[lrf[ib]]; ++e) {
+        const int64_t c = nk[e] & kKMask;
+        ca = std::min(ca, c);
+        cz = std::max(cz, c);
+      }
+      bool ok = cz >= ca;
+      if (ok) {
+        const int d1 = G->dim + 1;
+        std::vector<int32_t> hc(d1 * (cz + 1 - ca));
+        ok = cudaMemcpy(hc.data(), t->cells + ca * d1, 4 * hc.size(), cudaMemcpyDeviceToHost) == cudaSuccess;
+        for (size_t q = 0; ok && q < hc.size(); ++q) ok = hc[q] >= olo && hc[q] < ohi;
+      }
+      t->int_w_lo = ok ? ca : 0;
+      t->int_w_hi = ok ? cz + 1 : 0;
+      if (!ok) ia = ib = 0;
+    } else {
+      t->int_w_lo = t->int_w_hi = 0;
+    }
+    t->int_row_lo = ia;
+    t->int_row_hi = ib;
   }
   // tiles of the local rows
   {

@@ -98,6 +98,8 @@ struct egfem_tensor {
 
   // partition bookkeeping (global handles: 0 / identity)
   int64_t row_begin = 0, col_begin = 0;
+  // local tensors: rows / interp items that read only owned u (egfem_interior); -1 = all
+  int64_t int_row_lo = -1, int_row_hi = -1, int_w_lo = -1, int_w_hi = -1;
 };
 
 namespace egfem {
@@ -116,7 +118,11 @@ cudaError_t dmalloc_padded(void** p, size_t bytes);
 
 // compute kernels (egfem_kernels.cu)
 egfem_status launch_interp(const egfem_tensor* t, egfem_interp_kind kind, double p, const void* u, void* w,
-                           void* chain, cudaStream_t s);
+                           void* chain, int64_t lo, int64_t hi, cudaStream_t s);
+int64_t interp_items(const egfem_tensor* t, egfem_interp_kind kind);
+egfem_status launch_tile_rows(const egfem_tensor* t, int64_t lo, int64_t hi, bool do_r, int jac,
+                              egfem_interp_kind kind, double p, const void* u, const void* w, const void* chain,
+                              void* r, void* csr_vals, cudaStream_t s);
 egfem_status launch_tile(const egfem_tensor* t, bool do_r, int jac, egfem_interp_kind kind, double p, const void* u,
                          const void* w, const void* chain, void* r, void* csr_vals, cudaStream_t s);
 egfem_status launch_rows(const egfem_tensor* t, bool do_r, int jac, egfem_interp_kind kind, double p, const void* u,

@@ -748,42 +748,61 @@ __global__ void k_halo(const int32_t* __restrict__ idx, int64_t n, const S* __re
 
 }  // namespace
 
+// Interp work items: W DOFs for the pointwise kinds on W = V, mesh cells otherwise.
+static bool interp_pointwise_wv(const egfem_tensor* t, egfem_interp_kind kind) {
+  return kind == EGFEM_INTERP_IDENTITY || (kind == EGFEM_INTERP_SQUARE && t->w_is_v) ||
+         (kind == EGFEM_INTERP_RECIPROCAL && t->w_is_v);
+}
+int64_t interp_items(const egfem_tensor* t, egfem_interp_kind kind) {
+  return interp_pointwise_wv(t, kind) ? t->n_f : t->n_cells;
+}
+
+// Items [lo, hi) of the work: every kernel runs on base pointers shifted to item lo (cell
+// records, V/W DOF tables, and for the IOTA / copy kernels w and chain), so a sub-range is
+// the same per-item arithmetic as the whole call.
 egfem_status launch_interp(const egfem_tensor* t, egfem_interp_kind kind, double p, const void* u, void* w,
-                           void* chain, cudaStream_t s) {
+                           void* chain, int64_t lo, int64_t hi, cudaStream_t s) {
   const bool f64 = t->dtype == EGFEM_F64;
-  if (kind == EGFEM_INTERP_IDENTITY || (kind == EGFEM_INTERP_SQUARE && t->w_is_v) ||
-      (kind == EGFEM_INTERP_RECIPROCAL && t->w_is_v)) {
-    const int64_t n = t->n_f;
+  const size_t vs = f64 ? 8 : 4;
+  const int64_t n = hi - lo;
+  if (n <= 0) return EGFEM_OK;
+  if (interp_pointwise_wv(t, kind)) {
     const int grid = std::max(1, std::min(nblk(n), 148 * 16));
     const int mode = kind == EGFEM_INTERP_IDENTITY ? 0 : (kind == EGFEM_INTERP_SQUARE ? 1 : 2);
+    const void* ul = (const char*)u + vs * lo;
+    void* wl = (char*)w + vs * lo;
     if (f64)
-      k_interp_copy<double><<<grid, 256, 0, s>>>((const double*)u, (double*)w, n, mode, p);
+      k_interp_copy<double><<<grid, 256, 0, s>>>((const double*)ul, (double*)wl, n, mode, p);
     else
-      k_interp_copy<float><<<grid, 256, 0, s>>>((const float*)u, (float*)w, n, mode, p);
+      k_interp_copy<float><<<grid, 256, 0, s>>>((const float*)ul, (float*)wl, n, mode, p);
     count_launch();
   } else if (kind == EGFEM_INTERP_RECIPROCAL || kind == EGFEM_INTERP_SQUARE) {  // cell-wise W, V = P1
-    if (t->n_cells > 0) {
-      const int mode = kind == EGFEM_INTERP_RECIPROCAL ? 0 : 1;
-      if (f64)
-        k_interp_points<double><<<nblk(t->n_cells, 128), 128, 0, s>>>(t->vdofs, t->wdofs, t->wpts, t->n_cells, t->dim + 1,
-                                                                 t->nwc, (const double*)u, (double*)w, (double*)chain,
-                                                                 mode, p);
-      else
-        k_interp_points<float><<<nblk(t->n_cells, 128), 128, 0, s>>>(t->vdofs, t->wdofs, t->wpts, t->n_cells, t->dim + 1,
-                                                                t->nwc, (const float*)u, (float*)w, (float*)chain,
-                                                                mode, p);
-      count_launch();
-    }
+    const int mode = kind == EGFEM_INTERP_RECIPROCAL ? 0 : 1;
+    const int d1 = t->dim + 1;
+    const int32_t* vd = t->vdofs + lo * d1;
+    const int32_t* wd = t->wdofs + lo * t->nwc;
+    if (f64)
+      k_interp_points<double><<<nblk(n, 128), 128, 0, s>>>(vd, wd, t->wpts, n, d1, t->nwc, (const double*)u,
+                                                           (double*)w, (double*)chain, mode, p);
+    else
+      k_interp_points<float><<<nblk(n, 128), 128, 0, s>>>(vd, wd, t->wpts, n, d1, t->nwc, (const float*)u,
+                                                          (float*)w, (float*)chain, mode, p);
+    count_launch();
   } else if (kind == EGFEM_INTERP_GRADPOW_P0 || kind == EGFEM_INTERP_MINSURF_P0) {
-    const int grid = std::max(1, nblk(t->n_cells, 128));  // capped at one resident wave below
-    if (t->n_cells > 0) {
+    const int grid = std::max(1, nblk(n, 128));  // capped at one resident wave below
+    const int d1 = t->dim + 1;
+    const int32_t* cl = t->cells + lo * d1;
+    const int32_t* vd = t->vdofs + lo * t->nV;
+    const int32_t* wd = t->wdofs + lo * t->nwc;
 #define EGFEM_GP3(S, D, SA, IO)                                                                       \
   do {                                                                                                \
     int per_sm = 0;                                                                                   \
     cudaOccupancyMaxActiveBlocksPerMultiprocessor(&per_sm, k_interp_gradpow<S, D, SA, IO>, 128, 0);   \
     const int g = (int)std::min<int64_t>(grid, (int64_t)std::max(per_sm, 1) * 148);                   \
-    k_interp_gradpow<S, D, SA, IO><<<g, 128, 0, s>>>(D == 3 ? t->coords4 : t->coords, t->cells, t->vdofs, \
-                                                     t->wdofs, t->n_cells, (const S*)u, (S*)w, (S*)chain, p, \
+    S* wl = IO ? (S*)w + lo : (S*)w;                                                                  \
+    S* cl2 = (IO && chain) ? (S*)chain + lo * (D + 1) : (S*)chain;                                    \
+    k_interp_gradpow<S, D, SA, IO><<<g, 128, 0, s>>>(D == 3 ? t->coords4 : t->coords, cl, vd, wd, n,  \
+                                                     (const S*)u, wl, cl2, p,                         \
                                                      kind == EGFEM_INTERP_MINSURF_P0, t->nwc);         \
   } while (0)
 #define EGFEM_GP(S, D)                                                          \
@@ -791,25 +810,22 @@ egfem_status launch_interp(const egfem_tensor* t, egfem_interp_kind kind, double
     if (t->vdofs_is_cells && t->wdofs_is_iota) EGFEM_GP3(S, D, true, true);     \
     else EGFEM_GP3(S, D, false, false);                                         \
   } while (0)
-      if (f64) {
-        if (t->dim == 1) EGFEM_GP(double, 1); else if (t->dim == 2) EGFEM_GP(double, 2); else EGFEM_GP(double, 3);
-      } else {
-        if (t->dim == 1) EGFEM_GP(float, 1); else if (t->dim == 2) EGFEM_GP(float, 2); else EGFEM_GP(float, 3);
-      }
+    if (f64) {
+      if (t->dim == 1) EGFEM_GP(double, 1); else if (t->dim == 2) EGFEM_GP(double, 2); else EGFEM_GP(double, 3);
+    } else {
+      if (t->dim == 1) EGFEM_GP(float, 1); else if (t->dim == 2) EGFEM_GP(float, 2); else EGFEM_GP(float, 3);
+    }
 #undef EGFEM_GP3
 #undef EGFEM_GP
-      count_launch();
-    }
+    count_launch();
   } else {
-    if (t->n_cells > 0) {
-      if (f64)
-        k_interp_p1p2sq<double><<<nblk(t->n_cells), 256, 0, s>>>(t->vdofs, t->wdofs, t->n_cells, (const double*)u,
-                                                                 (double*)w);
-      else
-        k_interp_p1p2sq<float><<<nblk(t->n_cells), 256, 0, s>>>(t->vdofs, t->wdofs, t->n_cells, (const float*)u,
-                                                                (float*)w);
-      count_launch();
-    }
+    const int32_t* vd = t->vdofs + lo * 3;
+    const int32_t* wd = t->wdofs + lo * 6;
+    if (f64)
+      k_interp_p1p2sq<double><<<nblk(n), 256, 0, s>>>(vd, wd, n, (const double*)u, (double*)w);
+    else
+      k_interp_p1p2sq<float><<<nblk(n), 256, 0, s>>>(vd, wd, n, (const float*)u, (float*)w);
+    count_launch();
   }
   EGFEM_CUDA_TRY(cudaGetLastError());
   return EGFEM_OK;
@@ -828,6 +844,60 @@ egfem_status launch_tile(const egfem_tensor* t, bool do_r, int jac, egfem_interp
   if (!tile && rows_path_ok(t, jac)) return launch_rows(t, do_r, jac, kind, p, u, w, chain, r, csr_vals, s);
   if (t->dtype == EGFEM_F64) return tile_dispatch<double>(t, do_r, jac, kind, p, u, w, chain, r, csr_vals, s);
   return tile_dispatch<float>(t, do_r, jac, kind, p, u, w, chain, r, csr_vals, s);
+}
+
+// Rows [lo, hi): a shallow view of the tensor whose row arrays start at row lo (row_nz,
+// row_fib hold absolute nonzero / fiber offsets, so the streams, csr and the fiber data are
+// addressed as in the whole call) and whose diagonal offset moves with it; r is shifted.
+// Only the row-group kernels (cell-major, segmented) take a view.
+egfem_status launch_tile_rows(const egfem_tensor* t, int64_t lo, int64_t hi, bool do_r, int jac,
+                              egfem_interp_kind kind, double p, const void* u, const void* w, const void* chain,
+                              void* r, void* csr_vals, cudaStream_t s) {
+  if (lo == 0 && hi == t->n_u) return launch_tile(t, do_r, jac, kind, p, u, w, chain, r, csr_vals, s);
+  if (hi <= lo) return EGFEM_OK;
+  static const char* force = getenv("EGFEM_PATH");
+  const bool tile = force && force[0] == 't';
+  const bool rows_only = force && force[0] == 'r';
+  const bool cells = !tile && !rows_only && cells_path_ok(t, jac);
+  if (!cells && (tile || !rows_path_ok(t, jac))) {
+    set_error("row sub-ranges need a row-group kernel (rows of at most 256 nonzeros)");
+    return EGFEM_ERR_UNSUPPORTED;
+  }
+  egfem_tensor v;
+  v.device = t->device;
+  v.dtype = t->dtype;
+  v.has_mesh = t->has_mesh;
+  v.dim = t->dim;
+  v.n_u = hi - lo;
+  v.n_f = t->n_f;
+  v.vfam = t->vfam;
+  v.wfam = t->wfam;
+  v.form = t->form;
+  v.nnz = t->nnz;
+  v.n_fib = t->n_fib;
+  v.w_is_v = t->w_is_v;
+  v.w_p0 = t->w_p0;
+  v.nwc = t->nwc;
+  v.newton_wv_ok = t->newton_wv_ok;
+  v.max_row_nnz = t->max_row_nnz;
+  v.max_row_fib = t->max_row_fib;
+  v.row_fib = t->row_fib + lo;
+  v.row_nz = t->row_nz + lo;
+  v.fib_j = t->fib_j;
+  v.fib_nz = t->fib_nz;
+  v.nz_k = t->nz_k;
+  v.nz_val = t->nz_val;
+  v.nz_aux = t->nz_aux;
+  v.nz_kpos = t->nz_kpos;
+  v.fib_kr = t->fib_kr;
+  v.ck_k = t->ck_k;
+  v.ck_val = t->ck_val;
+  v.ck_b = t->ck_b;
+  v.row_begin = t->row_begin + lo;
+  v.col_begin = t->col_begin;
+  void* rl = r ? (char*)r + (t->dtype == EGFEM_F64 ? 8 : 4) * lo : nullptr;
+  if (cells) return launch_cells(&v, do_r, jac, u, w, chain, rl, csr_vals, s);
+  return launch_rows(&v, do_r, jac, kind, p, u, w, chain, rl, csr_vals, s);
 }
 
 egfem_status launch_batched(const egfem_tensor* t, int32_t batch, egfem_layout layout, const void* U, const void* W,

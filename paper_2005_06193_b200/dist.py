@@ -77,14 +77,37 @@ def gather_windows(win: Window, group=None) -> List[Window]:
     return [Window(*[int(x) for x in t.cpu().tolist()]) for t in allw]
 
 
-def halo_exchange(plan: HaloPlan, u_local, group=None) -> None:
-    """Fill u_local's halo entries from their owners (grouped P2P send/recv)."""
+def halo_start(plan: HaloPlan, u_local, group=None) -> list:
+    """Post the halo exchange of u_local (grouped P2P send/recv of contiguous slices) and
+    return its requests.  Under NCCL the transfers run on the communicator's stream, which
+    first waits for the work already queued on the caller's stream (u is ready); kernels the
+    caller queues next run concurrently with them."""
     import torch.distributed as dist
     ops = []
     for peer, off, n in plan.recvs:
         ops.append(dist.P2POp(dist.irecv, u_local[off:off + n], peer, group))
     for peer, off, n in plan.sends:
-        ops.append(dist.P2POp(dist.isend, u_local[off:off + n].contiguous(), peer, group))
-    if ops:
-        for req in dist.batch_isend_irecv(ops):
-            req.wait()
+        ops.append(dist.P2POp(dist.isend, u_local[off:off + n], peer, group))
+    return dist.batch_isend_irecv(ops) if ops else []
+
+
+def halo_finish(reqs: list) -> None:
+    """Wait for posted halo requests (NCCL: the caller's stream waits on the communicator's;
+    gloo: the host blocks until the data is in place)."""
+    for req in reqs:
+        req.wait()
+
+
+def halo_exchange(plan: HaloPlan, u_local, group=None) -> None:
+    """Fill u_local's halo entries from their owners (grouped P2P send/recv)."""
+    halo_finish(halo_start(plan, u_local, group))
+
+
+def overlapped_step(plan: HaloPlan, u_local, interior, boundary, group=None) -> None:
+    """One distributed step with the u-halo exchange hidden behind the interior work (§8(e)):
+    post the exchange, run interior() — which must read owned entries of u_local only
+    (egfem_interior's rows and interp items) — wait for the halo, run boundary()."""
+    reqs = halo_start(plan, u_local, group)
+    interior()
+    halo_finish(reqs)
+    boundary()

@@ -80,3 +80,77 @@ def test_halo_exchange_gloo(world, reach):
     for p in procs:
         p.join(timeout=60)
     assert all(res.values()), res
+
+
+def _overlap_worker(rank, world, port, n, reach, q):
+    import torch
+    import torch.distributed as dist
+
+    import paper_2005_06193_b200 as eg
+    from paper_2005_06193_b200.dist import Window, gather_windows, make_plan, overlapped_step
+    os.environ.update(MASTER_ADDR="127.0.0.1", MASTER_PORT=str(port))
+    dist.init_process_group("gloo", rank=rank, world_size=world)
+    try:
+        u = torch.sin(torch.arange(n, dtype=torch.float64)) + 2.0
+        b = np.linspace(0, n, world + 1).astype(int)
+        me = Window(int(b[rank]), int(b[rank + 1]), max(0, int(b[rank]) - reach), min(n, int(b[rank + 1]) + reach))
+        plan = make_plan(gather_windows(me), rank)
+        ul = torch.full((plan.n_local,), float("nan"), dtype=torch.float64)
+        o, nr = plan.owned_offset, me.row_end - me.row_begin
+        ul[o:o + nr] = u[me.row_begin:me.row_end]
+        # a banded operator on the owned rows, columns in the local window
+        rp, col, val = [0], [], []
+        for i in range(me.row_begin, me.row_end):
+            for j in range(max(0, i - reach), min(n, i + reach + 1)):
+                col.append(j - me.col_begin)
+                val.append(1.0 / (1 + abs(i - j)) + 1e-3 * i)
+            rp.append(len(col))
+        rp, col, val = np.array(rp), np.array(col, np.int32), torch.tensor(val, dtype=torch.float64)
+        lo, hi = eg.egfem_interior_rows(rp, col, o, o + nr)
+        r = torch.full((nr,), float("nan"), dtype=torch.float64)
+        seen_nan = []
+
+        def rows(a, z):
+            for i in range(a, z):
+                cs = torch.from_numpy(col[rp[i]:rp[i + 1]].astype(np.int64))
+                r[i] = (val[rp[i]:rp[i + 1]] * ul[cs]).sum()
+
+        def interior():
+            rows(lo, hi)
+            seen_nan.append(bool(torch.isnan(r[lo:hi]).any()))
+
+        def boundary():
+            rows(0, lo)
+            rows(hi, nr)
+
+        overlapped_step(plan, ul, interior, boundary)
+        ug = u[me.col_begin:me.col_end]
+        ref = torch.stack([(val[rp[i]:rp[i + 1]] * ug[torch.from_numpy(col[rp[i]:rp[i + 1]].astype(np.int64))]).sum()
+                           for i in range(nr)])
+        q.put((rank, (bool(torch.equal(r, ref)), not seen_nan[0], hi - lo)))
+    finally:
+        dist.destroy_process_group()
+
+
+@pytest.mark.parametrize("world,reach", [(2, 17), (3, 40), (3, 400)])
+def test_overlapped_step_gloo(world, reach):
+    """dist.overlapped_step with egfem_interior_rows' split: the interior rows, computed while the
+    halo is in flight, read no halo entry (none is NaN-poisoned into them), and the step's result
+    equals the serial one on every rank; with a reach wider than a rank (400) the interior is
+    empty and the step degenerates to exchange-then-compute."""
+    import multiprocessing as mp
+
+    import __graft_entry__
+    __graft_entry__.build()
+    ctx = mp.get_context("spawn")
+    q = ctx.Queue()
+    port = _free_port()
+    procs = [ctx.Process(target=_overlap_worker, args=(r, world, port, 600, reach, q)) for r in range(world)]
+    for p in procs:
+        p.start()
+    res = dict(q.get(timeout=120) for _ in range(world))
+    for p in procs:
+        p.join(timeout=60)
+    for rank, (equal, clean, n_inner) in res.items():
+        assert equal and clean, (rank, res)
+        assert (n_inner > 0) == (reach < 100), (rank, n_inner)

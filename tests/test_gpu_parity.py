@@ -377,6 +377,66 @@ def test_partition_emulation_bitwise(eg, name, nranks):
     assert np.array_equal(np.concatenate(J_all), ref["J"])
 
 
+@pytest.mark.parametrize("name,nranks", [("cfg4", 2), ("cfg4", 3), ("cfg3", 4), ("cfg2", 3), ("cfg1", 5),
+                                          ("biochem_p0", 2)])
+def test_overlap_split_reads_no_halo(eg, name, nranks):
+    """8(e) overlap: with every halo entry of u poisoned (NaN), the interior phase — interp over
+    egfem_interior's items, apply+Jacobian over its rows — already yields those rows' r and CSR
+    values bitwise equal to the single-GPU pass (so it can run while the halo is in flight);
+    after the halo arrives, the boundary phase completes r, J bitwise."""
+    import torch
+    pr = I.make_problem(name, n=I.SMALL_N[name])
+    t = eg.egfem_tensor_build(pr.mesh, pr.V, pr.W, pr.form, device=0)
+    ref = gpu_pass(eg, t, pr, pr.u)
+    grp = np.asarray(t.export(values=False)["csr_row_ptr"])
+    cell_wise = pr.W.family in (I.P0, I.QUAD)
+    n_inner = 0
+    for rank in range(nranks):
+        loc, win = eg.egfem_partition(t, nranks, rank)
+        ra, rb, wa, wb = eg.egfem_interior(loc)
+        n_items = loc.n_f  # P0: local cells = local W DOFs; W = V: W DOFs
+        assert 0 <= ra <= rb <= loc.n_u and 0 <= wa <= wb
+        n_inner += rb - ra
+        cb, ce, r0, r1 = win["col_begin"], win["col_end"], win["row_begin"], win["row_end"]
+        u_true = torch.tensor(pr.u[cb:ce], device="cuda")
+        ul = torch.full_like(u_true, float("nan"))
+        ul[r0 - cb:r1 - cb] = u_true[r0 - cb:r1 - cb]
+        nan = float("nan")
+        wl = torch.full((loc.n_f,), nan, dtype=torch.float64, device="cuda")
+        chain = None
+        if pr.W.family in (I.P0, I.QUAD) and pr.interp != I.INTERP_IDENTITY:
+            chain = torch.full((loc.n_f * (pr.mesh.dim + 1),), nan, dtype=torch.float64, device="cuda")
+        r = torch.full((loc.n_u,), nan, dtype=torch.float64, device="cuda")
+        J = torch.full((loc.nnz_csr,), nan, dtype=torch.float64, device="cuda")
+        lrp = np.asarray(loc.export(values=False)["csr_row_ptr"])
+        f0 = grp[r0]
+        # interior phase on the poisoned window
+        eg.egfem_interp_range(loc, pr.interp, pr.p, ul, wl, chain, wa, wb)
+        eg.egfem_apply_jacobian_rows(loc, 1, pr.interp, pr.p, ul, wl, chain, r, J, ra, rb)
+        torch.cuda.synchronize()
+        rr, JJ = r.cpu().numpy(), J.cpu().numpy()
+        assert np.array_equal(rr[ra:rb], ref["r"][r0 + ra:r0 + rb])
+        assert np.array_equal(JJ[lrp[ra]:lrp[rb]], ref["J"][f0 + lrp[ra]:f0 + lrp[rb]])
+        assert np.all(np.isnan(rr[:ra])) and np.all(np.isnan(rr[rb:]))  # nothing else written
+        # the halo arrives; boundary phase
+        ul.copy_(u_true)
+        eg.egfem_interp_range(loc, pr.interp, pr.p, ul, wl, chain, 0, wa)
+        eg.egfem_interp_range(loc, pr.interp, pr.p, ul, wl, chain, wb, n_items)
+        eg.egfem_apply_jacobian_rows(loc, 1, pr.interp, pr.p, ul, wl, chain, r, J, 0, ra)
+        eg.egfem_apply_jacobian_rows(loc, 1, pr.interp, pr.p, ul, wl, chain, r, J, rb, loc.n_u)
+        torch.cuda.synchronize()
+        assert np.array_equal(r.cpu().numpy(), ref["r"][r0:r1])
+        assert np.array_equal(J.cpu().numpy(), ref["J"][f0:grp[r1]])
+        with pytest.raises(eg.EgfemError):
+            eg.egfem_apply_jacobian_rows(loc, 1, pr.interp, pr.p, ul, wl, chain, r, J, 0, loc.n_u + 1)
+        with pytest.raises(eg.EgfemError):
+            eg.egfem_interp_range(loc, pr.interp, pr.p, ul, wl, chain, 1, 0)
+    assert n_inner > 0
+    # a global tensor has no halo: its interior is everything
+    n_items = t.n_cells if cell_wise else t.n_f
+    assert eg.egfem_interior(t) == (0, t.n_u, 0, n_items)
+
+
 @pytest.mark.parametrize("env", [{"EGFEM_PATH": "tile"}, {"EGFEM_PATH": "rows", "EGFEM_BATCHED": "csf"}])
 def test_kernel_paths(eg, env):
     """The non-default kernels (TMA tile kernel, canonical-CSF row kernel for P0 W, CSF batched

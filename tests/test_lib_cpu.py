@@ -60,6 +60,9 @@ def test_null_handle_is_rejected_without_gpu(eg):
     assert L.egfem_jacobian(None, 0, 0, 0.0, None, None, None, None, None) == 1
     assert "NULL" in L.egfem_last_error().decode()
     assert L.egfem_tensor_destroy(None) == 0
+    assert L.egfem_interp_range(None, 0, 0.0, None, None, None, 0, 0, None) == 1
+    assert L.egfem_apply_jacobian_rows(None, 0, 0, 0.0, None, None, None, None, None, 0, 0, None) == 1
+    assert L.egfem_interior(None, None, None, None, None) == 1
 
 
 def _py_partition(prefix, nranks):
@@ -88,3 +91,42 @@ def test_partition_rows_matches_python(eg, nranks):
 def test_partition_rows_edge_cases(eg):
     assert np.array_equal(eg.egfem_partition_rows(np.array([0]), 4), [0, 0, 0, 0, 0])
     assert np.array_equal(eg.egfem_partition_rows(np.array([0, 5]), 3), [0, 1, 1, 1])
+
+
+def _brute_interior(rp, col, lo, hi):
+    """Longest run of consecutive rows whose columns all lie in [lo, hi) (first on ties)."""
+    n = len(rp) - 1
+    ok = [bool(np.all((col[rp[i]:rp[i + 1]] >= lo) & (col[rp[i]:rp[i + 1]] < hi))) for i in range(n)]
+    best = (0, 0)
+    for a in range(n):
+        for b in range(a + 1, n + 1):
+            if all(ok[a:b]) and b - a > best[1] - best[0]:
+                best = (a, b)
+    return best
+
+
+@pytest.mark.parametrize("seed", range(12))
+def test_interior_rows_matches_brute_force(eg, seed):
+    """egfem_interior_rows (the halo-free row run behind the overlapped exchange) against brute force."""
+    rng = np.random.default_rng(seed)
+    n = int(rng.integers(0, 40))
+    counts = rng.integers(0, 5, n)
+    rp = np.concatenate([[0], np.cumsum(counts)]).astype(np.int64)
+    col = rng.integers(0, 30, int(rp[-1])).astype(np.int32)
+    lo, hi = sorted(rng.integers(0, 31, 2))
+    assert eg.egfem_interior_rows(rp, col, lo, hi) == _brute_interior(rp, col, lo, hi)
+
+
+def test_interior_rows_band_structure(eg):
+    """A banded pattern (the structured lexicographic numbering of a rank's window): the halo-free
+    rows are the owned rows at least one bandwidth away from either end."""
+    n_local, own_lo, own_hi, bw = 100, 10, 90, 10
+    rows = range(own_lo, own_hi)
+    rp, col = [0], []
+    for i in rows:
+        c = [j for j in range(i - bw, i + bw + 1) if 0 <= j < n_local]
+        col += c
+        rp.append(len(col))
+    lo, hi = eg.egfem_interior_rows(np.array(rp), np.array(col), own_lo, own_hi)
+    assert (lo, hi) == (bw, own_hi - own_lo - bw)
+    assert eg.egfem_interior_rows(np.array([0]), np.array([], np.int32), 0, 1) == (0, 0)
