@@ -124,7 +124,7 @@ __device__ __forceinline__ float xfma(float a, float b, float c) { return __fmaf
 // scratch.  With warp-level bulk staging the 32/G groups of a warp pool their stage regions
 // into one warp stage per buffer (the warp's rows are consecutive, so their slices are one
 // contiguous span per array) and the warp's two mbarriers sit in group 0's tail.
-template <typename S, int D1, int G, int CPL, bool JT>
+template <typename S, int D1, int G, int CPL, bool JT, int SUN = 0>
 struct CellSmem {
   static constexpr int CC = G * CPL;  // cells per row (max)
   static constexpr int CE = CC * D1;  // nonzeros per row (max)
@@ -141,10 +141,12 @@ struct CellSmem {
   static constexpr int w_v = (w_k + WPG * CC * 4 + 32 + 15) & ~15;
   static constexpr int w_b = (w_v + WPG * CE * (int)sizeof(S) + 32 + 15) & ~15;
   static constexpr int wstage = (w_b + WPG * CE * 2 + 32 + 15) & ~15;
-  static constexpr int raw = (o_t + (JT ? CE * (int)sizeof(S) : 0) + 15) & ~15;  // s_t only with a Jacobian
+  static constexpr int o_u = (o_t + (JT ? CE * (int)sizeof(S) : 0) + 15) & ~15;  // s_t only with a Jacobian
+  static constexpr int raw = (o_u + SUN * (int)sizeof(S) + 15) & ~15;              // s_u: u at the row's fibers
   // per-warp layout for bulk staging: [2 warp stages][WPG x s_t][2 mbarriers]
   static constexpr int wo_t = 2 * wstage;
-  static constexpr int wo_bar = (wo_t + (JT ? WPG * CE * (int)sizeof(S) : 0) + 15) & ~15;
+  static constexpr int wo_u = (wo_t + (JT ? WPG * CE * (int)sizeof(S) : 0) + 15) & ~15;
+  static constexpr int wo_bar = (wo_u + WPG * SUN * (int)sizeof(S) + 15) & ~15;
   static constexpr int wraw = wo_bar + 16;
   static constexpr int wbytes = wraw + ((16 - wraw % 128) + 128) % 128;
   // group stride = 16 (mod 128): the groups of a warp start on different bank quads, so
@@ -238,9 +240,19 @@ __device__ __forceinline__ Meta meta(const CellArgs<S>& A, int64_t row) {
   return m;
 }
 
+// u at a nonzero's column: from a per-group shared copy of the row's fiber u (one shared load)
+// or by shuffles from the fiber lanes (FREG shuffles + selects, 2 instructions each for fp64).
+// Measured on cfg3/cfg4: the shared copy wins for FREG >= 4, for fp32 and for the apply-only
+// kernel; fp64 Newton with FREG = 2 is faster with shuffles (bank conflicts between groups).
+template <typename S, int FREG, int JAC>
+__host__ __device__ constexpr bool cells_su() {
+  return FREG >= 4 || sizeof(S) == 4 || JAC == kJacNone;
+}
+
 template <typename S, int D1, int G, int CPL, int FREG, bool DO_R, int JAC, bool WB>
 __global__ void __launch_bounds__(256, (JAC == kJacNone || G >= 16) ? 3 : 2) k_cell(const CellArgs<S> A) {
-  using L = CellSmem<S, D1, G, CPL, JAC != kJacNone>;
+  constexpr bool SU = cells_su<S, FREG, JAC>() && (DO_R || JAC == kJacNewtonP0);
+  using L = CellSmem<S, D1, G, CPL, JAC != kJacNone, SU ? G * FREG : 0>;
   constexpr int GPB = 256 / G;
   constexpr bool kJ = JAC != kJacNone;
   constexpr bool kN = JAC == kJacNewtonP0;
@@ -256,6 +268,7 @@ __global__ void __launch_bounds__(256, (JAC == kJacNone || G >= 16) ? 3 : 2) k_c
   const uint32_t gs_s = smem_u32(gs);
   S* s_t = reinterpret_cast<S*>(WB ? gs + L::wo_t + (grp % L::WPG) * L::CE * (int)sizeof(S) : gs + L::o_t);
   uint64_t* bars = reinterpret_cast<uint64_t*>(gs + L::wo_bar);
+  S* s_u = reinterpret_cast<S*>(WB ? gs + L::wo_u + (grp % L::WPG) * G * FREG * (int)sizeof(S) : gs + L::o_u);
   constexpr int STG = WB ? L::wstage : L::stage;
   constexpr int SK = WB ? L::w_k : L::st_k, SV = WB ? L::w_v : L::st_v, SB = WB ? L::w_b : L::st_b;
   const uint64_t pol = evict_first_policy();
@@ -377,6 +390,11 @@ __global__ void __launch_bounds__(256, (JAC == kJacNone || G >= 16) ? 3 : 2) k_c
       }
     }
     const bool vec_v = (reinterpret_cast<uintptr_t>(bv) & 15u) == 0;
+    if constexpr (SU && kU) {  // u at the row's fibers, for one shared load per nonzero
+#pragma unroll
+      for (int q = 0; q < FREG; ++q) s_u[lane + q * G] = uj_cur[q];
+      __syncwarp();
+    }
     // the diagonal fiber (i, i): one nonzero per cell of the row — summed in registers
     int fd = -1;
     if constexpr (kJ) {
@@ -421,11 +439,16 @@ __global__ void __launch_bounds__(256, (JAC == kJacNone || G >= 16) ? 3 : 2) k_c
 #pragma unroll
         for (int m = 0; m < D1; ++m) {
           const int fid = (int)(bq[m] & 0xffu);
-          S um = __shfl_sync(FM, uj_cur[0], fid % G, G);
+          S um;
+          if constexpr (SU) {
+            um = s_u[fid];
+          } else {
+            um = __shfl_sync(FM, uj_cur[0], fid % G, G);
 #pragma unroll
-          for (int x = 1; x < FREG; ++x) {
-            const S y = __shfl_sync(FM, uj_cur[x], fid % G, G);
-            um = (fid / G == x) ? y : um;
+            for (int x = 1; x < FREG; ++x) {
+              const S y = __shfl_sync(FM, uj_cur[x], fid % G, G);
+              um = (fid / G == x) ? y : um;
+            }
           }
           B = (m == 0) ? xmul(tv[m], um) : xfma(tv[m], um, B);
         }
@@ -541,7 +564,8 @@ bool cells_warp_bulk(int G) {
 
 template <typename S, int D1, int G, int CPL, int FREG, bool DO_R, int JAC>
 egfem_status run_cells(const egfem_tensor* t, const CellArgs<S>& A, cudaStream_t s) {
-  using L = CellSmem<S, D1, G, CPL, JAC != kJacNone>;
+  constexpr bool SU = cells_su<S, FREG, JAC>() && (DO_R || JAC == kJacNewtonP0);
+  using L = CellSmem<S, D1, G, CPL, JAC != kJacNone, SU ? G * FREG : 0>;
   const bool wb = cells_warp_bulk(G);
   auto fn = wb ? k_cell<S, D1, G, CPL, FREG, DO_R, JAC, true> : k_cell<S, D1, G, CPL, FREG, DO_R, JAC, false>;
   const int smem = wb ? L::wbytes * 8 : L::bytes * (256 / G);
