@@ -200,6 +200,31 @@ __device__ __forceinline__ void load_cell_ldg(const S* p, S* out) {
     }
   }
 }
+// the D1 values of one cell from global memory, streaming (evict-first) loads; 16-byte vectors
+// when D1·sizeof(S) is a multiple of 16 (cells start at multiples of D1 values)
+template <typename S, int D1>
+__device__ __forceinline__ void load_cell_cs(const S* p, S* out) {
+  if constexpr ((D1 * sizeof(S)) % 16 == 0) {
+    constexpr int NV = D1 * (int)sizeof(S) / 16;
+#pragma unroll
+    for (int v = 0; v < NV; ++v) {
+      if constexpr (sizeof(S) == 8) {
+        const double2 x = __ldcs(reinterpret_cast<const double2*>(p) + v);
+        out[2 * v] = x.x;
+        out[2 * v + 1] = x.y;
+      } else {
+        const float4 x = __ldcs(reinterpret_cast<const float4*>(p) + v);
+        out[4 * v] = x.x;
+        out[4 * v + 1] = x.y;
+        out[4 * v + 2] = x.z;
+        out[4 * v + 3] = x.w;
+      }
+    }
+  } else {
+#pragma unroll
+    for (int m = 0; m < D1; ++m) out[m] = __ldcs(p + m);
+  }
+}
 // NC consecutive values at p (16-byte vectors when NC·sizeof(S) is a multiple of 16 and p is aligned)
 template <typename S, int NC>
 __device__ __forceinline__ void load_run(const S* p, S* out) {
@@ -320,7 +345,7 @@ __global__ void __launch_bounds__(256, (JAC == kJacNone || G >= 16) ? 3 : 2) k_c
     } else {
       const int n = (int)(m.e1 - m.e0);
       sk = stage_span<uint32_t, G, L::CC>(dst + SK, A.ck_k + m.e0 / D1, n / D1, lane, pol);
-      sv = stage_span<S, G, L::CE>(dst + SV, A.ck_val + m.e0, n, lane, pol);
+      sv = 0;  // values: read straight into registers (below)
       sb = stage_span<uint16_t, G, L::CE>(dst + SB, A.ck_b + m.e0, n, lane, pol);
       commit();
     }
@@ -369,6 +394,17 @@ __global__ void __launch_bounds__(256, (JAC == kJacNone || G >= 16) ? 3 : 2) k_c
     const uint32_t* bk = reinterpret_cast<const uint32_t*>(cs + SK) + shk;
     const S* bv = reinterpret_cast<const S*>(cs + SV) + shv;
     const uint16_t* bb = reinterpret_cast<const uint16_t*>(cs + SB) + shb;
+    // ---- the lane's cell values (cp.async path: streamed straight into registers, issued with
+    // the gathers below so their latencies overlap; a lane past the row's cells reads cell 0)
+    S tvg[WB ? 1 : CPL][D1];
+    if constexpr (!WB) {
+#pragma unroll
+      for (int c = 0; c < CPL; ++c) {
+        const int q = lane + c * G;
+        const S* pv = A.ck_val + (q < nc ? (size_t)cur.e0 + (size_t)q * D1 : (size_t)0);
+        load_cell_cs<S, D1>(pv, tvg[c]);
+      }
+    }
     // ---- gathers of the lane's cells: w_K and (D_u w)_{K, 0..d}, all in flight together
     S wk[CPL];
     S dd[kN ? CPL : 1][D1];
@@ -416,7 +452,12 @@ __global__ void __launch_bounds__(256, (JAC == kJacNone || G >= 16) ? 3 : 2) k_c
       S tv[D1];
       uint32_t bq[D1];
       if (ok) {
-        load_cell<S, D1>(bv + q * D1, vec_v, tv);
+        if constexpr (WB) {
+          load_cell<S, D1>(bv + q * D1, vec_v, tv);
+        } else {
+#pragma unroll
+          for (int m = 0; m < D1; ++m) tv[m] = tvg[c][m];
+        }
         if constexpr (D1 == 4) {
           const uint2 x = *reinterpret_cast<const uint2*>(bb + q * D1);  // 8-byte aligned: e0 % 4 == 0
           bq[0] = x.x & 0xffffu;
