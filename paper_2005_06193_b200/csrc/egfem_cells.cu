@@ -49,6 +49,7 @@ struct CellArgs {
   S* r;
   S* csr;
   int64_t diag_off;        // column of row i's diagonal = i + diag_off (local tensors of a partition)
+  bool chain32;            // chain is 32-byte aligned (one 256-bit load per cell row)
 };
 
 __device__ __forceinline__ uint32_t smem_u32(const void* p) { return (uint32_t)__cvta_generic_to_shared(p); }
@@ -183,7 +184,13 @@ __device__ __forceinline__ void load_cell(const S* p, bool vec, S* out) {
 }
 // the D1 values of one cell from global memory (16-byte read-only vector loads; D1·sizeof(S) % 16 == 0)
 template <typename S, int D1>
-__device__ __forceinline__ void load_cell_ldg(const S* p, S* out) {
+__device__ __forceinline__ void load_cell_ldg(const S* p, S* out, bool a32 = false) {
+  if constexpr (sizeof(S) == 8 && D1 == 4) {
+    if (a32) {  // 32-byte aligned: one 256-bit load
+      asm("ld.global.nc.v4.f64 {%0,%1,%2,%3}, [%4];" : "=d"(out[0]), "=d"(out[1]), "=d"(out[2]), "=d"(out[3]) : "l"(p));
+      return;
+    }
+  }
   constexpr int NV = D1 * (int)sizeof(S) / 16;
 #pragma unroll
   for (int v = 0; v < NV; ++v) {
@@ -203,8 +210,12 @@ __device__ __forceinline__ void load_cell_ldg(const S* p, S* out) {
 // the D1 values of one cell from global memory, streaming (evict-first) loads; 16-byte vectors
 // when D1·sizeof(S) is a multiple of 16 (cells start at multiples of D1 values)
 template <typename S, int D1>
-__device__ __forceinline__ void load_cell_cs(const S* p, S* out) {
-  if constexpr ((D1 * sizeof(S)) % 16 == 0) {
+__device__ __forceinline__ void load_cell_cs(const S* p, S* out, uint64_t pol) {
+  if constexpr (sizeof(S) == 8 && D1 == 4) {  // one 32-byte load (sm_100 256-bit LDG), L1 bypass, L2 evict-first
+    asm("ld.global.nc.L1::no_allocate.L2::cache_hint.v4.f64 {%0,%1,%2,%3}, [%4], %5;"
+        : "=d"(out[0]), "=d"(out[1]), "=d"(out[2]), "=d"(out[3])
+        : "l"(p), "l"(pol));
+  } else if constexpr ((D1 * sizeof(S)) % 16 == 0) {
     constexpr int NV = D1 * (int)sizeof(S) / 16;
 #pragma unroll
     for (int v = 0; v < NV; ++v) {
@@ -402,7 +413,7 @@ __global__ void __launch_bounds__(256, (JAC == kJacNone || G >= 16) ? 3 : 2) k_c
       for (int c = 0; c < CPL; ++c) {
         const int q = lane + c * G;
         const S* pv = A.ck_val + (q < nc ? (size_t)cur.e0 + (size_t)q * D1 : (size_t)0);
-        load_cell_cs<S, D1>(pv, tvg[c]);
+        load_cell_cs<S, D1>(pv, tvg[c], pol);
       }
     }
     // ---- gathers of the lane's cells: w_K and (D_u w)_{K, 0..d}, all in flight together
@@ -418,7 +429,7 @@ __global__ void __launch_bounds__(256, (JAC == kJacNone || G >= 16) ? 3 : 2) k_c
         // the cell's D1 values (16-byte vector loads); a lane past the row's cells loads cell 0's
         // row and never uses it (no select on the loaded value)
         if constexpr ((D1 * sizeof(S)) % 16 == 0) {
-          load_cell_ldg<S, D1>(A.chain + (size_t)K * D1, dd[c]);
+          load_cell_ldg<S, D1>(A.chain + (size_t)K * D1, dd[c], A.chain32);
         } else {
 #pragma unroll
           for (int m = 0; m < D1; ++m) dd[c][m] = __ldg(A.chain + (size_t)K * D1 + m);
@@ -678,6 +689,7 @@ egfem_status cells_dispatch(const egfem_tensor* t, bool do_r, int jac, const voi
   A.r = static_cast<S*>(r);
   A.csr = static_cast<S*>(csr);
   A.diag_off = t->row_begin - t->col_begin;
+  A.chain32 = (reinterpret_cast<uintptr_t>(chain) & 31u) == 0;
   CellCfg c{};
   if (!pick_cells(t, &c)) {
     set_error("no cell-major configuration");
