@@ -110,11 +110,11 @@ __device__ __forceinline__ void cp16_dense(void* dst, const void* src) {
 
 // One launch per stencil width N (rows grouped by N offline, `dense_rows`, and their blocks
 // stored contiguously in that order), so every instance holds exactly 2N W values per lane and
-// the narrow stencils run at high occupancy.  CTA c walks a contiguous range of its class's
-// rows (listed in row order: neighbours share most of their stencil, U/W lines are reused from
-// L1) RB rows at a time: the next RB blocks (one contiguous span) and stencil columns are
-// copied into shared memory by cp.async while this batch is used; its warps take the 64-pair
-// chunks of each row.
+// the narrow stencils run at high occupancy.  The class's rows (listed in row order: neighbours
+// share most of their stencil) are cut into batches of RB, dealt round-robin to the CTAs; a
+// CTA's next batch (one contiguous span of blocks) and its stencil columns are copied into
+// shared memory by cp.async while this batch is used; its warps take the 64-pair chunks of
+// each row.
 template <int N, typename S>
 struct DenseTile {
   static constexpr int NP = N + (N & 1);
@@ -129,7 +129,7 @@ struct DensePPT {  // pairs per lane (4 for N <= 12 measured slower on cfg5: 1.7
 
 template <typename S, int N, bool NM>
 __global__ void __launch_bounds__(128) k_dense(const DenseArgs<S> A, const int32_t* __restrict__ rows, int64_t nrows,
-                                              int64_t blk0) {
+                                              int64_t blk0, int rb) {
   using TL = DenseTile<N, S>;
   constexpr int PPT = DensePPT<N>::value;
   constexpr int NP = TL::NP, RB = TL::RB;
@@ -138,19 +138,22 @@ __global__ void __launch_bounds__(128) k_dense(const DenseArgs<S> A, const int32
   const int warp = threadIdx.x >> 5, lane = threadIdx.x & 31;
   const int nwarps = blockDim.x >> 5;
   const int nchunks = (A.B + 32 * PPT - 1) / (32 * PPT);
-  const int64_t per = (nrows + gridDim.x - 1) / gridDim.x;
-  const int64_t q0 = (int64_t)blockIdx.x * per;
-  const int64_t q1 = min(nrows, q0 + per);
+  // batches of RB consecutive class entries, dealt round-robin to the CTAs: the rows in flight
+  // form one moving window, so the U / W rows their stencils touch stay L2-resident
+  const int64_t q1 = nrows;
+  // rb <= RB rows per batch: small classes use short batches so that every SM gets work
+  const int64_t step = (int64_t)gridDim.x * rb;
+  const int64_t q0 = (int64_t)blockIdx.x * rb;
   if (q0 >= q1) return;
   if constexpr (N == 0) {  // empty rows
-    for (int64_t q = q0; q < q1; ++q)
+    for (int64_t q = (int64_t)blockIdx.x; q < q1; q += gridDim.x)
       for (int p = threadIdx.x; p < A.B; p += blockDim.x) A.R[at<NM>(rows[q], p, A.B, A.n_u)] = S(0);
     return;
   } else {
     // stage entries [q, min(q + RB, q1)) of the class list into buffer b; returns the shift
     auto stage = [&](int64_t q, int b) -> int {
       if (q >= q1) return 0;
-      const int nr = (int)(q1 - q < (int64_t)RB ? q1 - q : (int64_t)RB);
+      const int nr = (int)(q1 - q < (int64_t)rb ? q1 - q : (int64_t)rb);
       for (int x = threadIdx.x; x < nr * N; x += blockDim.x) {
         const int64_t row = __ldg(rows + q + x / N);
         s_cols[b][x] = __ldg(A.fib_j + __ldg(A.row_fib + row) + x % N);
@@ -165,12 +168,12 @@ __global__ void __launch_bounds__(128) k_dense(const DenseArgs<S> A, const int32
     int sh_cur = stage(q0, 0);
     asm volatile("cp.async.commit_group;" ::: "memory");
     int st = 0;
-    for (int64_t q = q0; q < q1; q += RB) {
-      const int sh_nxt = stage(q + RB, st ^ 1);
+    for (int64_t q = q0; q < q1; q += step) {
+      const int sh_nxt = stage(q + step, st ^ 1);
       asm volatile("cp.async.commit_group;" ::: "memory");
       asm volatile("cp.async.wait_group 1;" ::: "memory");
       __syncthreads();  // this batch's blocks and columns are in buffer st for every warp
-      const int nr = (int)(q1 - q < (int64_t)RB ? q1 - q : (int64_t)RB);
+      const int nr = (int)(q1 - q < (int64_t)rb ? q1 - q : (int64_t)rb);
       const S* M = reinterpret_cast<const S*>(s_blk[st]) + sh_cur;
       for (int ch = warp; ch < nchunks; ch += nwarps) {
         const int p0 = ch * 32 * PPT + lane;
@@ -256,8 +259,10 @@ egfem_status launch_dense(const egfem_tensor* t, int32_t batch, egfem_layout lay
     const int threads = 32 * std::min(4, (batch + 32 * DensePPT<N_>::value - 1) / (32 * DensePPT<N_>::value)); \
     int per_sm = 0;                                                                                           \
     EGFEM_CUDA_TRY(cudaOccupancyMaxActiveBlocksPerMultiprocessor(&per_sm, fn, threads, 0));                   \
-    const int grid = (int)std::min<int64_t>(count, (int64_t)std::max(per_sm, 1) * g_sms_dense[dev]);         \
-    fn<<<grid, threads, 0, s>>>(A, rows, count, cls[3]);                                                      \
+    const int64_t slots = (int64_t)std::max(per_sm, 1) * g_sms_dense[dev];                                   \
+    const int rb = (int)std::max<int64_t>(1, std::min<int64_t>(DenseTile<N_, S_>::RB, (count + slots - 1) / slots)); \
+    const int grid = (int)std::max<int64_t>(1, std::min<int64_t>((count + rb - 1) / rb, slots));               \
+    fn<<<grid, threads, 0, s>>>(A, rows, count, cls[3], rb);                                                  \
     break;                                                                                                    \
   }
 #define EGFEM_DALL(S_)                                                                                         \
