@@ -22,6 +22,8 @@ namespace egfem {
 namespace {
 
 constexpr int kDenseMaxN = 20;  // longest stencil with a dense-block instance
+constexpr int kDense1MaxN = 16;  // longest stencil of the single-vector dense kernel (one lane per point)
+int g_sms_dense1[64] = {0};
 
 template <typename S>
 struct DenseArgs {
@@ -204,6 +206,182 @@ __global__ void __launch_bounds__(128) k_dense(const DenseArgs<S> A, const int32
   }
 }
 
+// ------------------------------------------------------------------ single-vector W = V path
+// Steps (2)+(3) for W = V tensors from the same dense blocks:
+//   X_a = Σ_b M_i[a][b] w_{N_b}            Picard value of CSR slot (i, N_a)   (T·w)
+//   r_i = Σ_a u_{N_a} X_a                   residual                            (T:(u⊗w))
+//   Y_c = Σ_a u_{N_a} M_i[a][c]             (T·₂u)_{i N_c}
+//   J_{i N_c} = X_c + f'(u_{N_c}) Y_c      Newton (f' = 1, 2u, −1/(k+u)²)
+// A group of G lanes per row (rows in row order, grid-stride; a row range [lo, hi) is a
+// sub-range of it): lane a owns stencil point N_a — it reads block row a (the group's reads
+// cover the block contiguously), takes w_{N_b} from the other lanes by shuffles, and Y by a
+// reduce-scatter of u_a M[a][·] over the group; r by a butterfly.  Fixed summation orders
+// (sequential in b, fixed trees over lanes): bitwise reproducible, fused == separate.
+template <typename S>
+struct Dense1Args {
+  const int64_t* row_fib;
+  const int32_t* fib_j;
+  const int64_t* blk_off;
+  const S* blk;
+  const S* u;
+  const S* w;
+  S* r;
+  S* csr;
+  int dmode;
+  double pk;
+  int64_t lo, hi;
+};
+
+__device__ __forceinline__ double dmul1(double a, double b) { return __dmul_rn(a, b); }
+__device__ __forceinline__ float dmul1(float a, float b) { return __fmul_rn(a, b); }
+
+template <typename S, int G, bool DO_R, int JAC>
+__global__ void __launch_bounds__(256) k_dense1(const Dense1Args<S> A) {
+  constexpr bool kN = JAC == 2;  // W = V Newton
+  constexpr bool kU = DO_R || kN;
+  constexpr unsigned FM = 0xffffffffu;
+  constexpr int RPW = 32 / G;  // rows per warp
+  const int lane = threadIdx.x % G;
+  const int64_t stride = (int64_t)gridDim.x * (blockDim.x / G);
+  // warp-uniform loop: a group past the end runs on an empty row.  Software-pipelined: the next
+  // row's (f0, n, block offset) are loaded during the current row and its stencil column one
+  // step behind them, so the u / w gathers and block reads of a row are the only loads it waits on.
+  struct Meta1 {
+    int64_t f0;
+    int n;
+    int64_t off;
+  };
+  auto meta = [&](int64_t row) {
+    Meta1 x{0, 0, 0};
+    if (row < A.hi) {
+      x.f0 = __ldg(A.row_fib + row);
+      x.n = (int)(__ldg(A.row_fib + row + 1) - x.f0);
+      x.off = __ldg(A.blk_off + row);
+    }
+    return x;
+  };
+  const int64_t wr0 = A.lo + ((int64_t)blockIdx.x * blockDim.x + (threadIdx.x & ~31)) / G;
+  const int64_t gofs = (threadIdx.x & 31) / G;
+  Meta1 cur = meta(wr0 + gofs);
+  Meta1 nxt = meta(wr0 + gofs + stride);
+  int jc = lane < cur.n ? __ldg(A.fib_j + cur.f0 + lane) : 0;
+  for (int64_t wr = wr0; wr < A.hi; wr += stride) {
+    const int64_t row = wr + gofs;
+    const bool live = row < A.hi;
+    const Meta1 nn = meta(row + 2 * stride);
+    const int jn = lane < nxt.n ? __ldg(A.fib_j + nxt.f0 + lane) : 0;
+    const int n = cur.n;
+    const int64_t f0 = cur.f0;
+    const int np = n + (n & 1);
+    const S* M = A.blk + cur.off;
+    const bool has = lane < n;
+    const S wl = __ldg(A.w + jc);  // j = 0 for lanes past the stencil: a valid, unused value
+    const S ul = kU ? __ldg(A.u + jc) : S(0);
+    // block row `lane` (16-byte loads) and column `lane`
+    S m[G + 1], c[G];
+#pragma unroll
+    for (int b = 0; b < G; b += 2) {
+      if (has && b < n) {
+        const typename Vec2<S>::T v = __ldg(reinterpret_cast<const typename Vec2<S>::T*>(M + lane * np + b));
+        m[b] = v.x;
+        m[b + 1] = v.y;
+      } else {
+        m[b] = S(0);
+        m[b + 1] = S(0);
+      }
+    }
+    S X = S(0), Y = S(0);
+#pragma unroll
+    for (int b = 0; b < G; ++b) {
+      const S wb = __shfl_sync(FM, wl, b, G);
+      if (b < n) X = fma(m[b], wb, X);
+    }
+    if constexpr (kN) {
+      // Y_l = Σ_a u_a M[a][l]: lane a forms u_a M[a][·] from its own row, then a fixed-tree
+      // reduce-scatter over the group leaves component l in lane l
+#pragma unroll
+      for (int l = 0; l < G; ++l) c[l] = has ? dmul1(ul, m[l]) : S(0);
+#pragma unroll
+      for (int o = G / 2; o > 0; o >>= 1) {
+        const bool upper = (lane & o) != 0;
+#pragma unroll
+        for (int t = 0; t < o; ++t) {
+          const S send = upper ? c[t] : c[t + o];
+          const S keep = upper ? c[t + o] : c[t];
+          c[t] = keep + __shfl_xor_sync(FM, send, o, G);
+        }
+      }
+      Y = c[0];
+    }
+    if constexpr (DO_R) {
+      S acc = has ? dmul1(ul, X) : S(0);
+#pragma unroll
+      for (int o = G / 2; o > 0; o >>= 1) acc = acc + __shfl_xor_sync(FM, acc, o, G);
+      if (live && lane == 0) A.r[row] = acc;
+    }
+    if constexpr (JAC != 0) {
+      if (has) {
+        S v = X;
+        if constexpr (kN) {
+          S cm = S(1);
+          if (A.dmode == 1) cm = dmul1(S(2), ul);
+          if (A.dmode == 2) {
+            const S iv = S(1) / (S(A.pk) + ul);
+            cm = -dmul1(iv, iv);
+          }
+          v = A.dmode ? fma(cm, Y, v) : v + Y;
+        }
+        A.csr[f0 + lane] = v;
+      }
+    }
+    cur = nxt;
+    nxt = nn;
+    jc = jn;
+  }
+  (void)RPW;
+}
+
+template <typename S, int NMAX, bool DO_R, int JAC>
+egfem_status run_dense1(const egfem_tensor* t, const Dense1Args<S>& A, cudaStream_t s) {
+  auto fn = k_dense1<S, NMAX, DO_R, JAC>;
+  const int dev = t->device & 63;
+  int per_sm = 0;
+  EGFEM_CUDA_TRY(cudaOccupancyMaxActiveBlocksPerMultiprocessor(&per_sm, fn, 256, 0));
+  const int64_t need = (A.hi - A.lo + (256 / NMAX) - 1) / (256 / NMAX);
+  const int grid = (int)std::max<int64_t>(1, std::min<int64_t>(need, (int64_t)std::max(per_sm, 1) * g_sms_dense1[dev]));
+  fn<<<grid, 256, 0, s>>>(A);
+  count_launch();
+  EGFEM_CUDA_TRY(cudaGetLastError());
+  return EGFEM_OK;
+}
+
+template <typename S, int NMAX>
+egfem_status dense1_mode(const egfem_tensor* t, const Dense1Args<S>& A, bool do_r, int jac, cudaStream_t s) {
+  if (do_r) {
+    if (jac == 0) return run_dense1<S, NMAX, true, 0>(t, A, s);
+    if (jac == 1) return run_dense1<S, NMAX, true, 1>(t, A, s);
+    return run_dense1<S, NMAX, true, 2>(t, A, s);
+  }
+  if (jac == 1) return run_dense1<S, NMAX, false, 1>(t, A, s);
+  return run_dense1<S, NMAX, false, 2>(t, A, s);
+}
+
+template <typename S>
+egfem_status dense1_dispatch(const egfem_tensor* t, int64_t lo, int64_t hi, bool do_r, int jac,
+                             egfem_interp_kind kind, double p, const void* u, const void* w, void* r, void* csr,
+                             cudaStream_t s) {
+  Dense1Args<S> A{t->row_fib, t->fib_j, t->blk_off, static_cast<const S*>(t->blk), static_cast<const S*>(u),
+                  static_cast<const S*>(w), static_cast<S*>(r), static_cast<S*>(csr),
+                  kind == EGFEM_INTERP_SQUARE ? 1 : (kind == EGFEM_INTERP_RECIPROCAL ? 2 : 0), p, lo, hi};
+  const int dev = t->device & 63;
+  if (!g_sms_dense1[dev])
+    EGFEM_CUDA_TRY(cudaDeviceGetAttribute(&g_sms_dense1[dev], cudaDevAttrMultiProcessorCount, t->device));
+  const int mx = t->max_row_fib;  // G lanes per row, one per stencil point
+  if (mx <= 4) return dense1_mode<S, 4>(t, A, do_r, jac, s);
+  if (mx <= 8) return dense1_mode<S, 8>(t, A, do_r, jac, s);
+  return dense1_mode<S, 16>(t, A, do_r, jac, s);
+}
+
 // Offline: the dense block of each row (one thread per row).  err = 1 if a k lies outside
 // its row's stencil (then the tensor keeps only the CSF kernels).
 template <typename S>
@@ -238,6 +416,19 @@ int g_sms_dense[64] = {0};
 }  // namespace
 
 bool dense_path_ok(const egfem_tensor* t) { return t->blk != nullptr; }
+
+// single vector: W = V tensors with dense blocks and stencils of at most 16 (jac: 0 none,
+// 1 Picard, 2 W = V Newton)
+bool dense1_path_ok(const egfem_tensor* t, int jac) {
+  return t->blk != nullptr && t->w_is_v && t->max_row_fib <= kDense1MaxN && jac >= 0 && jac <= 2;
+}
+
+egfem_status launch_dense1(const egfem_tensor* t, int64_t lo, int64_t hi, bool do_r, int jac, egfem_interp_kind kind,
+                           double p, const void* u, const void* w, void* r, void* csr_vals, cudaStream_t s) {
+  if (hi <= lo) return EGFEM_OK;
+  if (t->dtype == EGFEM_F64) return dense1_dispatch<double>(t, lo, hi, do_r, jac, kind, p, u, w, r, csr_vals, s);
+  return dense1_dispatch<float>(t, lo, hi, do_r, jac, kind, p, u, w, r, csr_vals, s);
+}
 
 egfem_status launch_dense(const egfem_tensor* t, int32_t batch, egfem_layout layout, const void* U, const void* W,
                           void* R, cudaStream_t s) {

@@ -134,6 +134,9 @@ egfem_status launch_cells(const egfem_tensor* t, bool do_r, int jac, const void*
                           void* r, void* csr_vals, cudaStream_t s);
 egfem_status make_p0_cells(egfem_tensor* t);
 bool dense_path_ok(const egfem_tensor* t);
+bool dense1_path_ok(const egfem_tensor* t, int jac);
+egfem_status launch_dense1(const egfem_tensor* t, int64_t lo, int64_t hi, bool do_r, int jac, egfem_interp_kind kind,
+                           double p, const void* u, const void* w, void* r, void* csr_vals, cudaStream_t s);
 egfem_status launch_dense(const egfem_tensor* t, int32_t batch, egfem_layout layout, const void* U, const void* W,
                           void* R, cudaStream_t s);
 egfem_status make_dense_blocks(egfem_tensor* t, const std::vector<int64_t>& hrf);

@@ -841,6 +841,8 @@ egfem_status launch_tile(const egfem_tensor* t, bool do_r, int jac, egfem_interp
   const bool rows_only = force && force[0] == 'r';
   if (!tile && !rows_only && cells_path_ok(t, jac))
     return launch_cells(t, do_r, jac, u, w, chain, r, csr_vals, s);
+  if (!tile && !rows_only && dense1_path_ok(t, jac))
+    return launch_dense1(t, 0, t->n_u, do_r, jac, kind, p, u, w, r, csr_vals, s);
   if (!tile && rows_path_ok(t, jac)) return launch_rows(t, do_r, jac, kind, p, u, w, chain, r, csr_vals, s);
   if (t->dtype == EGFEM_F64) return tile_dispatch<double>(t, do_r, jac, kind, p, u, w, chain, r, csr_vals, s);
   return tile_dispatch<float>(t, do_r, jac, kind, p, u, w, chain, r, csr_vals, s);
@@ -859,6 +861,8 @@ egfem_status launch_tile_rows(const egfem_tensor* t, int64_t lo, int64_t hi, boo
   const bool tile = force && force[0] == 't';
   const bool rows_only = force && force[0] == 'r';
   const bool cells = !tile && !rows_only && cells_path_ok(t, jac);
+  if (!cells && !tile && !rows_only && dense1_path_ok(t, jac))  // rows [lo, hi) of the row-order dense kernel
+    return launch_dense1(t, lo, hi, do_r, jac, kind, p, u, w, r, csr_vals, s);
   if (!cells && (tile || !rows_path_ok(t, jac))) {
     set_error("row sub-ranges need a row-group kernel (rows of at most 256 nonzeros)");
     return EGFEM_ERR_UNSUPPORTED;
