@@ -155,14 +155,49 @@ def test_cfg4_full_size_sampled_rows(eg, orc, dtype):
     torch.cuda.empty_cache()
 
 
-@pytest.mark.parametrize("n", [6, 10])
-def test_cfg4_fp32_small(eg, orc, n):
-    pr = I.make_problem("cfg4", n=n)
+@pytest.mark.parametrize("name,n", [("cfg4", 6), ("cfg4", 10), ("cfg3", 9), ("cfg2", 17), ("cfg1", 300),
+                                    ("biochem_p1", 20), ("minsurf2d", 12)])
+def test_fp32_small(eg, orc, name, n):
+    """fp32 handles (the fp64 build rounded once) on every single-vector kernel family: cell-major
+    P0 (cfg3/cfg4), W = V dense blocks (cfg1/cfg2, RECIPROCAL Newton), MINSURF interp."""
+    pr = I.make_problem(name, n=n)
     t, o = _build_both(eg, orc, pr, dtype=1)
     g = gpu_pass(eg, t, pr, pr.u)
     ref = oracle_pass(o, pr, pr.u)
     for key in ("w", "r", "A", "J"):
         assert rel_l2(g[key], ref[key]) <= FP32_TOL, key
+
+
+@pytest.mark.parametrize("form,kind", [(I.FORM_CONV_J, I.INTERP_IDENTITY), (I.FORM_MASS3, I.INTERP_SQUARE),
+                                       (I.FORM_MASS3, I.INTERP_RECIPROCAL), (I.FORM_CONV_I, I.INTERP_IDENTITY)])
+def test_wv_3d_wide_stencils(eg, orc, form, kind):
+    """W = V on a 3D P1 mesh: stencils up to 15 points take the 16-lane dense single-vector
+    kernel; every W = V Newton factor (IDENTITY, SQUARE 2u, RECIPROCAL −1/(k+u)²), fused and
+    separate, and a split row range, against the oracle."""
+    import torch
+    mesh = I.mesh_cube(5)
+    V = I.space_p1(mesh)
+    u = I.random_vector(V.n_dofs, 11, 0.5, 1.5)
+    pr = I.Problem("wv3d", mesh, V, V, form, kind, 1.0, ("f64",), u)
+    t, o = _build_both(eg, orc, pr)
+    ref = oracle_pass(o, pr, u)
+    for fused in (False, True):
+        g = gpu_pass(eg, t, pr, u, fused=fused)
+        for key in ("w", "r", "A", "J"):
+            assert rel_l2(g[key], ref[key]) <= FP64_TOL, (fused, key)
+    # two row ranges reproduce the whole-range call bitwise
+    ud = torch.tensor(u, device="cuda")
+    w = torch.empty(t.n_f, dtype=torch.float64, device="cuda")
+    eg.egfem_interp(t, kind, 1.0, ud, w)
+    r0, J0 = torch.empty(t.n_u, dtype=torch.float64, device="cuda"), torch.empty(t.nnz_csr, dtype=torch.float64,
+                                                                                  device="cuda")
+    eg.egfem_apply_jacobian(t, 1, kind, 1.0, ud, w, None, r0, J0)
+    r1, J1 = torch.full_like(r0, float("nan")), torch.full_like(J0, float("nan"))
+    cut = t.n_u // 3
+    eg.egfem_apply_jacobian_rows(t, 1, kind, 1.0, ud, w, None, r1, J1, cut, t.n_u)
+    eg.egfem_apply_jacobian_rows(t, 1, kind, 1.0, ud, w, None, r1, J1, 0, cut)
+    torch.cuda.synchronize()
+    assert torch.equal(r0, r1) and torch.equal(J0, J1)
 
 
 @pytest.mark.parametrize("layout", [0, 1])
