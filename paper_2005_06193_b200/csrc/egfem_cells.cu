@@ -285,7 +285,9 @@ __host__ __device__ constexpr bool cells_su() {
   return FREG >= 4 || sizeof(S) == 4 || JAC == kJacNone;
 }
 
-template <typename S, int D1, int G, int CPL, int FREG, bool DO_R, int JAC, bool WB>
+// C32: the D_u w rows are 32-byte aligned and read with one 256-bit load each (a compile-time
+// choice: a runtime branch between load widths makes the merged result wait on the load at once)
+template <typename S, int D1, int G, int CPL, int FREG, bool DO_R, int JAC, bool WB, bool C32 = false>
 __global__ void __launch_bounds__(256, (JAC == kJacNone || G >= 16) ? 3 : 2) k_cell(const CellArgs<S> A) {
   constexpr bool SU = cells_su<S, FREG, JAC>() && (DO_R || JAC == kJacNewtonP0);
   using L = CellSmem<S, D1, G, CPL, JAC != kJacNone, SU ? G * FREG : 0>;
@@ -429,7 +431,7 @@ __global__ void __launch_bounds__(256, (JAC == kJacNone || G >= 16) ? 3 : 2) k_c
         // the cell's D1 values (16-byte vector loads); a lane past the row's cells loads cell 0's
         // row and never uses it (no select on the loaded value)
         if constexpr ((D1 * sizeof(S)) % 16 == 0) {
-          load_cell_ldg<S, D1>(A.chain + (size_t)K * D1, dd[c], A.chain32);
+          load_cell_ldg<S, D1>(A.chain + (size_t)K * D1, dd[c], C32);
         } else {
 #pragma unroll
           for (int m = 0; m < D1; ++m) dd[c][m] = __ldg(A.chain + (size_t)K * D1 + m);
@@ -620,6 +622,10 @@ egfem_status run_cells(const egfem_tensor* t, const CellArgs<S>& A, cudaStream_t
   using L = CellSmem<S, D1, G, CPL, JAC != kJacNone, SU ? G * FREG : 0>;
   const bool wb = cells_warp_bulk(G);
   auto fn = wb ? k_cell<S, D1, G, CPL, FREG, DO_R, JAC, true> : k_cell<S, D1, G, CPL, FREG, DO_R, JAC, false>;
+  if constexpr (JAC == kJacNewtonP0 && D1 == 4 && sizeof(S) == 8) {
+    if (A.chain32)
+      fn = wb ? k_cell<S, D1, G, CPL, FREG, DO_R, JAC, true, true> : k_cell<S, D1, G, CPL, FREG, DO_R, JAC, false, true>;
+  }
   const int smem = wb ? L::wbytes * 8 : L::bytes * (256 / G);
   if (smem > 48 * 1024) EGFEM_CUDA_TRY(cudaFuncSetAttribute(fn, cudaFuncAttributeMaxDynamicSharedMemorySize, smem));
   const int dev = t->device & 63;
