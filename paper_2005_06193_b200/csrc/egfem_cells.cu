@@ -131,9 +131,11 @@ struct CellSmem {
   static constexpr int CE = CC * D1;  // nonzeros per row (max)
   // each slice gets 32 B of slack (its 16-byte-aligned span may start up to 15 B early and
   // end up to 15 B late) and starts 16-byte aligned (cp.async destination)
+  // (per-lane cp.async path: K and the (fiber, position) pairs only — the values go straight
+  // to registers, so st_v is an empty slot)
   static constexpr int st_k = 0;
   static constexpr int st_v = (st_k + CC * 4 + 32 + 15) & ~15;
-  static constexpr int st_b = (st_v + CE * (int)sizeof(S) + 32 + 15) & ~15;
+  static constexpr int st_b = st_v;
   static constexpr int stage = (st_b + CE * 2 + 32 + 15) & ~15;
   static constexpr int o_t = 2 * stage;  // S[CE]: Jacobian terms at canonical positions
   // warp stage (bulk): WPG groups' slices back to back, each array with 32 B of slack
