@@ -609,20 +609,23 @@ int g_sm_count[64] = {0};
 // at least 8 rows (G <= 4: the copies are large, measured faster on cfg3: fused 0.139 ->
 // 0.107 ms), per-lane cp.async otherwise (cfg4, 4 rows per warp: 0.87 vs 0.94 ms with WB).
 // EGFEM_CELLS_STAGE=cp|bulk forces one (experiments).
-bool cells_warp_bulk(int G) {
+// Warp-level TMA staging pays off for narrow groups (many rows per warp) of fp32 rows; with fp64
+// the per-lane path (values straight to registers, small shared footprint) measured faster
+// (cfg3 fused 0.107 -> 0.103 ms), with fp32 the bulk path (apply 0.043 -> 0.038 ms).
+bool cells_warp_bulk(int G, int vbytes) {
   static int v = -1;
   if (v < 0) {
     const char* e = getenv("EGFEM_CELLS_STAGE");
     v = (e && e[0] == 'b') ? 1 : (e && e[0] == 'c') ? 0 : 2;
   }
-  return v == 2 ? (G <= 4) : (v == 1);
+  return v == 2 ? (G <= 4 && vbytes == 4) : (v == 1);
 }
 
 template <typename S, int D1, int G, int CPL, int FREG, bool DO_R, int JAC>
 egfem_status run_cells(const egfem_tensor* t, const CellArgs<S>& A, cudaStream_t s) {
   constexpr bool SU = cells_su<S, FREG, JAC>() && (DO_R || JAC == kJacNewtonP0);
   using L = CellSmem<S, D1, G, CPL, JAC != kJacNone, SU ? G * FREG : 0>;
-  const bool wb = cells_warp_bulk(G);
+  const bool wb = cells_warp_bulk(G, (int)sizeof(S));
   auto fn = wb ? k_cell<S, D1, G, CPL, FREG, DO_R, JAC, true> : k_cell<S, D1, G, CPL, FREG, DO_R, JAC, false>;
   if constexpr (JAC == kJacNewtonP0 && D1 == 4 && sizeof(S) == 8) {
     if (A.chain32)
