@@ -192,20 +192,7 @@ def run_ours(args):
     def dist_step(ux, rx, e=None):
         """N>1: post the u-halo exchange, run the interior phase, wait for the halo (the
         compute stream waits on the communicator's), run the boundary phase."""
-        def interior():
-            eg.egfem_interp_range(t, pr.interp, pr.p, ux, w, chain, iw0, iw1, stream)
-            eg.egfem_apply_jacobian_rows(t, eg.JAC_NEWTON, pr.interp, pr.p, ux, w, chain, rx, J, ir0, ir1, stream)
-            if e:
-                e[1].record(stream)
-
-        def boundary():
-            if e:
-                e[2].record(stream)
-            eg.egfem_interp_range(t, pr.interp, pr.p, ux, w, chain, 0, iw0, stream)
-            eg.egfem_interp_range(t, pr.interp, pr.p, ux, w, chain, iw1, t.n_f, stream)
-            eg.egfem_apply_jacobian_rows(t, eg.JAC_NEWTON, pr.interp, pr.p, ux, w, chain, rx, J, 0, ir0, stream)
-            eg.egfem_apply_jacobian_rows(t, eg.JAC_NEWTON, pr.interp, pr.p, ux, w, chain, rx, J, ir1, t.n_u, stream)
-        edist.overlapped_step(plan, ux, interior, boundary)
+        edist.split_step(eg, t, plan, (ir0, ir1, iw0, iw1), pr.interp, pr.p, ux, w, chain, rx, J, stream, e)
 
     K, Wm = args.steps, args.warmup
     ev = [[torch.cuda.Event(enable_timing=True) for _ in range(4)] for _ in range(K)]

@@ -111,3 +111,32 @@ def overlapped_step(plan: HaloPlan, u_local, interior, boundary, group=None) -> 
     interior()
     halo_finish(reqs)
     boundary()
+
+
+def split_step(eg, t, plan: HaloPlan, split, kind, p, u_local, w, chain, r, csr, stream=None, events=None,
+               group=None) -> None:
+    """One distributed step (interp + fused apply/Newton Jacobian) of a row-partitioned local
+    tensor `t` with the u-halo exchange overlapped: `split` = egfem_interior(t) =
+    (row_lo, row_hi, item_lo, item_hi).  The interior items / rows run while the halo is in
+    flight; the boundary items [0, item_lo), [item_hi, n_items) and rows [0, row_lo),
+    [row_hi, n_u) after it has arrived.  P0 local tensors: interp items are cells = W DOFs,
+    W = V: W DOFs, so n_items = t.n_f.  `events` (optional, 4 CUDA events): [1] is recorded
+    after the interior phase, [2] once the halo has arrived."""
+    r0, r1, i0, i1 = split
+    n_items = t.n_f
+
+    def interior():
+        eg.egfem_interp_range(t, kind, p, u_local, w, chain, i0, i1, stream)
+        eg.egfem_apply_jacobian_rows(t, eg.JAC_NEWTON, kind, p, u_local, w, chain, r, csr, r0, r1, stream)
+        if events:
+            events[1].record(stream)
+
+    def boundary():
+        if events:
+            events[2].record(stream)
+        eg.egfem_interp_range(t, kind, p, u_local, w, chain, 0, i0, stream)
+        eg.egfem_interp_range(t, kind, p, u_local, w, chain, i1, n_items, stream)
+        eg.egfem_apply_jacobian_rows(t, eg.JAC_NEWTON, kind, p, u_local, w, chain, r, csr, 0, r0, stream)
+        eg.egfem_apply_jacobian_rows(t, eg.JAC_NEWTON, kind, p, u_local, w, chain, r, csr, r1, t.n_u, stream)
+
+    overlapped_step(plan, u_local, interior, boundary, group)

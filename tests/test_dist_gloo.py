@@ -154,3 +154,77 @@ def test_overlapped_step_gloo(world, reach):
     for rank, (equal, clean, n_inner) in res.items():
         assert equal and clean, (rank, res)
         assert (n_inner > 0) == (reach < 100), (rank, n_inner)
+
+
+class _MockEg:
+    """Records the library calls of dist.split_step (no GPU): which interp items and rows each
+    phase covers, and whether the halo had arrived when a call was made."""
+    JAC_NEWTON = 1
+
+    def __init__(self, ul, halo_mask):
+        self.ul, self.halo = ul, halo_mask
+        self.calls = []
+
+    def _halo_ready(self):
+        import torch
+        return bool(not torch.isnan(self.ul[self.halo]).any())
+
+    def egfem_interp_range(self, t, kind, p, u, w, chain, lo, hi, stream):
+        self.calls.append(("interp", lo, hi, self._halo_ready()))
+
+    def egfem_apply_jacobian_rows(self, t, mode, kind, p, u, w, chain, r, J, lo, hi, stream):
+        self.calls.append(("rows", lo, hi, self._halo_ready()))
+
+
+def _split_worker(rank, world, port, q):
+    import types
+
+    import torch
+    import torch.distributed as dist
+
+    from paper_2005_06193_b200.dist import Window, gather_windows, make_plan, split_step
+    os.environ.update(MASTER_ADDR="127.0.0.1", MASTER_PORT=str(port))
+    dist.init_process_group("gloo", rank=rank, world_size=world)
+    try:
+        n, reach = 400, 20
+        b = np.linspace(0, n, world + 1).astype(int)
+        me = Window(int(b[rank]), int(b[rank + 1]), max(0, int(b[rank]) - reach), min(n, int(b[rank + 1]) + reach))
+        plan = make_plan(gather_windows(me), rank)
+        ul = torch.full((plan.n_local,), float("nan"), dtype=torch.float64)
+        o, nr = plan.owned_offset, me.row_end - me.row_begin
+        ul[o:o + nr] = torch.arange(me.row_begin, me.row_end, dtype=torch.float64)
+        halo = torch.ones(plan.n_local, dtype=torch.bool)
+        halo[o:o + nr] = False
+        eg = _MockEg(ul, halo)
+        t = types.SimpleNamespace(n_u=nr, n_f=plan.n_local)
+        split = (reach, nr - reach, o, o + nr)  # interior rows / items of a banded operator
+        split_step(eg, t, plan, split, 0, 0.0, ul, None, None, None, None)
+        q.put((rank, eg.calls, nr, plan.n_local, split))
+    finally:
+        dist.destroy_process_group()
+
+
+def test_split_step_orchestration_gloo():
+    """dist.split_step (the bench's N>1 step): the interior interp items and rows are issued
+    before the halo is waited for, the boundary ones after it has arrived, and the ranges of
+    each kind cover [0, n) exactly once."""
+    import multiprocessing as mp
+    ctx = mp.get_context("spawn")
+    q = ctx.Queue()
+    port = _free_port()
+    procs = [ctx.Process(target=_split_worker, args=(r, 2, port, q)) for r in range(2)]
+    for p in procs:
+        p.start()
+    res = [q.get(timeout=120) for _ in range(2)]
+    for p in procs:
+        p.join(timeout=60)
+    for rank, calls, nr, n_items, split in res:
+        kinds = [c[0] for c in calls]
+        assert kinds == ["interp", "rows", "interp", "interp", "rows", "rows"], calls
+        assert all(c[3] for c in calls[2:]), calls  # boundary phase: halo in place
+        for kind, n in (("interp", n_items), ("rows", nr)):
+            cover = np.zeros(n, int)
+            for c in calls:
+                if c[0] == kind:
+                    cover[c[1]:c[2]] += 1
+            assert np.all(cover == 1), (kind, cover)
