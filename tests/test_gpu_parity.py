@@ -472,6 +472,33 @@ def test_overlap_split_reads_no_halo(eg, name, nranks):
     assert eg.egfem_interior(t) == (0, t.n_u, 0, n_items)
 
 
+@pytest.mark.parametrize("name,nranks", [("cfg4", 3), ("cfg2", 2), ("biochem_p0", 2)])
+def test_split_step_library_bitwise(eg, name, nranks):
+    """dist.split_step — the N>1 bench step through the library — on each rank's local tensor
+    with its window already filled (a plan without exchanges) reproduces the single-GPU r and J."""
+    import torch
+
+    from paper_2005_06193_b200 import dist as edist
+    pr = I.make_problem(name, n=I.SMALL_N[name])
+    t = eg.egfem_tensor_build(pr.mesh, pr.V, pr.W, pr.form, device=0)
+    ref = gpu_pass(eg, t, pr, pr.u)
+    grp = np.asarray(t.export(values=False)["csr_row_ptr"])
+    for rank in range(nranks):
+        loc, win = eg.egfem_partition(t, nranks, rank)
+        wdw = edist.Window(win["row_begin"], win["row_end"], win["col_begin"], win["col_end"])
+        plan = edist.HaloPlan(rank, wdw, [], [])
+        ul = torch.tensor(pr.u[wdw.col_begin:wdw.col_end], device="cuda")
+        wl = torch.empty(loc.n_f, dtype=torch.float64, device="cuda")
+        chain = torch.empty(loc.n_f * (pr.mesh.dim + 1), dtype=torch.float64, device="cuda") \
+            if pr.W.family in (I.P0, I.QUAD) and pr.interp != I.INTERP_IDENTITY else None
+        r = torch.empty(loc.n_u, dtype=torch.float64, device="cuda")
+        J = torch.empty(loc.nnz_csr, dtype=torch.float64, device="cuda")
+        edist.split_step(eg, loc, plan, eg.egfem_interior(loc), pr.interp, pr.p, ul, wl, chain, r, J)
+        torch.cuda.synchronize()
+        assert np.array_equal(r.cpu().numpy(), ref["r"][wdw.row_begin:wdw.row_end])
+        assert np.array_equal(J.cpu().numpy(), ref["J"][grp[wdw.row_begin]:grp[wdw.row_end]])
+
+
 @pytest.mark.parametrize("env", [{"EGFEM_PATH": "tile"}, {"EGFEM_PATH": "rows", "EGFEM_BATCHED": "csf"}])
 def test_kernel_paths(eg, env):
     """The non-default kernels (TMA tile kernel, canonical-CSF row kernel for P0 W, CSF batched
