@@ -551,6 +551,27 @@ __global__ void __launch_bounds__(kThreads) k_tile(const TileArgs<S> A) {
       }
     }
     if (DO_R || L::kP0) __syncthreads();
+    if (L::kP0) {
+      // B_iK = Σ_m (T_{i v_m K} u_{v_m}) once per (row, cell) of the tile, compacted in place to
+      // bp[cell]: rows of P0-W tensors hold d+1 nonzeros per cell, so cell c's parts sit at
+      // bp[c·(d+1) .. +d] (fixed summation order m = 0..d)
+      constexpr int CPT = (kTileNnz / 2 + kThreads - 1) / kThreads;  // cells per thread (d+1 >= 2)
+      S bs[CPT];
+      const int ncell = g.ne / A.d1;
+#pragma unroll
+      for (int c = 0; c < CPT; ++c) {
+        const int cc = tid + c * kThreads;
+        S B = S(0);
+        if (cc < ncell)
+          for (int m = 0; m < A.d1; ++m) B += bp[cc * A.d1 + m];
+        bs[c] = B;
+      }
+      __syncthreads();
+#pragma unroll
+      for (int c = 0; c < CPT; ++c)
+        if (tid + c * kThreads < ncell) bp[tid + c * kThreads] = bs[c];
+      __syncthreads();
+    }
     // ---- phase C: rows and Newton terms
     if (DO_R) {
       for (int row = tid; row < g.nr; row += kThreads) {
@@ -597,12 +618,8 @@ __global__ void __launch_bounds__(kThreads) k_tile(const TileArgs<S> A) {
           const int rowbase = (int)(v.fnz[v.rf[row] - g.f0] - (uint32_t)g.e0);
           const int ya = (int)(v.fnz[x] - (uint32_t)g.e0), yb = (int)(v.fnz[x + 1] - (uint32_t)g.e0);
           S acc = areg[c];
-          for (int y = ya; y < yb; ++y) {
-            const int b = rowbase + (int)v.aux[y] * A.d1;
-            S B = S(0);
-            for (int m = 0; m < A.d1; ++m) B += bp[b + m];
-            acc += B * v.d[y];
-          }
+          const int cbase = rowbase / A.d1;
+          for (int y = ya; y < yb; ++y) acc += bp[cbase + (int)v.aux[y]] * v.d[y];
           A.csr[g.f0 + x] = acc;
         }
       }
