@@ -425,9 +425,9 @@ egfem_status upload_mesh(egfem_tensor* t, const egfem_mesh* mesh, const egfem_sp
   EGFEM_CUDA_TRY(cudaMalloc(&t->wdofs, sizeof(int32_t) * nc * t->nW));
   EGFEM_CUDA_TRY(cudaMemcpy(t->wdofs, hw, sizeof(int32_t) * nc * t->nW, cudaMemcpyHostToDevice));
   t->vdofs_is_cells = (V->family == EGFEM_P1) && std::equal(hvcopy.begin(), hvcopy.end(), mesh->cells);
-  if (W->family == EGFEM_P0) {
+  if (W->family == EGFEM_P0 || W->family == EGFEM_QUAD) {  // canonical cell-wise numbering: (c, l) -> c·nW + l
     t->wdofs_is_iota = true;
-    for (int64_t c = 0; c < nc && t->wdofs_is_iota; ++c) t->wdofs_is_iota = (hw[c] == (int32_t)c);
+    for (int64_t x = 0; x < nc * t->nW && t->wdofs_is_iota; ++x) t->wdofs_is_iota = (hw[x] == (int32_t)x);
   }
   if (d == 3) {
     std::vector<double> c4((size_t)mesh->n_vertices * 4, 0.0);

@@ -90,7 +90,7 @@ struct egfem_tensor {
   double* coords = nullptr;     // n_vertices*dim
   double* coords4 = nullptr;    // 3D only: n_vertices*4 (x, y, z, 0) for 32-byte vector loads
   bool vdofs_is_cells = false;  // V DOF table == mesh cell table (canonical P1)
-  bool wdofs_is_iota = false;   // W DOF of cell c is c (canonical P0)
+  bool wdofs_is_iota = false;   // W DOF l of cell c is c·nW + l (canonical P0 / QUAD)
   int32_t* cells = nullptr;     // n_cells*(dim+1) mesh vertex ids (geometry)
   int32_t* vdofs = nullptr;     // n_cells*nV  V dof ids (u indices)
   int32_t* wdofs = nullptr;     // n_cells*nW  W dof ids

@@ -260,6 +260,51 @@ __global__ void k_interp_points(const int32_t* __restrict__ vdofs, const int32_t
   }
 }
 
+// The same with canonical cell-wise numbering (W DOF l of cell c is c·nw + l): a CTA's cells own
+// one contiguous span of w and of the chain, so each thread computes its cell's points into
+// shared memory and the CTA writes both spans out coalesced (the per-thread rows of the kernel
+// above are nw and nw·(d+1) values apart between neighbouring threads).
+template <typename S>
+__global__ void __launch_bounds__(128) k_interp_points_blk(const int32_t* __restrict__ vdofs,
+                                                           const double* __restrict__ wpts, int64_t n_cells, int d1,
+                                                           int nw, const S* __restrict__ u, S* __restrict__ w,
+                                                           S* __restrict__ chain, int mode, double pk) {
+  extern __shared__ __align__(16) unsigned char smem_pts[];
+  S* s_w = reinterpret_cast<S*>(smem_pts);
+  S* s_c = s_w + 128 * nw;
+  const int64_t c0 = (int64_t)blockIdx.x * 128;
+  const int nc = (int)min((int64_t)128, n_cells - c0);
+  const int tid = threadIdx.x;
+  if (tid < nc) {
+    const int64_t c = c0 + tid;
+    double uv[4];
+    for (int a = 0; a < d1; ++a) uv[a] = (double)__ldg(u + __ldg(vdofs + c * d1 + a));
+    for (int l = 0; l < nw; ++l) {
+      const double* lam = wpts + l * d1;
+      double uh = 0.0;
+      for (int a = 0; a < d1; ++a) uh += lam[a] * uv[a];
+      double f, df;
+      if (mode == 0) {
+        f = 1.0 / (pk + uh);
+        df = -(f * f);
+      } else {
+        f = uh * uh;
+        df = 2.0 * uh;
+      }
+      s_w[tid * nw + l] = (S)f;
+      if (chain)
+        for (int a = 0; a < d1; ++a) s_c[(tid * nw + l) * d1 + a] = (S)(df * lam[a]);
+    }
+  }
+  __syncthreads();
+  S* wo = w + c0 * nw;
+  for (int x = tid; x < nc * nw; x += 128) wo[x] = s_w[x];
+  if (chain) {
+    S* co = chain + c0 * nw * d1;
+    for (int x = tid; x < nc * nw * d1; x += 128) co[x] = s_c[x];
+  }
+}
+
 // P1 → P2 interpolant squared: vertex DOFs u_v², edge DOFs ((u_a + u_b)/2)².
 template <typename S>
 __global__ void k_interp_p1p2sq(const int32_t* __restrict__ vdofs, const int32_t* __restrict__ wdofs, int64_t n_cells,
@@ -798,12 +843,29 @@ egfem_status launch_interp(const egfem_tensor* t, egfem_interp_kind kind, double
     const int d1 = t->dim + 1;
     const int32_t* vd = t->vdofs + lo * d1;
     const int32_t* wd = t->wdofs + lo * t->nwc;
-    if (f64)
+    if (t->wdofs_is_iota) {  // outputs of cells [lo, hi) are the spans from W DOF lo·nw on
+      const int sm = 128 * t->nwc * (1 + d1) * (int)vs;
+      const int64_t wo = lo * t->nwc;
+      if (f64) {
+        if (sm > 48 * 1024)
+          EGFEM_CUDA_TRY(cudaFuncSetAttribute(k_interp_points_blk<double>, cudaFuncAttributeMaxDynamicSharedMemorySize, sm));
+        k_interp_points_blk<double><<<nblk(n, 128), 128, sm, s>>>(vd, t->wpts, n, d1, t->nwc, (const double*)u,
+                                                                  (double*)w + wo,
+                                                                  chain ? (double*)chain + wo * d1 : nullptr, mode, p);
+      } else {
+        if (sm > 48 * 1024)
+          EGFEM_CUDA_TRY(cudaFuncSetAttribute(k_interp_points_blk<float>, cudaFuncAttributeMaxDynamicSharedMemorySize, sm));
+        k_interp_points_blk<float><<<nblk(n, 128), 128, sm, s>>>(vd, t->wpts, n, d1, t->nwc, (const float*)u,
+                                                                 (float*)w + wo,
+                                                                 chain ? (float*)chain + wo * d1 : nullptr, mode, p);
+      }
+    } else if (f64) {
       k_interp_points<double><<<nblk(n, 128), 128, 0, s>>>(vd, wd, t->wpts, n, d1, t->nwc, (const double*)u,
                                                            (double*)w, (double*)chain, mode, p);
-    else
+    } else {
       k_interp_points<float><<<nblk(n, 128), 128, 0, s>>>(vd, wd, t->wpts, n, d1, t->nwc, (const float*)u,
                                                           (float*)w, (float*)chain, mode, p);
+    }
     count_launch();
   } else if (kind == EGFEM_INTERP_GRADPOW_P0 || kind == EGFEM_INTERP_MINSURF_P0) {
     const int grid = std::max(1, nblk(n, 128));  // capped at one resident wave below
@@ -824,7 +886,7 @@ egfem_status launch_interp(const egfem_tensor* t, egfem_interp_kind kind, double
   } while (0)
 #define EGFEM_GP(S, D)                                                          \
   do {                                                                          \
-    if (t->vdofs_is_cells && t->wdofs_is_iota) EGFEM_GP3(S, D, true, true);     \
+    if (t->vdofs_is_cells && t->wdofs_is_iota && t->nwc == 1) EGFEM_GP3(S, D, true, true); \
     else EGFEM_GP3(S, D, false, false);                                         \
   } while (0)
     if (f64) {
