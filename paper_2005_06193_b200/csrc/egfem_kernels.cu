@@ -72,13 +72,19 @@ struct CellIn {
   double x[D + 1][D];
   double uv[D + 1];
 };
-template <typename S, int D, bool SAME>
-__device__ __forceinline__ void gather_cell(const double* __restrict__ coords, const CellIdx<D>& cv,
-                                            const CellIdx<D>& dv, const S* __restrict__ u, CellIn<S, D>& in) {
+template <typename S, int D, bool SAME, bool CF>
+__device__ __forceinline__ void gather_cell(const double* __restrict__ coords, const float* __restrict__ coordsf,
+                                            const CellIdx<D>& cv, const CellIdx<D>& dv, const S* __restrict__ u,
+                                            CellIn<S, D>& in) {
 #pragma unroll
   for (int a = 0; a <= D; ++a) {
     const int64_t v = cv.v[a];
-    if constexpr (D == 3) {
+    if constexpr (D == 3 && CF) {  // exact float copy of the coordinates: one 16-byte load
+      const float4 q = __ldg(reinterpret_cast<const float4*>(coordsf) + v);
+      in.x[a][0] = (double)q.x;
+      in.x[a][1] = (double)q.y;
+      in.x[a][2] = (double)q.z;
+    } else if constexpr (D == 3) {
       const double2 xy = __ldg(reinterpret_cast<const double2*>(coords + v * 4));
       in.x[a][0] = xy.x;
       in.x[a][1] = xy.y;
@@ -201,8 +207,9 @@ __device__ __forceinline__ void gradpow_cell(const CellIn<S, D>& in, int64_t c, 
 // Grid-stride and software-pipelined: the cell record is loaded two cells ahead and the next
 // cell's vertex coordinates and u one cell ahead, so the dependent record → coordinates
 // gather chain overlaps the current cell's arithmetic instead of stalling every thread.
-template <typename S, int D, bool SAME, bool IOTA>
-__global__ void __launch_bounds__(128) k_interp_gradpow(const double* __restrict__ coords, const int32_t* __restrict__ cells,
+template <typename S, int D, bool SAME, bool IOTA, bool CF>
+__global__ void __launch_bounds__(128) k_interp_gradpow(const double* __restrict__ coords, const float* __restrict__ coordsf,
+                                 const int32_t* __restrict__ cells,
                                  const int32_t* __restrict__ vdofs, const int32_t* __restrict__ wdofs, int64_t n_cells,
                                  const S* __restrict__ u, S* __restrict__ w, S* __restrict__ chain, double p,
                                  bool minsurf, int nw) {
@@ -217,11 +224,11 @@ __global__ void __launch_bounds__(128) k_interp_gradpow(const double* __restrict
   CellIdx<D> cv1, dv1, cv2, dv2;
   idx(c, cv1, dv1);
   CellIn<S, D> cur;
-  gather_cell<S, D, SAME>(coords, cv1, dv1, u, cur);
+  gather_cell<S, D, SAME, CF>(coords, coordsf, cv1, dv1, u, cur);
   idx(c + stride, cv2, dv2);
   for (; c < n_cells; c += stride) {
     CellIn<S, D> nxt;
-    gather_cell<S, D, SAME>(coords, cv2, dv2, u, nxt);  // next cell's gathers in flight
+    gather_cell<S, D, SAME, CF>(coords, coordsf, cv2, dv2, u, nxt);  // next cell's gathers in flight
     idx(c + 2 * stride, cv2, dv2);                      // record two cells ahead
     gradpow_cell<S, D, IOTA>(cur, c, wdofs, w, chain, p, minsurf, nw);
     cur = nxt;
@@ -873,16 +880,21 @@ egfem_status launch_interp(const egfem_tensor* t, egfem_interp_kind kind, double
     const int32_t* cl = t->cells + lo * d1;
     const int32_t* vd = t->vdofs + lo * t->nV;
     const int32_t* wd = t->wdofs + lo * t->nwc;
-#define EGFEM_GP3(S, D, SA, IO)                                                                       \
+#define EGFEM_GP4(S, D, SA, IO, CF)                                                                   \
   do {                                                                                                \
     int per_sm = 0;                                                                                   \
-    cudaOccupancyMaxActiveBlocksPerMultiprocessor(&per_sm, k_interp_gradpow<S, D, SA, IO>, 128, 0);   \
+    cudaOccupancyMaxActiveBlocksPerMultiprocessor(&per_sm, k_interp_gradpow<S, D, SA, IO, CF>, 128, 0); \
     const int g = (int)std::min<int64_t>(grid, (int64_t)std::max(per_sm, 1) * 148);                   \
     S* wl = IO ? (S*)w + lo : (S*)w;                                                                  \
     S* cl2 = (IO && chain) ? (S*)chain + lo * (D + 1) : (S*)chain;                                    \
-    k_interp_gradpow<S, D, SA, IO><<<g, 128, 0, s>>>(D == 3 ? t->coords4 : t->coords, cl, vd, wd, n,  \
-                                                     (const S*)u, wl, cl2, p,                         \
-                                                     kind == EGFEM_INTERP_MINSURF_P0, t->nwc);         \
+    k_interp_gradpow<S, D, SA, IO, CF><<<g, 128, 0, s>>>(D == 3 ? t->coords4 : t->coords, t->coords4f, cl, vd, \
+                                                         wd, n, (const S*)u, wl, cl2, p,              \
+                                                         kind == EGFEM_INTERP_MINSURF_P0, t->nwc);     \
+  } while (0)
+#define EGFEM_GP3(S, D, SA, IO)                                                 \
+  do {                                                                          \
+    if (D == 3 && t->coords4f) EGFEM_GP4(S, D, SA, IO, true);                   \
+    else EGFEM_GP4(S, D, SA, IO, false);                                        \
   } while (0)
 #define EGFEM_GP(S, D)                                                          \
   do {                                                                          \
@@ -894,6 +906,7 @@ egfem_status launch_interp(const egfem_tensor* t, egfem_interp_kind kind, double
     } else {
       if (t->dim == 1) EGFEM_GP(float, 1); else if (t->dim == 2) EGFEM_GP(float, 2); else EGFEM_GP(float, 3);
     }
+#undef EGFEM_GP4
 #undef EGFEM_GP3
 #undef EGFEM_GP
     count_launch();
