@@ -743,9 +743,10 @@ egfem_status egfem_partition(const egfem_tensor* G, int32_t nranks, int32_t rank
     if (G->dim == 3 && (cudaMalloc(&t->coords4, 32 * std::max<int64_t>(n_local, 1)) ||
                         cudaMemcpy(t->coords4, G->coords4 + cb * 4, 32 * n_local, cudaMemcpyDeviceToDevice)))
       return bail(fail(EGFEM_ERR_CUDA, "coords4 copy failed"));
-    if (G->coords4f && (cudaMalloc(&t->coords4f, 16 * std::max<int64_t>(n_local, 1)) ||
-                        cudaMemcpy(t->coords4f, G->coords4f + cb * 4, 16 * n_local, cudaMemcpyDeviceToDevice)))
-      return bail(fail(EGFEM_ERR_CUDA, "coords4f copy failed"));
+    const int cfs = G->dim == 3 ? 4 : 2;  // floats per vertex of the exact float copy
+    if (G->coordsf && (cudaMalloc(&t->coordsf, 4 * cfs * std::max<int64_t>(n_local, 1)) ||
+                       cudaMemcpy(t->coordsf, G->coordsf + cb * cfs, 4 * cfs * n_local, cudaMemcpyDeviceToDevice)))
+      return bail(fail(EGFEM_ERR_CUDA, "coordsf copy failed"));
     if (cudaMemcpy(t->coords, G->coords + cb * G->dim, 8 * n_local * G->dim, cudaMemcpyDeviceToDevice) ||
         (ncl && cudaMemcpy(t->cells, lc.data(), 4 * lc.size(), cudaMemcpyHostToDevice)) ||
         (ncl && cudaMemcpy(t->vdofs, lv.data(), 4 * lv.size(), cudaMemcpyHostToDevice)) ||

@@ -445,8 +445,18 @@ egfem_status upload_mesh(egfem_tensor* t, const egfem_mesh* mesh, const egfem_sp
       }
     if (exact) {
       std::vector<float> c4f(c4.begin(), c4.end());
-      EGFEM_CUDA_TRY(cudaMalloc(&t->coords4f, sizeof(float) * c4f.size()));
-      EGFEM_CUDA_TRY(cudaMemcpy(t->coords4f, c4f.data(), sizeof(float) * c4f.size(), cudaMemcpyHostToDevice));
+      EGFEM_CUDA_TRY(cudaMalloc(&t->coordsf, sizeof(float) * c4f.size()));
+      EGFEM_CUDA_TRY(cudaMemcpy(t->coordsf, c4f.data(), sizeof(float) * c4f.size(), cudaMemcpyHostToDevice));
+    }
+  }
+  if (d == 2) {  // lossless float2 copy when every coordinate is exactly a float
+    const int64_t nv2 = (int64_t)mesh->n_vertices * 2;
+    bool exact = true;
+    for (int64_t x = 0; x < nv2 && exact; ++x) exact = (double)(float)mesh->coords[x] == mesh->coords[x];
+    if (exact) {
+      std::vector<float> c2f(mesh->coords, mesh->coords + nv2);
+      EGFEM_CUDA_TRY(cudaMalloc(&t->coordsf, sizeof(float) * std::max<int64_t>(nv2, 1)));
+      EGFEM_CUDA_TRY(cudaMemcpy(t->coordsf, c2f.data(), sizeof(float) * nv2, cudaMemcpyHostToDevice));
     }
   }
   t->w_is_v = (V->family == W->family) && (V->n_dofs == W->n_dofs) &&
@@ -900,7 +910,7 @@ egfem_status export_arrays(const egfem_tensor* t, int64_t* t_row_ptr, int32_t* t
 
 void free_tensor(egfem_tensor* t) {
   void* ptrs[] = {t->row_fib, t->row_nz, t->fib_j, t->fib_nz, t->nz_k, t->nz_val, t->nz_aux, t->nz_kpos, t->fib_kr, t->ck_k, t->ck_val, t->ck_b, t->blk_off, t->blk, t->dense_rows,
-                  t->tile_row, t->tile_fib, t->tile_nz, t->coords, t->coords4, t->coords4f, t->cells, t->vdofs, t->wdofs, t->wcell, t->wpts};
+                  t->tile_row, t->tile_fib, t->tile_nz, t->coords, t->coords4, t->coordsf, t->cells, t->vdofs, t->wdofs, t->wcell, t->wpts};
   for (void* p : ptrs)
     if (p) cudaFree(p);
 }

@@ -89,7 +89,7 @@ struct egfem_tensor {
   // interpolation data (device): geometry in fp64 regardless of dtype
   double* coords = nullptr;     // n_vertices*dim
   double* coords4 = nullptr;    // 3D only: n_vertices*4 (x, y, z, 0) for 32-byte vector loads
-  float* coords4f = nullptr;    // 3D only, when every coordinate is exactly a float: the same as float4 (lossless)
+  float* coordsf = nullptr;     // 2D/3D, when every coordinate is exactly a float: float2 (x, y) / float4 (x, y, z, 0) copy (lossless)
   bool vdofs_is_cells = false;  // V DOF table == mesh cell table (canonical P1)
   bool wdofs_is_iota = false;   // W DOF l of cell c is c·nW + l (canonical P0 / QUAD)
   int32_t* cells = nullptr;     // n_cells*(dim+1) mesh vertex ids (geometry)

@@ -84,6 +84,10 @@ __device__ __forceinline__ void gather_cell(const double* __restrict__ coords, c
       in.x[a][0] = (double)q.x;
       in.x[a][1] = (double)q.y;
       in.x[a][2] = (double)q.z;
+    } else if constexpr (D == 2 && CF) {  // exact float copy: one 8-byte load
+      const float2 q = __ldg(reinterpret_cast<const float2*>(coordsf) + v);
+      in.x[a][0] = (double)q.x;
+      in.x[a][1] = (double)q.y;
     } else if constexpr (D == 3) {
       const double2 xy = __ldg(reinterpret_cast<const double2*>(coords + v * 4));
       in.x[a][0] = xy.x;
@@ -887,13 +891,13 @@ egfem_status launch_interp(const egfem_tensor* t, egfem_interp_kind kind, double
     const int g = (int)std::min<int64_t>(grid, (int64_t)std::max(per_sm, 1) * 148);                   \
     S* wl = IO ? (S*)w + lo : (S*)w;                                                                  \
     S* cl2 = (IO && chain) ? (S*)chain + lo * (D + 1) : (S*)chain;                                    \
-    k_interp_gradpow<S, D, SA, IO, CF><<<g, 128, 0, s>>>(D == 3 ? t->coords4 : t->coords, t->coords4f, cl, vd, \
+    k_interp_gradpow<S, D, SA, IO, CF><<<g, 128, 0, s>>>(D == 3 ? t->coords4 : t->coords, t->coordsf, cl, vd, \
                                                          wd, n, (const S*)u, wl, cl2, p,              \
                                                          kind == EGFEM_INTERP_MINSURF_P0, t->nwc);     \
   } while (0)
 #define EGFEM_GP3(S, D, SA, IO)                                                 \
   do {                                                                          \
-    if (D == 3 && t->coords4f) EGFEM_GP4(S, D, SA, IO, true);                   \
+    if (D >= 2 && t->coordsf) EGFEM_GP4(S, D, SA, IO, true);                    \
     else EGFEM_GP4(S, D, SA, IO, false);                                        \
   } while (0)
 #define EGFEM_GP(S, D)                                                          \
