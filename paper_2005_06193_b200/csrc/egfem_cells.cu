@@ -32,6 +32,12 @@ namespace egfem {
 namespace {
 
 enum { kJacNone = 0, kJacPicard = 1, kJacNewtonP0 = 3 };
+// threads per CTA: 256 for fp64 (2 CTAs/SM at 128 registers), 128 for fp32 (4 CTAs/SM; measured
+// on cfg4 fp32: fused 0.51 -> 0.47 ms; fp64 fused is faster with 256)
+template <typename S>
+__host__ __device__ constexpr int cell_threads() {
+  return sizeof(S) == 4 ? 128 : 256;
+}
 
 template <typename S>
 struct CellArgs {
@@ -290,10 +296,12 @@ __host__ __device__ constexpr bool cells_su() {
 // C32: the D_u w rows are 32-byte aligned and read with one 256-bit load each (a compile-time
 // choice: a runtime branch between load widths makes the merged result wait on the load at once)
 template <typename S, int D1, int G, int CPL, int FREG, bool DO_R, int JAC, bool WB, bool C32 = false>
-__global__ void __launch_bounds__(256, (JAC == kJacNone || G >= 16) ? 3 : 2) k_cell(const CellArgs<S> A) {
+__global__ void __launch_bounds__(cell_threads<S>(),
+                                  (JAC == kJacNone || G >= 16) ? 3 * 256 / cell_threads<S>() : 2 * 256 / cell_threads<S>())
+    k_cell(const CellArgs<S> A) {
   constexpr bool SU = cells_su<S, FREG, JAC>() && (DO_R || JAC == kJacNewtonP0);
   using L = CellSmem<S, D1, G, CPL, JAC != kJacNone, SU ? G * FREG : 0>;
-  constexpr int GPB = 256 / G;
+  constexpr int GPB = cell_threads<S>() / G;
   constexpr bool kJ = JAC != kJacNone;
   constexpr bool kN = JAC == kJacNewtonP0;
   constexpr bool kU = DO_R || kN;  // u (and B_iK) needed; the Picard matrix alone reads no u
@@ -631,16 +639,17 @@ egfem_status run_cells(const egfem_tensor* t, const CellArgs<S>& A, cudaStream_t
     if (A.chain32)
       fn = wb ? k_cell<S, D1, G, CPL, FREG, DO_R, JAC, true, true> : k_cell<S, D1, G, CPL, FREG, DO_R, JAC, false, true>;
   }
-  const int smem = wb ? L::wbytes * 8 : L::bytes * (256 / G);
+  constexpr int CT = cell_threads<S>();
+  const int smem = wb ? L::wbytes * (CT / 32) : L::bytes * (CT / G);
   if (smem > 48 * 1024) EGFEM_CUDA_TRY(cudaFuncSetAttribute(fn, cudaFuncAttributeMaxDynamicSharedMemorySize, smem));
   const int dev = t->device & 63;
   if (!g_sm_count[dev])
     EGFEM_CUDA_TRY(cudaDeviceGetAttribute(&g_sm_count[dev], cudaDevAttrMultiProcessorCount, t->device));
   int per_sm = 0;
-  EGFEM_CUDA_TRY(cudaOccupancyMaxActiveBlocksPerMultiprocessor(&per_sm, fn, 256, smem));
-  const int64_t need = (t->n_u + (256 / G) - 1) / (256 / G);
+  EGFEM_CUDA_TRY(cudaOccupancyMaxActiveBlocksPerMultiprocessor(&per_sm, fn, CT, smem));
+  const int64_t need = (t->n_u + (CT / G) - 1) / (CT / G);
   const int grid = (int)std::max<int64_t>(1, std::min<int64_t>(need, (int64_t)std::max(per_sm, 1) * g_sm_count[dev]));
-  fn<<<grid, 256, smem, s>>>(A);
+  fn<<<grid, CT, smem, s>>>(A);
   count_launch();
   EGFEM_CUDA_TRY(cudaGetLastError());
   return EGFEM_OK;
