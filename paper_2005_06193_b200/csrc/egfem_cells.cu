@@ -32,11 +32,12 @@ namespace egfem {
 namespace {
 
 enum { kJacNone = 0, kJacPicard = 1, kJacNewtonP0 = 3 };
-// threads per CTA: 256 for fp64 (2 CTAs/SM at 128 registers), 128 for fp32 (4 CTAs/SM; measured
-// on cfg4 fp32: fused 0.51 -> 0.47 ms; fp64 fused is faster with 256)
-template <typename S>
+// threads per CTA: 256 for the fp64 Newton / apply kernels (2-3 CTAs/SM), 128 for fp32 and for
+// the fp64 Picard matrix (measured on cfg4: fp32 fused 0.51 -> 0.47 ms, fp64 Picard 0.51 ->
+// 0.48 ms; fp64 fused is faster with 256)
+template <typename S, int JAC>
 __host__ __device__ constexpr int cell_threads() {
-  return sizeof(S) == 4 ? 128 : 256;
+  return (sizeof(S) == 4 || JAC == kJacPicard) ? 128 : 256;
 }
 
 template <typename S>
@@ -296,12 +297,12 @@ __host__ __device__ constexpr bool cells_su() {
 // C32: the D_u w rows are 32-byte aligned and read with one 256-bit load each (a compile-time
 // choice: a runtime branch between load widths makes the merged result wait on the load at once)
 template <typename S, int D1, int G, int CPL, int FREG, bool DO_R, int JAC, bool WB, bool C32 = false>
-__global__ void __launch_bounds__(cell_threads<S>(),
-                                  (JAC == kJacNone || G >= 16) ? 3 * 256 / cell_threads<S>() : 2 * 256 / cell_threads<S>())
+__global__ void __launch_bounds__(cell_threads<S, JAC>(),
+                                  (JAC == kJacNone || G >= 16) ? 3 * 256 / cell_threads<S, JAC>() : 2 * 256 / cell_threads<S, JAC>())
     k_cell(const CellArgs<S> A) {
   constexpr bool SU = cells_su<S, FREG, JAC>() && (DO_R || JAC == kJacNewtonP0);
   using L = CellSmem<S, D1, G, CPL, JAC != kJacNone, SU ? G * FREG : 0>;
-  constexpr int GPB = cell_threads<S>() / G;
+  constexpr int GPB = cell_threads<S, JAC>() / G;
   constexpr bool kJ = JAC != kJacNone;
   constexpr bool kN = JAC == kJacNewtonP0;
   constexpr bool kU = DO_R || kN;  // u (and B_iK) needed; the Picard matrix alone reads no u
@@ -639,7 +640,7 @@ egfem_status run_cells(const egfem_tensor* t, const CellArgs<S>& A, cudaStream_t
     if (A.chain32)
       fn = wb ? k_cell<S, D1, G, CPL, FREG, DO_R, JAC, true, true> : k_cell<S, D1, G, CPL, FREG, DO_R, JAC, false, true>;
   }
-  constexpr int CT = cell_threads<S>();
+  constexpr int CT = cell_threads<S, JAC>();
   const int smem = wb ? L::wbytes * (CT / 32) : L::bytes * (CT / G);
   if (smem > 48 * 1024) EGFEM_CUDA_TRY(cudaFuncSetAttribute(fn, cudaFuncAttributeMaxDynamicSharedMemorySize, smem));
   const int dev = t->device & 63;
