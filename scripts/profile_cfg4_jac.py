@@ -1,4 +1,5 @@
-"""Launch sequence for ncu: cfg4 apply, Picard, Newton, fused (once each, after one warm pass)."""
+"""Launch sequence for ncu: cfg4 apply, Picard, Newton, fused (once each, after one warm pass).
+usage: python scripts/profile_cfg4_jac.py [f64|f32]"""
 import os
 import sys
 
@@ -9,12 +10,14 @@ import egfem_inputs as I
 import paper_2005_06193_b200 as eg
 
 pr = I.make_problem("cfg4")
-t = eg.egfem_tensor_build(pr.mesh, pr.V, pr.W, pr.form, device=0)
-u = torch.tensor(pr.u, device="cuda")
-w = torch.empty(t.n_f, dtype=torch.float64, device="cuda")
-chain = torch.empty(t.n_f * 4, dtype=torch.float64, device="cuda")
-r = torch.empty(t.n_u, dtype=torch.float64, device="cuda")
-J = torch.empty(t.nnz_csr, dtype=torch.float64, device="cuda")
+f32 = len(sys.argv) > 1 and sys.argv[1] == "f32"
+td = torch.float32 if f32 else torch.float64
+t = eg.egfem_tensor_build(pr.mesh, pr.V, pr.W, pr.form, dtype=eg.F32 if f32 else eg.F64, device=0)
+u = torch.tensor(pr.u, dtype=td, device="cuda")
+w = torch.empty(t.n_f, dtype=td, device="cuda")
+chain = torch.empty(t.n_f * 4, dtype=td, device="cuda")
+r = torch.empty(t.n_u, dtype=td, device="cuda")
+J = torch.empty(t.nnz_csr, dtype=td, device="cuda")
 eg.egfem_interp(t, pr.interp, pr.p, u, w, chain)
 eg.egfem_apply(t, u, w, r)
 eg.egfem_jacobian(t, eg.JAC_PICARD, pr.interp, pr.p, None, w, None, J)
