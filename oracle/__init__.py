@@ -59,8 +59,23 @@ def lib():
         L.oracle_jacobian.restype = i32
         L.oracle_bilinear.argtypes = [P, P]
         L.oracle_bilinear.restype = i32
+        L.oracle_rule.argtypes = [i32, i32, i32, P, P]
+        L.oracle_rule.restype = i32
         _lib = L
     return _lib
+
+
+def rule(dim, degree):
+    """The oracle's default quadrature rule for an integrand of `degree` in `dim` D:
+    (bary[nq, dim+1], weights[nq]) with weights summing to 1."""
+    L = lib()
+    nq = L.oracle_rule(dim, degree, 0, None, None)
+    if nq <= 0:
+        raise ValueError(f"oracle_rule failed rc={nq}")
+    bary = np.zeros((nq, dim + 1), np.float64)
+    w = np.zeros(nq, np.float64)
+    L.oracle_rule(dim, degree, nq, bary.ctypes.data_as(ctypes.c_void_p), w.ctypes.data_as(ctypes.c_void_p))
+    return bary, w
 
 
 def _p(a):

@@ -158,12 +158,68 @@ static int family_degree(int f) { return (f == OF_P0 || f == OF_QUAD) ? 0 : (f =
 // Reference rules in barycentric coordinates, weights summing to 1 (physical
 // weight = weight × |K|).  1D: 3-point Gauss.  2D: centroid (deg 1),
 // (2/3,1/6,1/6) (deg 2), 6-point symmetric Dunavant (deg 4).  3D: centroid,
-// 4-point (deg 2).
+// 4-point (deg 2), collapsed Gauss product (deg ≥ 3, below).
 struct Rule {
   int nq;
   std::vector<double> bary;  // nq*(d+1)
   std::vector<double> w;
 };
+
+// n-point Gauss–Legendre on [0,1] (textbook: Newton on the three-term Legendre recurrence
+// P_{m+1} = ((2m+1) x P_m − m P_{m−1})/(m+1) on [−1,1], weights 2/((1−x²)P_n'(x)²), then
+// mapped to [0,1]).  Exact for polynomials of degree ≤ 2n−1.
+static void gauss_legendre01(int n, std::vector<double>& x01, std::vector<double>& w01) {
+  const double pi = std::acos(-1.0);
+  x01.assign(n, 0.0);
+  w01.assign(n, 0.0);
+  for (int i = 0; i < n; ++i) {
+    double x = std::cos(pi * (i + 0.75) / (n + 0.5));
+    double dp = 0;
+    for (int it = 0; it < 100; ++it) {
+      double p0 = 1.0, p1 = x;
+      for (int m = 1; m < n; ++m) {
+        double p2 = ((2.0 * m + 1.0) * x * p1 - m * p0) / (m + 1.0);
+        p0 = p1;
+        p1 = p2;
+      }
+      // p1 = P_n(x), p0 = P_{n-1}(x)
+      dp = n * (x * p1 - p0) / (x * x - 1.0);
+      double dx = p1 / dp;
+      x -= dx;
+      if (std::fabs(dx) < 1e-17) break;
+    }
+    x01[i] = 0.5 * (1.0 - x);
+    w01[i] = 0.5 * 2.0 / ((1.0 - x * x) * dp * dp);
+  }
+}
+
+// Tetrahedral rule exact for total degree `degree` (≥ 3): the collapsed-coordinate (Duffy)
+// product of Gauss–Legendre rules.  The unit cube maps onto the reference tetrahedron
+// {ξ ≥ 0, ξ1+ξ2+ξ3 ≤ 1} by ξ1 = s, ξ2 = t(1−s), ξ3 = v(1−s)(1−t) with Jacobian (1−s)²(1−t); a
+// polynomial of degree p in ξ becomes one of degree ≤ p+2 in s, p+1 in t, p in v, so n points
+// per direction with 2n−1 ≥ p+2 integrate it exactly.  All weights are positive.  Weights are
+// normalised to sum to 1 (physical weight = weight × |K|), barycentric λ = (1−Σξ, ξ1, ξ2, ξ3).
+// This makes every 3D form the exact integral of PAPER.md L196–203 eq. (egfem_terms), e.g. the
+// trilinear mass M of L327 (degree 3 for P1×P1×P1).
+static Rule collapsed_gauss_tet(int degree) {
+  const int n = (degree + 4) / 2;
+  std::vector<double> x, w;
+  gauss_legendre01(n, x, w);
+  Rule R;
+  R.nq = n * n * n;
+  for (int a = 0; a < n; ++a)
+    for (int b = 0; b < n; ++b)
+      for (int c = 0; c < n; ++c) {
+        const double s = x[a], t = x[b], v = x[c];
+        const double xi1 = s, xi2 = t * (1 - s), xi3 = v * (1 - s) * (1 - t);
+        R.bary.push_back(1.0 - xi1 - xi2 - xi3);
+        R.bary.push_back(xi1);
+        R.bary.push_back(xi2);
+        R.bary.push_back(xi3);
+        R.w.push_back(6.0 * w[a] * w[b] * w[c] * (1 - s) * (1 - s) * (1 - t));
+      }
+  return R;
+}
 
 static Rule default_rule(int d, int degree) {
   Rule R;
@@ -210,12 +266,14 @@ static Rule default_rule(int d, int degree) {
     R.nq = 1;
     R.bary = {0.25, 0.25, 0.25, 0.25};
     R.w = {1.0};
-  } else {
+  } else if (degree == 2) {
     const double a = 0.1381966011250105, b = 0.5854101966249685;
     R.nq = 4;
     for (int q = 0; q < 4; ++q)
       for (int x = 0; x < 4; ++x) R.bary.push_back(x == q ? b : a);
     R.w = {0.25, 0.25, 0.25, 0.25};
+  } else {
+    R = collapsed_gauss_tet(degree);
   }
   return R;
 }
@@ -410,6 +468,20 @@ int oracle_build(int dim, int64_t n_vertices, const double* coords, int64_t n_ce
 }
 
 void oracle_free(void* h) { delete static_cast<OTensor*>(h); }
+
+// The default rule the element loop takes for (dim, integrand degree): returns the number of
+// points and, if the buffers are non-NULL (capacity `cap` points), its barycentric points and
+// weights.  Exported so tests can pin every rule by monomial exactness.
+int oracle_rule(int dim, int degree, int cap, double* bary, double* w) {
+  if (dim < 1 || dim > 3) return -1;
+  Rule R = default_rule(dim, degree);
+  if (bary && w) {
+    if (R.nq > cap) return -2;
+    std::copy(R.bary.begin(), R.bary.end(), bary);
+    std::copy(R.w.begin(), R.w.end(), w);
+  }
+  return R.nq;
+}
 
 void oracle_sizes(const void* h, int64_t* nnz, int64_t* nnz_csr, int64_t* n_u, int64_t* n_f) {
   const OTensor* T = static_cast<const OTensor*>(h);

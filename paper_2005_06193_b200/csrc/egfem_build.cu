@@ -357,6 +357,26 @@ void default_rule(int d, int degree, int* nq, double* bary, double* wq) {
     *nq = 1;
     for (int a = 0; a < 4; ++a) bary[a] = 0.25;
     wq[0] = 1.0;
+  } else if (degree >= 3) {
+    // Symmetric 14-point rule, degree 5, positive weights: two S31 orbits (1−3a, a, a, a) and
+    // one S22 orbit (c, c, ½−c, ½−c).  Constants solved from the |α| ≤ 5 moment equations in
+    // 50-digit arithmetic (scripts/tet14_rule.py); exact for every 3D P1 form (MASS3 is degree 3,
+    // PAPER.md L327).  Callers never ask for degree > 5 in 3D (P2 is 2D only).
+    const double orbit_a[2] = {0.092735250310891226, 0.31088591926330061};
+    const double orbit_w[2] = {0.07349304311636195, 0.11268792571801585};
+    const double c = 0.045503704125649649, wc = 0.042546020777081466;
+    *nq = 14;
+    int q = 0;
+    for (int o = 0; o < 2; ++o)
+      for (int v = 0; v < 4; ++v, ++q) {
+        for (int a = 0; a < 4; ++a) bary[4 * q + a] = (a == v) ? 1.0 - 3.0 * orbit_a[o] : orbit_a[o];
+        wq[q] = orbit_w[o];
+      }
+    for (int x = 0; x < 4; ++x)
+      for (int y = x + 1; y < 4; ++y, ++q) {
+        for (int a = 0; a < 4; ++a) bary[4 * q + a] = (a == x || a == y) ? c : 0.5 - c;
+        wq[q] = wc;
+      }
   } else {
     const double a = 0.1381966011250105, b = 0.5854101966249685;
     *nq = 4;

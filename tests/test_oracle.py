@@ -184,7 +184,7 @@ def test_conv_j_p1_closed_form(oracle_mod):
 # ----------------------------------------------------------------------------- brute force (exact integration)
 @pytest.mark.parametrize("case", ["conv_k_1d", "conv_j_p1", "conv_i_p1", "plap_2d", "plap_3d", "mass3_p1p1p2",
                                   "mass3_p1p1p1", "conv_j_p1_jitter", "plap_2d_jitter", "plap_3d_jitter",
-                                  "mass3_jitter"])
+                                  "mass3_jitter", "mass3_3d", "mass3_3d_jitter", "mass3_3d_p0", "conv_j_3d_jitter"])
 def test_oracle_vs_dense_brute_force(oracle_mod, case):
     """Oracle element loop + canonicalisation vs an independent dense build with exact integration."""
     if case == "conv_k_1d":
@@ -197,13 +197,17 @@ def test_oracle_vs_dense_brute_force(oracle_mod, case):
         m = I.mesh_square(3); form = I.FORM_PLAP
     elif case.startswith("plap_3d"):
         m = I.mesh_cube(2); form = I.FORM_PLAP
+    elif case.startswith("mass3_3d"):  # the trilinear mass M, degree 3 in 3D
+        m = I.mesh_cube(2); form = I.FORM_MASS3
+    elif case == "conv_j_3d_jitter":
+        m = I.mesh_cube(2); form = I.FORM_CONV_J
     elif case.startswith("mass3"):
         m = I.mesh_square(2); form = I.FORM_MASS3
     if case.endswith("jitter"):
         m = jitter(m, 0.2, 7)
     if case != "conv_k_1d":
         V = I.space_p1(m)
-        if case.startswith("plap"):
+        if case.startswith("plap") or case == "mass3_3d_p0":
             W = I.space_p0(m)
         elif case in ("mass3_p1p1p2", "mass3_jitter"):
             W = I.space_p2_square(2)
@@ -221,6 +225,46 @@ def test_oracle_vs_dense_brute_force(oracle_mod, case):
                 for c in W.cell_dofs[K]:
                     trip.add((a, b, c))
     assert T.nnz == len(trip)
+
+
+@pytest.mark.parametrize("dim", [1, 2, 3])
+def test_oracle_rules_monomial_exactness(oracle_mod, dim):
+    """Every default rule the oracle's element loop takes integrates ∫_K λ^α = |K| d! α!/(|α|+d)!
+    exactly for |α| ≤ the degree it is chosen for (2D: ≤ 4, reading C3) (T is an integral), and has
+    positive weights summing to 1.  Pins the 3D degree ≥ 3 collapsed Gauss rule (MASS3, L327)."""
+    import itertools
+    from math import factorial
+    import oracle
+    for degree in range(0, 6):
+        bary, w = oracle.rule(dim, degree)
+        assert np.all(w > 0) and abs(w.sum() - 1) < 4e-15
+        assert np.all(bary >= -1e-15) and np.allclose(bary.sum(axis=1), 1, atol=1e-15)
+        # 1D: 3-point Gauss (degree 5) always; 2D degree ≥ 5 takes the 6-point degree-4 rule by
+        # reading C3 (BJ cfg5 names "6-point quadrature"; DESIGN.md §2)
+        exact_to = 5 if dim == 1 else (min(degree, 4) if dim == 2 else degree)
+        for al in itertools.product(range(exact_to + 1), repeat=dim + 1):
+            if sum(al) > exact_to:
+                continue
+            exact = factorial(dim) * np.prod([factorial(a) for a in al]) / factorial(sum(al) + dim)
+            got = float(np.sum(w * np.prod(bary ** np.array(al), axis=1)))
+            assert abs(got - exact) <= 4e-15 * max(1.0, exact), (dim, degree, al, got, exact)
+
+
+def test_tet_mass3_single_cell_closed_form(oracle_mod):
+    """One Kuhn tet: M_abc = ∫ λ_a λ_b λ_c = |K|·3!·Π(mult)!/6!, i.e. |K|/20 (a=b=c), |K|/60 (two equal),
+    |K|/120 (distinct) — the exact trilinear mass of PAPER.md L327 (the round-1 4-point rule gave 0.00905|K|)."""
+    x = np.array([[0, 0, 0], [1, 0, 0], [1, 1, 0], [1, 1, 1]], float)
+    m = I.Mesh(3, x, np.array([[0, 1, 2, 3]], np.int32))
+    V = I.space_p1(m)
+    T = oracle_mod.OracleTensor(m, V, V, I.FORM_MASS3)
+    D = dense(T)
+    vol = 1.0 / 6
+    for a in range(4):
+        for b in range(4):
+            for c in range(4):
+                n = len({a, b, c})
+                want = vol / (20 if n == 1 else 60 if n == 2 else 120)
+                assert abs(D[a, b, c] - want) <= 4e-15 * want, (a, b, c, D[a, b, c], want)
 
 
 def test_p2_six_point_rule_brute_force(oracle_mod):
