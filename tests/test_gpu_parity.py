@@ -132,6 +132,9 @@ def test_cfg4_full_size_sampled_rows(eg, orc, dtype):
     t = eg.egfem_tensor_build(pr.mesh, pr.V, pr.W, pr.form, dtype=dtype, device=0)
     assert (t.nnz, t.nnz_csr) == (201326592, 31802497)
     g = gpu_pass(eg, t, pr, pr.u, fused=True)
+    # the separate entry points too: egfem_apply (the apply-only kernel) and the separate
+    # Newton egfem_jacobian, at full size in the same launch configuration
+    gs = gpu_pass(eg, t, pr, pr.u, fused=False)
     ex = t.export(loc=True)
     tol = FP64_TOL if dtype == 0 else FP32_TOL
     o_full = orc.OracleTensor(pr.mesh, pr.V, pr.W, pr.form, rows=(0, 1))
@@ -148,9 +151,12 @@ def test_cfg4_full_size_sampled_rows(eg, orc, dtype):
         ca, cb = ex["csr_row_ptr"][r0], ex["csr_row_ptr"][r1]
         assert np.array_equal(ex["csr_col"][ca:cb], oex["csr_col"])
         ref_r = o.apply(pr.u, ow)[r0:r1]
-        assert rel_l2(g["r"][r0:r1], ref_r) <= tol
-        assert rel_l2(g["A"][ca:cb], o.jacobian(0, pr.interp, pr.p, pr.u, ow)) <= tol
-        assert rel_l2(g["J"][ca:cb], o.jacobian(1, pr.interp, pr.p, pr.u, ow)) <= tol
+        ref_A = o.jacobian(0, pr.interp, pr.p, pr.u, ow)
+        ref_J = o.jacobian(1, pr.interp, pr.p, pr.u, ow)
+        for gg in (g, gs):
+            assert rel_l2(gg["r"][r0:r1], ref_r) <= tol
+            assert rel_l2(gg["A"][ca:cb], ref_A) <= tol
+            assert rel_l2(gg["J"][ca:cb], ref_J) <= tol
     del t
     torch.cuda.empty_cache()
 
@@ -248,7 +254,9 @@ def test_batched_small(eg, orc, layout, B):
 
 
 def test_cfg5_full_size_batched_sampled_pairs(eg, orc):
-    """cfg5 at BASELINE size, B = 256 node-major (the bench launch): pairs 0, 77, 255 whole."""
+    """cfg5 at BASELINE size, B = 256 node-major (the bench launch): pairs 0, 77, 255 whole, and
+    ALL 256 pairs (every pair chunk of the kernel) on the first / middle / last 3000-row blocks,
+    each against a row-restricted oracle build (r is defined row by row)."""
     import torch
     pr = I.make_problem("cfg5")
     t = eg.egfem_tensor_build(pr.mesh, pr.V, pr.W, pr.form, device=0)
@@ -259,6 +267,12 @@ def test_cfg5_full_size_batched_sampled_pairs(eg, orc):
     Rh = R.cpu().numpy()
     for p in (0, 77, 255):
         assert rel_l2(Rh[:, p], o.apply(pr.u[p], pr.u[p])) <= FP64_TOL
+    del o
+    for r0, r1 in _row_blocks(t.n_u, 3000):
+        ob = orc.OracleTensor(pr.mesh, pr.V, pr.W, pr.form, rows=(r0, r1))
+        Rb = ob.apply_batched(pr.u, pr.u)[:, r0:r1]  # (256, rows)
+        for p in range(256):
+            assert rel_l2(Rh[r0:r1, p], Rb[p]) <= FP64_TOL, (r0, p)
 
 
 def test_interp_kinds(eg, orc):
