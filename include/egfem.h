@@ -310,6 +310,25 @@ egfem_status egfem_halo_pack(const egfem_tensor* local, const int32_t* d_idx, in
 egfem_status egfem_halo_unpack(const egfem_tensor* local, const int32_t* d_idx, int64_t n,
                                const void* recv_buf, void* u_local, egfem_stream_t stream);
 
+/* Name of the kernel family `entry` dispatches to for this handle (0 = egfem_apply,
+ * 1 = egfem_jacobian, 2 = egfem_apply_jacobian with (mode, kind, p), 3 = egfem_apply_batched
+ * NODE_MAJOR), written NUL-terminated into the host buffer buf[len] (truncated if short).
+ * Used by bench.py to name the kernel its roofline line measures.  No launch.
+ * INVALID_ARGUMENT on NULL t/buf, len = 0 or a bad entry; the Jacobian checks of
+ * egfem_jacobian (without the pointer checks) for entries 1 and 2. */
+egfem_status egfem_kernel_name(const egfem_tensor* t, int32_t entry, egfem_jac_mode mode, egfem_interp_kind kind,
+                               double p, char* buf, size_t len);
+
+/* Diagnostic, no GPU needed: generates the compiled row-group kernel of the batched action
+ * (egfem_group.cu) for one group pattern and compiles it with NVRTC for
+ * sm_100a.  key[key_len] (host int32) serializes the pattern: n (stencil width), g (member
+ * rows), then per member its fiber count and per fiber (a, count, b_1..b_count) — positions
+ * in the n-point group stencil.  pairs_per_lane ∈ [1, 4]; fp64 if f64 else fp32.
+ * EGFEM_OK when it compiles; INVALID_ARGUMENT for a malformed key; CUDA (detail in
+ * egfem_last_error) when NVRTC fails.  EGFEM_GROUP_DUMP=<prefix> also writes the source and
+ * the CUBIN. */
+egfem_status egfem_group_compile(const int32_t* key, int32_t key_len, int32_t pairs_per_lane, int32_t f64);
+
 /* Number of CUDA kernels this library launched (process-wide, all threads); used
  * by bench.py to report gpu_launches. */
 uint64_t egfem_launch_count(void);

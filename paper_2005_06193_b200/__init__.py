@@ -42,7 +42,7 @@ EXPORTS = ("egfem_tensor_build", "egfem_tensor_from_coo", "egfem_tensor_destroy"
            "egfem_partition_rows", "egfem_halo_pack", "egfem_halo_unpack", "egfem_launch_count",
            "egfem_status_string", "egfem_last_error", "egfem_bilinear_build", "egfem_csr_spmv",
            "egfem_bilinear_jacobian", "egfem_interior", "egfem_interp_range", "egfem_apply_jacobian_rows",
-           "egfem_interior_rows")
+           "egfem_interior_rows", "egfem_kernel_name", "egfem_group_compile")
 
 
 class EgfemError(RuntimeError):
@@ -93,6 +93,8 @@ def _load():
         "egfem_interp_range": [P, st, ctypes.c_double, P, P, P, i64, i64, P],
         "egfem_apply_jacobian_rows": [P, st, st, ctypes.c_double, P, P, P, P, P, i64, i64, P],
         "egfem_interior_rows": [i64, P, P, i64, i64, P, P],
+        "egfem_kernel_name": [P, i32, st, st, ctypes.c_double, ctypes.c_char_p, ctypes.c_size_t],
+        "egfem_group_compile": [P, i32, i32, i32],
     }
     for name, args in sig.items():
         f = getattr(L, name)
@@ -122,19 +124,48 @@ def _np_ptr(a):
 
 
 def _dptr(x):
-    """Device pointer of a torch tensor (None -> NULL)."""
+    """Device pointer of a torch tensor (None -> NULL), unchecked (index buffers)."""
     if x is None:
         return None
     return ctypes.c_void_p(x.data_ptr())
 
 
-def _stream(stream):
+def _buf(t, x, n, name, required=True):
+    """Device pointer of a caller buffer after the checks the C ABI cannot make:
+    a torch tensor on the handle's CUDA device, of the handle's dtype, contiguous, with at
+    least `n` elements.  A failed check raises EgfemError(EGFEM_ERR_INVALID_ARGUMENT) before
+    anything is launched, like the library's own validation.  None -> NULL (the library
+    reports a missing required pointer itself)."""
+    if x is None:
+        return None
+    bad = None
+    if not x.is_cuda or x.device.index != t.device:
+        bad = f"{name} must be on cuda:{t.device}, got {x.device}"
+    elif x.dtype != t.torch_dtype:
+        bad = f"{name} must be {t.torch_dtype}, got {x.dtype}"
+    elif not x.is_contiguous():
+        bad = f"{name} must be contiguous"
+    elif x.numel() < n:
+        bad = f"{name} has {x.numel()} elements, needs {n}"
+    if bad:
+        raise EgfemError("binding", 1, bad)
+    return ctypes.c_void_p(x.data_ptr())
+
+
+def _stream(stream, t=None):
+    """The stream handle: a torch.cuda.Stream, a raw cudaStream_t int, or None = the current
+    stream of the handle's device."""
     if stream is None:
         import torch
-        return ctypes.c_void_p(torch.cuda.current_stream().cuda_stream)
+        dev = torch.device("cuda", t.device) if t is not None else None
+        return ctypes.c_void_p(torch.cuda.current_stream(dev).cuda_stream)
     if isinstance(stream, int):
         return ctypes.c_void_p(stream)
     return ctypes.c_void_p(stream.cuda_stream)
+
+
+def _chain_len(t):
+    return t.n_f * (t.dim + 1)
 
 
 def launch_count() -> int:
@@ -226,56 +257,72 @@ def egfem_tensor_from_coo(n_u, n_f, i, j, k, val, dtype=F64, device=0) -> Tensor
 
 def egfem_interp(t: Tensor, kind, p, u, w, chain=None, stream=None):
     """Step (1): w = f(Π_u u, Π_∇u ·₂ u)."""
-    _check("egfem_interp", _lib.egfem_interp(t.h, kind, float(p), _dptr(u), _dptr(w), _dptr(chain), _stream(stream)))
+    _check("egfem_interp", _lib.egfem_interp(t.h, kind, float(p), _buf(t, u, t.n_u, "u"), _buf(t, w, t.n_f, "w"),
+                                             _buf(t, chain, _chain_len(t), "chain", False), _stream(stream, t)))
 
 
 def egfem_apply(t: Tensor, u, w, r, stream=None):
     """Step (2): r = T:(u⊗w)."""
-    _check("egfem_apply", _lib.egfem_apply(t.h, _dptr(u), _dptr(w), _dptr(r), _stream(stream)))
+    _check("egfem_apply", _lib.egfem_apply(t.h, _buf(t, u, t.n_u, "u"), _buf(t, w, t.n_f, "w"), _buf(t, r, t.n_u, "r"),
+                                           _stream(stream, t)))
 
 
 def egfem_apply_batched(t: Tensor, batch, layout, U, W, R, stream=None):
-    _check("egfem_apply_batched", _lib.egfem_apply_batched(t.h, int(batch), layout, _dptr(U), _dptr(W), _dptr(R),
-                                                           _stream(stream)))
+    B = int(batch)
+    _check("egfem_apply_batched", _lib.egfem_apply_batched(t.h, B, layout, _buf(t, U, B * t.n_u, "U"),
+                                                           _buf(t, W, B * t.n_f, "W"), _buf(t, R, B * t.n_u, "R"),
+                                                           _stream(stream, t)))
 
 
 def egfem_jacobian(t: Tensor, mode, kind, p, u, w, chain, csr_vals, stream=None):
     """Step (3): A = T·w or J = T·w + (T·₂u)·D_u w into the CSR values."""
-    _check("egfem_jacobian", _lib.egfem_jacobian(t.h, mode, kind, float(p), _dptr(u), _dptr(w), _dptr(chain),
-                                                 _dptr(csr_vals), _stream(stream)))
+    _check("egfem_jacobian", _lib.egfem_jacobian(t.h, mode, kind, float(p), _buf(t, u, t.n_u, "u", False),
+                                                 _buf(t, w, t.n_f, "w"), _buf(t, chain, _chain_len(t), "chain", False),
+                                                 _buf(t, csr_vals, t.nnz_csr, "csr_vals"), _stream(stream, t)))
 
 
 def egfem_bilinear_build(t: Tensor, b_vals, stream=None):
     """F3: the bilinear GFEM matrix B = T·₂1 on the CSR pattern (W = V)."""
-    _check("egfem_bilinear_build", _lib.egfem_bilinear_build(t.h, _dptr(b_vals), _stream(stream)))
+    _check("egfem_bilinear_build", _lib.egfem_bilinear_build(t.h, _buf(t, b_vals, t.nnz_csr, "b_vals"),
+                                                             _stream(stream, t)))
 
 
 def egfem_csr_spmv(t: Tensor, vals, x, y, stream=None):
     """y = A x for values on the tensor's CSR pattern (the GFEM action r = B f)."""
-    _check("egfem_csr_spmv", _lib.egfem_csr_spmv(t.h, _dptr(vals), _dptr(x), _dptr(y), _stream(stream)))
+    _check("egfem_csr_spmv", _lib.egfem_csr_spmv(t.h, _buf(t, vals, t.nnz_csr, "vals"), _buf(t, x, t.n_u, "x"),
+                                                 _buf(t, y, t.n_u, "y"), _stream(stream, t)))
 
 
 def egfem_bilinear_jacobian(t: Tensor, b_vals, kind, p, u, csr_vals, stream=None):
     """J = B·diag(f'(u)) for the GFEM term r = B f(u) (W = V)."""
-    _check("egfem_bilinear_jacobian", _lib.egfem_bilinear_jacobian(t.h, _dptr(b_vals), kind, float(p), _dptr(u),
-                                                                   _dptr(csr_vals), _stream(stream)))
+    _check("egfem_bilinear_jacobian", _lib.egfem_bilinear_jacobian(t.h, _buf(t, b_vals, t.nnz_csr, "b_vals"), kind,
+                                                                   float(p), _buf(t, u, t.n_u, "u"),
+                                                                   _buf(t, csr_vals, t.nnz_csr, "csr_vals"),
+                                                                   _stream(stream, t)))
 
 
 def egfem_apply_jacobian(t: Tensor, mode, kind, p, u, w, chain, r, csr_vals, stream=None):
-    _check("egfem_apply_jacobian", _lib.egfem_apply_jacobian(t.h, mode, kind, float(p), _dptr(u), _dptr(w),
-                                                             _dptr(chain), _dptr(r), _dptr(csr_vals),
-                                                             _stream(stream)))
+    _check("egfem_apply_jacobian", _lib.egfem_apply_jacobian(t.h, mode, kind, float(p), _buf(t, u, t.n_u, "u"),
+                                                             _buf(t, w, t.n_f, "w"),
+                                                             _buf(t, chain, _chain_len(t), "chain", False),
+                                                             _buf(t, r, t.n_u, "r"),
+                                                             _buf(t, csr_vals, t.nnz_csr, "csr_vals"),
+                                                             _stream(stream, t)))
 
 
 def egfem_interp_range(t: Tensor, kind, p, u, w, chain, lo, hi, stream=None):
-    _check("egfem_interp_range", _lib.egfem_interp_range(t.h, kind, float(p), _dptr(u), _dptr(w), _dptr(chain),
-                                                         int(lo), int(hi), _stream(stream)))
+    _check("egfem_interp_range", _lib.egfem_interp_range(t.h, kind, float(p), _buf(t, u, t.n_u, "u"),
+                                                         _buf(t, w, t.n_f, "w"),
+                                                         _buf(t, chain, _chain_len(t), "chain", False),
+                                                         int(lo), int(hi), _stream(stream, t)))
 
 
 def egfem_apply_jacobian_rows(t: Tensor, mode, kind, p, u, w, chain, r, csr_vals, row_lo, row_hi, stream=None):
     _check("egfem_apply_jacobian_rows",
-           _lib.egfem_apply_jacobian_rows(t.h, mode, kind, float(p), _dptr(u), _dptr(w), _dptr(chain), _dptr(r),
-                                          _dptr(csr_vals), int(row_lo), int(row_hi), _stream(stream)))
+           _lib.egfem_apply_jacobian_rows(t.h, mode, kind, float(p), _buf(t, u, t.n_u, "u"), _buf(t, w, t.n_f, "w"),
+                                          _buf(t, chain, _chain_len(t), "chain", False), _buf(t, r, t.n_u, "r"),
+                                          _buf(t, csr_vals, t.nnz_csr, "csr_vals"), int(row_lo), int(row_hi),
+                                          _stream(stream, t)))
 
 
 def egfem_interior(t: Tensor):
@@ -316,10 +363,25 @@ def egfem_partition(t: Tensor, nranks, rank, device=None):
 
 
 def egfem_halo_pack(t: Tensor, idx, u_local, send_buf, stream=None):
-    _check("egfem_halo_pack", _lib.egfem_halo_pack(t.h, _dptr(idx), idx.numel(), _dptr(u_local), _dptr(send_buf),
-                                                   _stream(stream)))
+    _check("egfem_halo_pack", _lib.egfem_halo_pack(t.h, _dptr(idx), idx.numel(), _buf(t, u_local, 0, "u_local"),
+                                                   _buf(t, send_buf, idx.numel(), "send_buf"), _stream(stream, t)))
 
 
 def egfem_halo_unpack(t: Tensor, idx, recv_buf, u_local, stream=None):
-    _check("egfem_halo_unpack", _lib.egfem_halo_unpack(t.h, _dptr(idx), idx.numel(), _dptr(recv_buf),
-                                                       _dptr(u_local), _stream(stream)))
+    _check("egfem_halo_unpack", _lib.egfem_halo_unpack(t.h, _dptr(idx), idx.numel(),
+                                                       _buf(t, recv_buf, idx.numel(), "recv_buf"),
+                                                       _buf(t, u_local, 0, "u_local"), _stream(stream, t)))
+
+
+def egfem_kernel_name(t: Tensor, entry, mode=JAC_NEWTON, kind=INTERP_IDENTITY, p=0.0) -> str:
+    """Kernel family an entry point runs for this handle (0 apply, 1 jacobian, 2 apply_jacobian,
+    3 apply_batched node-major); bench.py names its roofline kernel with it."""
+    buf = ctypes.create_string_buffer(512)
+    _check("egfem_kernel_name", _lib.egfem_kernel_name(t.h, int(entry), mode, kind, float(p), buf, 512))
+    return buf.value.decode()
+
+
+def egfem_group_compile(key, pairs_per_lane=2, f64=True):
+    """NVRTC-compile the generated row-group kernel of one pattern (serialized key; no GPU needed)."""
+    k = np.ascontiguousarray(key, np.int32)
+    _check("egfem_group_compile", _lib.egfem_group_compile(_np_ptr(k), len(k), int(pairs_per_lane), int(bool(f64))))

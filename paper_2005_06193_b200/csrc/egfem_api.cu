@@ -3,6 +3,7 @@
 #include <algorithm>
 #include <cmath>
 #include <atomic>
+#include <cstdio>
 #include <cstring>
 #include <numeric>
 #include <string>
@@ -387,19 +388,19 @@ egfem_status egfem_apply_batched(const egfem_tensor* t, int32_t batch, egfem_lay
 }
 
 static egfem_status jac_mode_code(const egfem_tensor* t, egfem_jac_mode mode, egfem_interp_kind kind, double p,
-                                  const void* u, const void* chain, int* code) {
+                                  const void* u, const void* chain, int* code, bool check_ptrs = true) {
   if (mode == EGFEM_JAC_PICARD) {
     *code = 1;
     return EGFEM_OK;
   }
   if (mode != EGFEM_JAC_NEWTON) return fail(EGFEM_ERR_INVALID_ARGUMENT, "bad Jacobian mode");
   egfem_status st;
-  if ((st = check_dev_ptr(t, u, "u", true))) return st;
+  if (check_ptrs && (st = check_dev_ptr(t, u, "u", true))) return st;
   switch (kind) {
     case EGFEM_INTERP_IDENTITY:
     case EGFEM_INTERP_SQUARE:
       if (kind == EGFEM_INTERP_SQUARE && t->wfam == EGFEM_QUAD && t->vfam == EGFEM_P1) {
-        if ((st = check_dev_ptr(t, chain, "chain", true))) return st;
+        if (check_ptrs && (st = check_dev_ptr(t, chain, "chain", true))) return st;
         *code = 3;
         return EGFEM_OK;
       }
@@ -414,7 +415,7 @@ static egfem_status jac_mode_code(const egfem_tensor* t, egfem_jac_mode mode, eg
         return fail(EGFEM_ERR_UNSUPPORTED, "P0-W Newton needs V = P1, W = P0");
       if (kind == EGFEM_INTERP_GRADPOW_P0 && !(p > 1.0))
         return fail(EGFEM_ERR_INVALID_ARGUMENT, "GRADPOW_P0 needs p > 1");
-      if ((st = check_dev_ptr(t, chain, "chain", true))) return st;
+      if (check_ptrs && (st = check_dev_ptr(t, chain, "chain", true))) return st;
       *code = 3;
       return EGFEM_OK;
     case EGFEM_INTERP_RECIPROCAL:
@@ -426,7 +427,7 @@ static egfem_status jac_mode_code(const egfem_tensor* t, egfem_jac_mode mode, eg
       }
       if (!t->has_mesh || !t->w_p0 || t->vfam != EGFEM_P1)
         return fail(EGFEM_ERR_UNSUPPORTED, "RECIPROCAL Newton needs W = V, or V = P1 and W = P0");
-      if ((st = check_dev_ptr(t, chain, "chain", true))) return st;
+      if (check_ptrs && (st = check_dev_ptr(t, chain, "chain", true))) return st;
       *code = 3;
       return EGFEM_OK;
     case EGFEM_INTERP_P1_TO_P2_SQUARE:
@@ -434,6 +435,28 @@ static egfem_status jac_mode_code(const egfem_tensor* t, egfem_jac_mode mode, eg
     default:
       return fail(EGFEM_ERR_INVALID_ARGUMENT, "bad interp kind");
   }
+}
+
+egfem_status egfem_kernel_name(const egfem_tensor* t, int32_t entry, egfem_jac_mode mode, egfem_interp_kind kind,
+                               double p, char* buf, size_t len) {
+  if (!t || !buf || len == 0) return fail(EGFEM_ERR_INVALID_ARGUMENT, "tensor or buffer is NULL");
+  int code = 0;
+  egfem_status st;
+  if (entry == 1 || entry == 2)
+    if ((st = jac_mode_code(t, mode, kind, p, nullptr, nullptr, &code, false))) return st;
+  if (entry < 0 || entry > 3) return fail(EGFEM_ERR_INVALID_ARGUMENT, "entry must be 0..3");
+  const std::string name = dispatch_name(t, entry, code);
+  std::snprintf(buf, len, "%s", name.c_str());
+  return EGFEM_OK;
+}
+
+egfem_status egfem_group_compile(const int32_t* key, int32_t key_len, int32_t pairs_per_lane, int32_t f64) {
+  if (!key || key_len < 2 || pairs_per_lane < 1 || pairs_per_lane > 4)
+    return fail(EGFEM_ERR_INVALID_ARGUMENT, "group pattern key missing or pairs_per_lane out of [1, 4]");
+  std::string log;
+  egfem_status st = group_compile_key(key, key_len, pairs_per_lane, f64, &log);
+  if (st == EGFEM_ERR_INVALID_ARGUMENT) return fail(st, "malformed group pattern key");
+  return st;
 }
 
 egfem_status egfem_jacobian(const egfem_tensor* t, egfem_jac_mode mode, egfem_interp_kind kind, double p,
@@ -806,6 +829,8 @@ egfem_status egfem_partition(const egfem_tensor* G, int32_t nranks, int32_t rank
     if ((st = make_wv_aux(t))) return bail(st);
     if ((st = make_p0_cells(t))) return bail(st);
     if ((st = make_dense_blocks(t, lrf))) return bail(st);
+    // no compiled row groups on a partitioned handle: its columns are window indices, not rows
+    // (the batched action shards the batch, never the rows — DESIGN.md §8)
   }
   if (row_begin) *row_begin = rb;
   if (row_end) *row_end = re;

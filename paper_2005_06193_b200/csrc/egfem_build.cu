@@ -802,6 +802,7 @@ egfem_status build_from_triples(egfem_tensor* t, int64_t m, uint64_t* d_key_ij, 
   if ((st = make_wv_aux(t))) return st;
   if ((st = make_p0_cells(t))) return st;
   if ((st = make_dense_blocks(t, hrf))) return st;
+  if ((st = make_groups(t, hrf))) return st;
   EGFEM_CUDA_TRY(cudaDeviceSynchronize());
   return EGFEM_OK;
 }
@@ -933,6 +934,8 @@ void free_tensor(egfem_tensor* t) {
                   t->tile_row, t->tile_fib, t->tile_nz, t->coords, t->coords4, t->coordsf, t->cells, t->vdofs, t->wdofs, t->wcell, t->wpts};
   for (void* p : ptrs)
     if (p) cudaFree(p);
+  free_group_plan(t->grp);
+  t->grp = nullptr;
 }
 
 }  // namespace egfem

@@ -206,6 +206,35 @@ __global__ void __launch_bounds__(128) k_dense(const DenseArgs<S> A, const int32
   }
 }
 
+// Rows outside the compiled group classes (egfem_group.cu): one warp per (row, 64-pair chunk)
+// over an explicit row list of one stencil width, blocks read in place through blk_off.
+template <typename S, int N>
+__global__ void __launch_bounds__(128) k_dense_list(const DenseArgs<S> A, const int32_t* __restrict__ rows,
+                                                   int64_t count) {
+  constexpr int PPT = DensePPT<N>::value;
+  constexpr int NP = N + (N & 1);
+  const int lane = threadIdx.x & 31;
+  const int nch = (A.B + 32 * PPT - 1) / (32 * PPT);
+  const int64_t nitem = count * nch;
+  const int64_t ws = (int64_t)gridDim.x * (blockDim.x >> 5);
+  for (int64_t it = (int64_t)blockIdx.x * (blockDim.x >> 5) + (threadIdx.x >> 5); it < nitem; it += ws) {
+    const int64_t q = it / nch;
+    const int p0 = (int)(it - q * nch) * 32 * PPT + lane;
+    const int64_t row = __ldg(rows + q);
+    if constexpr (N == 0) {
+      for (int x = 0; x < PPT; ++x)
+        if (p0 + 32 * x < A.B) A.R[at<true>(row, p0 + 32 * x, A.B, A.n_u)] = S(0);
+    } else {
+      const int32_t* cols = A.fib_j + __ldg(A.row_fib + row);
+      const S* M = A.blk + __ldg(A.blk_off + row);
+      S wa[PPT][N];
+      load_w<S, N, true, PPT>(A, cols, p0, wa);
+      dense_row<S, N, true, PPT>(A, row, cols, M, p0, wa);
+    }
+    (void)NP;
+  }
+}
+
 // ------------------------------------------------------------------ single-vector W = V path
 // Steps (2)+(3) for W = V tensors from the same dense blocks:
 //   X_a = Σ_b M_i[a][b] w_{N_b}            Picard value of CSR slot (i, N_a)   (T·w)
@@ -471,6 +500,45 @@ egfem_status launch_dense(const egfem_tensor* t, int32_t batch, egfem_layout lay
     }
 #undef EGFEM_DALL
 #undef EGFEM_DN
+    count_launch();
+  }
+  EGFEM_CUDA_TRY(cudaGetLastError());
+  return EGFEM_OK;
+}
+
+egfem_status launch_dense_rows(const egfem_tensor* t, int32_t batch, const int32_t* rows,
+                               const std::vector<std::array<int64_t, 3>>& classes, const void* U, const void* W,
+                               void* R, cudaStream_t s) {
+  const int dev = t->device & 63;
+  if (!g_sms_dense[dev])
+    EGFEM_CUDA_TRY(cudaDeviceGetAttribute(&g_sms_dense[dev], cudaDevAttrMultiProcessorCount, t->device));
+  for (const auto& cls : classes) {
+    const int n = (int)cls[0];
+    const int64_t start = cls[1], count = cls[2];
+    const int nch = (batch + 63) / 64;
+    const int64_t ctas = std::max<int64_t>(1, std::min<int64_t>((count * nch + 3) / 4, (int64_t)g_sms_dense[dev] * 16));
+#define EGFEM_DL(S_, N_)                                                                                  \
+  case N_: {                                                                                             \
+    DenseArgs<S_> A{t->n_u, t->n_f, batch, t->row_fib, t->fib_j, t->blk_off, (const S_*)t->blk,         \
+                    (const S_*)U, (const S_*)W, (S_*)R};                                                 \
+    k_dense_list<S_, N_><<<(unsigned)ctas, 128, 0, s>>>(A, rows + start, count);                         \
+    break;                                                                                               \
+  }
+#define EGFEM_DLALL(S_)                                                                                   \
+  switch (n) {                                                                                           \
+    EGFEM_DL(S_, 0) EGFEM_DL(S_, 1) EGFEM_DL(S_, 2) EGFEM_DL(S_, 3) EGFEM_DL(S_, 4) EGFEM_DL(S_, 5)     \
+    EGFEM_DL(S_, 6) EGFEM_DL(S_, 7) EGFEM_DL(S_, 8) EGFEM_DL(S_, 9) EGFEM_DL(S_, 10) EGFEM_DL(S_, 11)   \
+    EGFEM_DL(S_, 12) EGFEM_DL(S_, 13) EGFEM_DL(S_, 14) EGFEM_DL(S_, 15) EGFEM_DL(S_, 16) EGFEM_DL(S_, 17) \
+    EGFEM_DL(S_, 18) EGFEM_DL(S_, 19) EGFEM_DL(S_, 20)                                                   \
+    default: set_error("dense stencil wider than 20"); return EGFEM_ERR_UNSUPPORTED;                    \
+  }
+    if (t->dtype == EGFEM_F64) {
+      EGFEM_DLALL(double)
+    } else {
+      EGFEM_DLALL(float)
+    }
+#undef EGFEM_DLALL
+#undef EGFEM_DL
     count_launch();
   }
   EGFEM_CUDA_TRY(cudaGetLastError());

@@ -24,6 +24,7 @@
 #include "egfem.h"
 
 namespace egfem {
+struct GroupPlan;  // egfem_group.cu: compiled row-group kernels of the batched action
 
 constexpr int kTileNnz = 1024;   // max nonzeros per tile
 constexpr int kTileFib = 512;    // max fibers per tile
@@ -79,6 +80,7 @@ struct egfem_tensor {
   void* blk = nullptr;          // dtype: M_i[a][b] = T_{i, N_a, N_b}
   int32_t* dense_rows = nullptr;  // n_u: rows grouped by stencil width |N(i)| (row order within a width)
   std::vector<std::array<int64_t, 4>> dense_classes;  // host: (width, first entry in dense_rows, count, first block value)
+  egfem::GroupPlan* grp = nullptr;  // W = V batched action: row groups with compiled-in patterns (egfem_group.cu)
 
   // tiles (device + host copy of the count)
   int32_t n_tiles = 0;
@@ -141,6 +143,20 @@ egfem_status launch_dense1(const egfem_tensor* t, int64_t lo, int64_t hi, bool d
 egfem_status launch_dense(const egfem_tensor* t, int32_t batch, egfem_layout layout, const void* U, const void* W,
                           void* R, cudaStream_t s);
 egfem_status make_dense_blocks(egfem_tensor* t, const std::vector<int64_t>& hrf);
+egfem_status launch_dense_rows(const egfem_tensor* t, int32_t batch, const int32_t* rows,
+                               const std::vector<std::array<int64_t, 3>>& classes, const void* U, const void* W,
+                               void* R, cudaStream_t s);
+// grouped batched action with compiled patterns (egfem_group.cu)
+egfem_status make_groups(egfem_tensor* t, const std::vector<int64_t>& hrf);
+void free_group_plan(GroupPlan* gp);
+bool group_path_ok(const egfem_tensor* t, egfem_layout layout);
+egfem_status launch_groups(const egfem_tensor* t, int32_t batch, const void* U, const void* W, void* R,
+                           cudaStream_t s);
+const char* group_plan_info(const egfem_tensor* t);
+egfem_status group_compile_key(const int32_t* key, int32_t len, int P, int f64, std::string* log);
+// the kernel family an entry point dispatches to (0 apply, 1 jacobian, 2 apply_jacobian,
+// 3 apply_batched node-major; jac = the Jacobian mode code)
+std::string dispatch_name(const egfem_tensor* t, int entry, int jac);
 egfem_status launch_spmv(const egfem_tensor* t, const void* vals, const void* x, void* y, cudaStream_t s);
 egfem_status launch_scale_cols(const egfem_tensor* t, const void* b, int mode, double p, const void* u, void* J,
                                cudaStream_t s);

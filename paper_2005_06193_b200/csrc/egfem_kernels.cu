@@ -944,6 +944,24 @@ egfem_status launch_tile(const egfem_tensor* t, bool do_r, int jac, egfem_interp
   return tile_dispatch<float>(t, do_r, jac, kind, p, u, w, chain, r, csr_vals, s);
 }
 
+std::string dispatch_name(const egfem_tensor* t, int entry, int jac) {
+  if (entry == 3) {
+    static const char* forceb = getenv("EGFEM_BATCHED");
+    const bool fc = forceb && forceb[0] == 'c', fd = forceb && forceb[0] == 'd';
+    if (group_path_ok(t, EGFEM_LAYOUT_NODE_MAJOR) && !fc && !fd)
+      return std::string("egfem_grp_* (compiled row groups, egfem_group.cu)") + group_plan_info(t);
+    if (dense_path_ok(t) && !fc) return "k_dense (per-row dense blocks, egfem_dense.cu)";
+    return "k_batched (CSF tiles, egfem_kernels.cu)";
+  }
+  static const char* force = getenv("EGFEM_PATH");
+  const bool tile = force && force[0] == 't';
+  const bool rows_only = force && force[0] == 'r';
+  if (!tile && !rows_only && cells_path_ok(t, jac)) return "k_cell (cell-major P0, egfem_cells.cu)";
+  if (!tile && !rows_only && dense1_path_ok(t, jac)) return "k_dense1 (dense single-vector W = V, egfem_dense.cu)";
+  if (!tile && rows_path_ok(t, jac)) return "k_seg (row groups on the CSF, egfem_rows.cu)";
+  return "k_tile (TMA row tiles, egfem_kernels.cu)";
+}
+
 // Rows [lo, hi): a shallow view of the tensor whose row arrays start at row lo (row_nz,
 // row_fib hold absolute nonzero / fiber offsets, so the streams, csr and the fiber data are
 // addressed as in the whole call) and whose diagonal offset moves with it; r is shifted.
@@ -1006,6 +1024,10 @@ egfem_status launch_batched(const egfem_tensor* t, int32_t batch, egfem_layout l
   // dense-local-block kernel (egfem_dense.cu) for W = V stencils; EGFEM_BATCHED=csf forces
   // the CSF tile kernel below
   static const char* force = getenv("EGFEM_BATCHED");
+  // compiled row-group kernels (egfem_group.cu) first; EGFEM_BATCHED=dense forces the per-row
+  // dense-block kernel
+  if (group_path_ok(t, layout) && !(force && (force[0] == 'c' || force[0] == 'd')))
+    return launch_groups(t, batch, U, W, R, s);
   if (dense_path_ok(t) && !(force && force[0] == 'c')) return launch_dense(t, batch, layout, U, W, R, s);
   const bool p0 = t->has_mesh && t->w_p0;
   const bool nm = layout == EGFEM_LAYOUT_NODE_MAJOR;

@@ -130,3 +130,26 @@ def test_interior_rows_band_structure(eg):
     lo, hi = eg.egfem_interior_rows(np.array(rp), np.array(col), own_lo, own_hi)
     assert (lo, hi) == (bw, own_hi - own_lo - bw)
     assert eg.egfem_interior_rows(np.array([0]), np.array([], np.int32), 0, 1) == (0, 0)
+
+
+def synthetic_group_key(n, g):
+    """Pattern key (include/egfem.h egfem_group_compile) of g member rows on an n-point stencil,
+    every member with fibers at every point and k positions (a + b + m) % 3 != 1."""
+    key = [n, g]
+    for m in range(g):
+        key.append(n)
+        for a in range(n):
+            bs = [b for b in range(n) if (a + b + m) % 3 != 1]
+            key += [a, len(bs)] + bs
+    return key
+
+
+@pytest.mark.parametrize("n,g,ppl,f64", [(19, 4, 2, 1), (9, 1, 1, 1), (12, 7, 4, 0), (1, 1, 2, 1)])
+def test_group_kernel_generation_compiles(eg, n, g, ppl, f64):
+    """The batched action's generated row-group kernels (egfem_group.cu) compile with NVRTC for
+    sm_100a (no GPU needed): straight-line code for a synthetic pattern, fp64 and fp32, 1-4 pairs
+    per lane; a malformed key is rejected before compiling."""
+    eg.egfem_group_compile(synthetic_group_key(n, g), ppl, bool(f64))
+    with pytest.raises(eg.EgfemError) as e:
+        eg.egfem_group_compile(synthetic_group_key(n, g)[:-1] + [n + 5], ppl, bool(f64))
+    assert e.value.status == 1
