@@ -60,15 +60,29 @@ struct GroupClass {
   void* vals = nullptr;     // ninst × nv, dtype: T values in FMA program order
   std::vector<int32_t> key; // the pattern (Pattern::key), kept to generate variants on demand
   cudaKernel_t fn[kVariants] = {nullptr, nullptr, nullptr, nullptr};
+  int per_sm[kVariants] = {0, 0, 0, 0};  // resident CTAs per SM (registers), for the persistent grid
+  size_t dyn_set[kVariants] = {0, 0, 0, 0};  // dynamic shared memory the kernel was opted in for
+  int carve_set[kVariants] = {0, 0, 0, 0};
 };
 
 struct GroupPlan {
   int pairs_per_lane = 2;
   int run = 4;  // consecutive instances per CTA run
+  int interleave = 4;  // fiber chains interleaved in the generated code
+  int prefetch = 0;  // unstaged form: 1 = bulk L2 prefetch one CTA round ahead (measured slower on cfg5)
+  bool persistent = false;  // grid = resident CTAs (else up to `cap` CTAs per SM of runs)
+  int cap = 32;
+  int carveout = -1;  // preferred shared-memory carveout in percent (-1: driver default)
+  bool staged = false;    // full variants: W tiles by TMA bulk copies (kernel_source_staged; measured slower on cfg5)
   bool f64 = true;
   std::vector<GroupClass> classes;
   std::vector<cudaLibrary_t> libs;
-  std::mutex mu;  // guards the lazily compiled variants
+  std::mutex mu;  // guards the lazily compiled variants and the side streams
+  // side streams for the small classes and the fallback rows (fork-join around the big class)
+  int side_dev = -1;
+  std::vector<cudaStream_t> side;
+  std::vector<cudaEvent_t> side_done;
+  cudaEvent_t fork = nullptr;
   // rows outside the compiled classes: per stencil width (width, first entry, count)
   int32_t* fb_rows = nullptr;
   std::vector<std::array<int64_t, 3>> fb_classes;
@@ -118,13 +132,67 @@ struct KeyHash {
 inline int cols_stride(int n) { return (n + 3) & ~3; }
 inline int vals_stride(int nnz, int vs) { const int per16 = 16 / vs; return (nnz + per16 - 1) / per16 * per16; }
 
+// Contiguous pair mapping (full variants): lane l owns pairs P·l .. P·l+P-1 of its 32·P chunk,
+// so its values at one node are P consecutive elements: loaded / stored as 16-byte vectors.
+std::string vec_load(const char* S, int P, const std::string& dst, const std::string& ptr) {
+  std::string o;
+  char b[256];
+  const bool dbl = std::strcmp(S, "double") == 0;
+  if (P == 1) {
+    std::snprintf(b, sizeof(b), "const %s %s_0 = __ldg(%s);", S, dst.c_str(), ptr.c_str());
+    return b;
+  }
+  const int per = dbl ? 2 : (P >= 4 ? 4 : 2);  // elements per vector load
+  const char* V = dbl ? "double2" : (per == 4 ? "float4" : "float2");
+  for (int v = 0; v < P / per; ++v) {
+    std::snprintf(b, sizeof(b), "const %s %s_v%d = __ldg(reinterpret_cast<const %s*>(%s) + %d); ", V, dst.c_str(), v, V,
+                  ptr.c_str(), v);
+    o += b;
+    const char* comp[4] = {"x", "y", "z", "w"};
+    for (int e = 0; e < per; ++e) {
+      std::snprintf(b, sizeof(b), "const %s %s_%d = %s_v%d.%s; ", S, dst.c_str(), v * per + e, dst.c_str(), v, comp[e]);
+      o += b;
+    }
+  }
+  return o;
+}
+
+std::string vec_store(const char* S, int P, const std::string& ptr, const std::string& src) {
+  std::string o;
+  char b[256];
+  const bool dbl = std::strcmp(S, "double") == 0;
+  if (P == 1) {
+    std::snprintf(b, sizeof(b), "*(%s) = %s_0;", ptr.c_str(), src.c_str());
+    return b;
+  }
+  const int per = dbl ? 2 : (P >= 4 ? 4 : 2);
+  for (int v = 0; v < P / per; ++v) {
+    if (dbl)
+      std::snprintf(b, sizeof(b), "reinterpret_cast<double2*>(%s)[%d] = make_double2(%s_%d, %s_%d); ", ptr.c_str(), v,
+                    src.c_str(), 2 * v, src.c_str(), 2 * v + 1);
+    else if (per == 4)
+      std::snprintf(b, sizeof(b), "reinterpret_cast<float4*>(%s)[%d] = make_float4(%s_%d, %s_%d, %s_%d, %s_%d); ",
+                    ptr.c_str(), v, src.c_str(), 4 * v, src.c_str(), 4 * v + 1, src.c_str(), 4 * v + 2, src.c_str(),
+                    4 * v + 3);
+    else
+      std::snprintf(b, sizeof(b), "reinterpret_cast<float2*>(%s)[%d] = make_float2(%s_%d, %s_%d); ", ptr.c_str(), v,
+                    src.c_str(), 2 * v, src.c_str(), 2 * v + 1);
+    o += b;
+  }
+  return o;
+}
+
+void emit_body(std::string& o, const Pattern& pt, const char* S, int P, bool same, bool full, int IL, int nv,
+               const char* indent, bool contig = false);
+
 // Straight-line kernel source for one pattern class.  P pairs per lane (lane, lane+32, ...).
 // A CTA walks runs of `run` consecutive instances (runs dealt round-robin, so the CTAs in flight
 // cover one moving window of the mesh and consecutive instances of a run share most of their
 // stencil in L1); each instance's column record and value record are staged in shared memory
 // by cp.async one instance ahead (double buffer), and the CTA's warps take its 32·P-pair chunks.
 // same: U == W (u_a is the register w_a); full: batch % (32·P) == 0 (no guards).
-std::string kernel_source(const Pattern& pt, const std::string& name, const char* S, int P, bool same, bool full) {
+std::string kernel_source(const Pattern& pt, const std::string& name, const char* S, int P, bool same, bool full,
+                          int IL) {
   const int n = pt.n, g = (int)pt.members.size();
   const int vs = std::strcmp(S, "double") == 0 ? 8 : 4;
   const int nv = vals_stride(pt.nnz(), vs), ncp = cols_stride(n);
@@ -135,13 +203,212 @@ std::string kernel_source(const Pattern& pt, const std::string& name, const char
     o += buf;
   };
   emit("extern \"C\" __global__ void __launch_bounds__(128) %s(const int* __restrict__ gcols, "
-       "const int* __restrict__ grows, const %s* __restrict__ gvals, long long ninst, int B, int run, "
+       "const int* __restrict__ grows, const %s* __restrict__ gvals, long long ninst, int B, int run, int pf, "
        "const %s* __restrict__ U, const %s* __restrict__ W, %s* __restrict__ R) {\n",
        name.c_str(), S, S, S, S);
   emit("  __shared__ __align__(16) %s s_v[2][%d];\n", S, nv);
   emit("  __shared__ __align__(16) int s_c[2][%d];\n", ncp);
   emit("  const int lane = threadIdx.x & 31, warp = threadIdx.x >> 5, nw = blockDim.x >> 5;\n");
   emit("  const int nch = (B + %d) / %d;\n", 32 * P - 1, 32 * P);
+  emit("  const long long gstride = (long long)gridDim.x * run;\n");
+  emit("  auto gof = [&](int q) { const int r = q / run; return (long long)blockIdx.x * run + r * gstride + (q - r * run); };\n");
+  emit("  auto stage = [&](long long gi, int b) {\n");
+  emit("    if (gi >= ninst) return;\n");
+  emit("    const char* vsrc = reinterpret_cast<const char*>(gvals + gi * %d);\n", nv);
+  emit("    const char* csrc = reinterpret_cast<const char*>(gcols + gi * %d);\n", ncp);
+  emit("    for (int x = threadIdx.x; x < %d; x += blockDim.x) {\n", nv * vs / 16 + ncp / 4);
+  emit("      const bool isv = x < %d;\n", nv * vs / 16);
+  emit("      char* dst = isv ? reinterpret_cast<char*>(s_v[b]) + 16 * x : reinterpret_cast<char*>(s_c[b]) + 16 * (x - %d);\n",
+       nv * vs / 16);
+  emit("      const char* src = isv ? vsrc + 16 * x : csrc + 16 * (x - %d);\n", nv * vs / 16);
+  emit("      asm volatile(\"cp.async.cg.shared.global [%%0], [%%1], 16;\" :: \"r\"((unsigned)__cvta_generic_to_shared(dst)), \"l\"(src) : \"memory\");\n");
+  emit("    }\n  };\n");
+  // value / column records one instance ahead (double buffer)
+  emit("  if (gof(0) >= ninst) return;\n");
+  emit("  stage(gof(0), 0);\n");
+  emit("  asm volatile(\"cp.async.commit_group;\" ::: \"memory\");\n");
+  emit("  for (int q = 0;; ++q) {\n");
+  emit("    const long long gi = gof(q);\n");
+  emit("    if (gi >= ninst) break;\n");
+  emit("    stage(gof(q + 1), (q + 1) & 1);\n");
+  emit("    asm volatile(\"cp.async.commit_group;\" ::: \"memory\");\n");
+  // pf == 1: L2 bulk prefetch of the W (and U) node rows of the instance one CTA round ahead
+  emit("    if (pf == 1 && threadIdx.x < %d) {\n", n);
+  emit("      const long long ga = gi + gstride;\n");
+  emit("      if (ga < ninst) {\n");
+  emit("        const long long c = __ldg(gcols + ga * %d + threadIdx.x);\n", ncp);
+  emit("        asm volatile(\"cp.async.bulk.prefetch.L2.global [%%0], %%1;\" :: \"l\"(W + c * B), \"r\"((unsigned)(B * %d)) : \"memory\");\n", vs);
+  if (!same)
+    emit("        asm volatile(\"cp.async.bulk.prefetch.L2.global [%%0], %%1;\" :: \"l\"(U + c * B), \"r\"((unsigned)(B * %d)) : \"memory\");\n", vs);
+  emit("      }\n    }\n");
+  emit("    asm volatile(\"cp.async.wait_group 1;\" ::: \"memory\");\n");
+  emit("    __syncthreads();\n");
+  emit("    const %s* sv = s_v[q & 1];\n", S);
+  emit("    const int* sc = s_c[q & 1];\n");
+  emit("    for (int ch = warp; ch < nch; ch += nw) {\n");
+  if (full)
+    emit("      const int p0 = ch * %d + %d * lane;\n", 32 * P, P);
+  else
+    emit("      const int p0 = ch * %d + lane;\n", 32 * P);
+  emit("      const %s* Wp = W + p0;\n", S);
+  if (!same) emit("      const %s* Up = U + p0;\n", S);
+  if (!full)
+    for (int q = 0; q < P; ++q) emit("      const bool ok%d = p0 + %d < B;\n", q, 32 * q);
+  for (int b = 0; b < n; ++b) {
+    emit("      const %s* wc%d = Wp + (long long)sc[%d] * B;\n", S, b, b);
+    if (full) {
+      o += "      " + vec_load(S, P, "w" + std::to_string(b), "wc" + std::to_string(b)) + "\n";
+      continue;
+    }
+    for (int q = 0; q < P; ++q)
+      emit("      const %s w%d_%d = ok%d ? __ldg(wc%d + %d) : (%s)0;\n", S, b, q, q, b, 32 * q, S);
+  }
+  emit("      {\n");
+  emit_body(o, pt, S, P, same, full, IL, nv, "        ", full);
+  for (int m = 0; m < g; ++m) {
+    emit("      { %s* rr = R + (long long)__ldg(grows + gi * %d + %d) * B + p0;\n", S, g, m);
+    if (full) {
+      o += "        " + vec_store(S, P, "rr", "r" + std::to_string(m)) + "\n";
+    } else {
+      for (int q = 0; q < P; ++q) emit("        if (ok%d) rr[%d] = r%d_%d;\n", q, 32 * q, m, q);
+    }
+    emit("      }\n");
+  }
+  emit("      }\n");
+  emit("    }\n");
+  emit("    __syncthreads();\n");
+  emit("  }\n}\n");
+  return o;
+}
+
+// The compute body shared by both kernel forms: register W (w<b>_<q>) is loaded; emits the
+// u values, the interleaved fiber chains and the accumulators r<m>_<q>.  `uload(a, q)` gives
+// the expression of U at stencil point a for pair slot q when U != W.
+void emit_body(std::string& o, const Pattern& pt, const char* S, int P, bool same, bool full, int IL, int nv,
+               const char* indent, bool contig) {
+  const int n = pt.n, g = (int)pt.members.size();
+  char buf[512];
+  auto emit = [&](const char* fmt, auto... a) {
+    o += indent;
+    std::snprintf(buf, sizeof(buf), fmt, a...);
+    o += buf;
+  };
+  for (int x = 0; x < nv / 2; ++x) emit("%s2 t%d;\n", S, x);
+  std::vector<char> r_live(g, 0), loaded(nv / 2 + 1, 0);
+  for (int m = 0; m < g; ++m)
+    for (int q = 0; q < P; ++q) emit("%s r%d_%d;\n", S, m, q);
+  int e = 0;
+  for (int a = 0; a < n; ++a) {
+    bool any = false;
+    for (int m = 0; m < g; ++m)
+      for (const auto& f : pt.members[m]) any |= f.first == a;
+    if (!any) continue;
+    emit("{\n");
+    if (same) {
+      for (int q = 0; q < P; ++q) emit("  const %s u%d = w%d_%d;\n", S, q, a, q);
+    } else {
+      emit("  const %s* uc = Up + (long long)sc[%d] * B;\n", S, a);
+      if (full && contig) {
+        o += indent;
+        o += "  " + vec_load(S, P, "uu", "uc") + "\n";
+        for (int q = 0; q < P; ++q) emit("  const %s u%d = uu_%d;\n", S, q, q);
+      } else {
+        for (int q = 0; q < P; ++q) {
+          if (full)
+            emit("  const %s u%d = __ldg(uc + %d);\n", S, q, 32 * q);
+          else
+            emit("  const %s u%d = ok%d ? __ldg(uc + %d) : (%s)0;\n", S, q, q, 32 * q, S);
+        }
+      }
+    }
+    struct Fib {
+      int m;
+      const std::vector<int>* bs;
+      int e0;
+    };
+    std::vector<Fib> fa;
+    for (int m = 0; m < g; ++m)
+      for (const auto& f : pt.members[m])
+        if (f.first == a) {
+          fa.push_back({m, &f.second, e});
+          e += (int)f.second.size();
+        }
+    for (size_t f0 = 0; f0 < fa.size(); f0 += IL) {
+      const size_t f1 = std::min(fa.size(), f0 + (size_t)IL);
+      emit("  {\n");
+      size_t len = 0;
+      for (size_t f = f0; f < f1; ++f) {
+        len = std::max(len, fa[f].bs->size());
+        for (int q = 0; q < P; ++q) emit("    %s x%d_%d;\n", S, (int)(f - f0), q);
+      }
+      for (size_t st = 0; st < len; ++st)
+        for (size_t f = f0; f < f1; ++f) {
+          if (st >= fa[f].bs->size()) continue;
+          const int ee = fa[f].e0 + (int)st, b = (*fa[f].bs)[st];
+          if (!loaded[ee >> 1]) {
+            emit("    t%d = *reinterpret_cast<const %s2*>(sv + %d);\n", ee >> 1, S, ee & ~1);
+            loaded[ee >> 1] = 1;
+          }
+          for (int q = 0; q < P; ++q) {
+            if (st == 0)
+              emit("    x%d_%d = t%d.%c * w%d_%d;\n", (int)(f - f0), q, ee >> 1, (ee & 1) ? 'y' : 'x', b, q);
+            else
+              emit("    x%d_%d = fma(t%d.%c, w%d_%d, x%d_%d);\n", (int)(f - f0), q, ee >> 1, (ee & 1) ? 'y' : 'x',
+                   b, q, (int)(f - f0), q);
+          }
+        }
+      for (size_t f = f0; f < f1; ++f) {
+        const int m = fa[f].m;
+        if (fa[f].bs->empty())
+          for (int q = 0; q < P; ++q) emit("    x%d_%d = (%s)0;\n", (int)(f - f0), q, S);
+        for (int q = 0; q < P; ++q) {
+          if (r_live[m])
+            emit("    r%d_%d = fma(u%d, x%d_%d, r%d_%d);\n", m, q, q, (int)(f - f0), q, m, q);
+          else
+            emit("    r%d_%d = u%d * x%d_%d;\n", m, q, q, (int)(f - f0), q);
+        }
+        r_live[m] = 1;
+      }
+      emit("  }\n");
+    }
+    emit("}\n");
+  }
+  for (int m = 0; m < g; ++m)
+    if (!r_live[m])
+      for (int q = 0; q < P; ++q) emit("r%d_%d = (%s)0;\n", m, q, S);
+}
+
+// Staged form (batch % (32·P) == 0): each warp's W tile (its 32·P pairs at the n stencil nodes,
+// one contiguous row segment per node in the node-major layout) arrives by TMA 1D bulk copies
+// (cp.async.bulk + mbarrier) one instance ahead, so the loads that start an instance are shared-
+// memory loads; value and column records are staged by cp.async two instances ahead (triple
+// buffer: the columns of the next instance address its W copies).  Pair blocks of nw·32·P pairs
+// are the grid's y dimension.
+std::string kernel_source_staged(const Pattern& pt, const std::string& name, const char* S, int P, bool same,
+                                 int IL) {
+  const int n = pt.n, g = (int)pt.members.size();
+  const int vs = std::strcmp(S, "double") == 0 ? 8 : 4;
+  const int nv = vals_stride(pt.nnz(), vs), ncp = cols_stride(n);
+  const int PW = 32 * P;
+  std::string o;
+  char buf[640];
+  auto emit = [&](const char* fmt, auto... a) {
+    std::snprintf(buf, sizeof(buf), fmt, a...);
+    o += buf;
+  };
+  emit("extern \"C\" __global__ void __launch_bounds__(128) %s(const int* __restrict__ gcols, "
+       "const int* __restrict__ grows, const %s* __restrict__ gvals, long long ninst, int B, int run, int pf, "
+       "const %s* __restrict__ U, const %s* __restrict__ W, %s* __restrict__ R) {\n",
+       name.c_str(), S, S, S, S);
+  emit("  extern __shared__ __align__(128) unsigned char s_dyn[];\n");
+  emit("  __shared__ __align__(16) %s s_v[3][%d];\n", S, nv);
+  emit("  __shared__ __align__(16) int s_c[3][%d];\n", ncp);
+  emit("  __shared__ __align__(8) unsigned long long s_bar[4];\n");
+  emit("  const int lane = threadIdx.x & 31, warp = threadIdx.x >> 5, nw = blockDim.x >> 5;\n");
+  emit("  %s* s_w = reinterpret_cast<%s*>(s_dyn) + (size_t)warp * %d;\n", S, S, n * PW);
+  emit("  const int pw0 = blockIdx.y * nw * %d + warp * %d;\n", PW, PW);
+  emit("  const int p0 = pw0 + lane;\n");
+  emit("  const unsigned bar = (unsigned)__cvta_generic_to_shared(&s_bar[warp]);\n");
   emit("  const long long gstride = (long long)gridDim.x * run;\n");
   emit("  auto gof = [&](long long q) { return (long long)blockIdx.x * run + (q / run) * gstride + (q %% run); };\n");
   emit("  auto stage = [&](long long gi, int b) {\n");
@@ -155,102 +422,55 @@ std::string kernel_source(const Pattern& pt, const std::string& name, const char
   emit("      const char* src = isv ? vsrc + 16 * x : csrc + 16 * (x - %d);\n", nv * vs / 16);
   emit("      asm volatile(\"cp.async.cg.shared.global [%%0], [%%1], 16;\" :: \"r\"((unsigned)__cvta_generic_to_shared(dst)), \"l\"(src) : \"memory\");\n");
   emit("    }\n  };\n");
+  emit("  auto issue_w = [&](long long gi, int cb) {\n");
+  emit("    if (gi >= ninst) return;\n");
+  emit("    if (lane == 0) asm volatile(\"mbarrier.arrive.expect_tx.shared::cta.b64 _, [%%0], %%1;\" :: \"r\"(bar), \"r\"(%d) : \"memory\");\n",
+       n * PW * vs);
+  emit("    __syncwarp();\n");
+  emit("    if (lane < %d) {\n", n);
+  emit("      asm volatile(\"fence.proxy.async.shared::cta;\" ::: \"memory\");\n");
+  emit("      const %s* src = W + (long long)s_c[cb][lane] * B + pw0;\n", S);
+  emit("      const unsigned dst = (unsigned)__cvta_generic_to_shared(s_w + lane * %d);\n", PW);
+  emit("      asm volatile(\"cp.async.bulk.shared::cluster.global.mbarrier::complete_tx::bytes [%%0], [%%1], %%2, [%%3];\" :: \"r\"(dst), \"l\"(src), \"r\"(%d), \"r\"(bar) : \"memory\");\n",
+       PW * vs);
+  emit("    }\n  };\n");
   emit("  if (gof(0) >= ninst) return;\n");
+  emit("  if (lane == 0) {\n");
+  emit("    asm volatile(\"mbarrier.init.shared::cta.b64 [%%0], 1;\" :: \"r\"(bar) : \"memory\");\n");
+  emit("    asm volatile(\"fence.mbarrier_init.release.cluster;\" ::: \"memory\");\n");
+  emit("  }\n");
   emit("  stage(gof(0), 0);\n");
+  emit("  stage(gof(1), 1);\n");
   emit("  asm volatile(\"cp.async.commit_group;\" ::: \"memory\");\n");
+  emit("  asm volatile(\"cp.async.wait_group 0;\" ::: \"memory\");\n");
+  emit("  __syncthreads();\n");
+  emit("  issue_w(gof(0), 0);\n");
+  emit("  int b0 = 0;\n");  // buffer of instance q (q % 3)
   emit("  for (long long q = 0;; ++q) {\n");
   emit("    const long long gi = gof(q);\n");
   emit("    if (gi >= ninst) break;\n");
-  emit("    stage(gof(q + 1), (int)((q + 1) & 1));\n");
+  emit("    const int b1 = b0 == 2 ? 0 : b0 + 1, b2 = b1 == 2 ? 0 : b1 + 1;\n");
+  emit("    stage(gof(q + 2), b2);\n");
   emit("    asm volatile(\"cp.async.commit_group;\" ::: \"memory\");\n");
-  emit("    asm volatile(\"cp.async.wait_group 1;\" ::: \"memory\");\n");
-  emit("    __syncthreads();\n");
-  emit("    const %s* sv = s_v[q & 1];\n", S);
-  emit("    const int* sc = s_c[q & 1];\n");
-  emit("    for (int ch = warp; ch < nch; ch += nw) {\n");
-  emit("      const int p0 = ch * %d + lane;\n", 32 * P);
-  emit("      const %s* Wp = W + p0;\n", S);
-  if (!same) emit("      const %s* Up = U + p0;\n", S);
-  if (!full)
-    for (int q = 0; q < P; ++q) emit("      const bool ok%d = p0 + %d < B;\n", q, 32 * q);
-  for (int x = 0; x < nv / 2; ++x) emit("      %s2 t%d;\n", S, x);
-  for (int b = 0; b < n; ++b) {
-    emit("      const %s* wc%d = Wp + (long long)sc[%d] * B;\n", S, b, b);
-    for (int q = 0; q < P; ++q) {
-      if (full)
-        emit("      const %s w%d_%d = __ldg(wc%d + %d);\n", S, b, q, b, 32 * q);
-      else
-        emit("      const %s w%d_%d = ok%d ? __ldg(wc%d + %d) : (%s)0;\n", S, b, q, q, b, 32 * q, S);
-    }
-  }
-  // program order: stencil point a ascending; members in order; b ascending.  The first product
-  // of every chain is a plain multiply (fma(a, b, 0) rounds identically), so no zero-fills.
-  std::vector<char> r_live(g, 0);
-  for (int m = 0; m < g; ++m)
-    for (int q = 0; q < P; ++q) emit("      %s r%d_%d;\n", S, m, q);
-  int e = 0;
-  for (int a = 0; a < n; ++a) {
-    bool any = false;
-    for (int m = 0; m < g; ++m)
-      for (const auto& f : pt.members[m]) any |= f.first == a;
-    if (!any) continue;
-    emit("      {\n");
-    if (same) {
-      for (int q = 0; q < P; ++q) emit("        const %s u%d = w%d_%d;\n", S, q, a, q);
-    } else {
-      emit("        const %s* uc = Up + (long long)sc[%d] * B;\n", S, a);
-      for (int q = 0; q < P; ++q) {
-        if (full)
-          emit("        const %s u%d = __ldg(uc + %d);\n", S, q, 32 * q);
-        else
-          emit("        const %s u%d = ok%d ? __ldg(uc + %d) : (%s)0;\n", S, q, q, 32 * q, S);
-      }
-    }
-    for (int m = 0; m < g; ++m)
-      for (const auto& f : pt.members[m]) {
-        if (f.first != a) continue;
-        emit("        {\n");
-        for (int q = 0; q < P; ++q) emit("          %s x%d;\n", S, q);
-        bool first = true;
-        for (int b : f.second) {
-          if ((e & 1) == 0) emit("          t%d = *reinterpret_cast<const %s2*>(sv + %d);\n", e >> 1, S, e);
-          for (int q = 0; q < P; ++q) {
-            if (first)
-              emit("          x%d = t%d.%c * w%d_%d;\n", q, e >> 1, (e & 1) ? 'y' : 'x', b, q);
-            else
-              emit("          x%d = fma(t%d.%c, w%d_%d, x%d);\n", q, e >> 1, (e & 1) ? 'y' : 'x', b, q, q);
-          }
-          first = false;
-          ++e;
-        }
-        if (f.second.empty())
-          for (int q = 0; q < P; ++q) emit("          x%d = (%s)0;\n", q, S);
-        for (int q = 0; q < P; ++q) {
-          if (r_live[m])
-            emit("          r%d_%d = fma(u%d, x%d, r%d_%d);\n", m, q, q, q, m, q);
-          else
-            emit("          r%d_%d = u%d * x%d;\n", m, q, q, q);
-        }
-        r_live[m] = 1;
-        emit("        }\n");
-      }
-    emit("      }\n");
-  }
-  for (int m = 0; m < g; ++m)
-    if (!r_live[m])
-      for (int q = 0; q < P; ++q) emit("      r%d_%d = (%s)0;\n", m, q, S);
+  emit("    asm volatile(\"{\\n.reg .pred p;\\nWAIT_%%=:\\nmbarrier.try_wait.parity.shared::cta.b64 p, [%%0], %%1;\\n@!p bra WAIT_%%=;\\n}\\n\" :: \"r\"(bar), \"r\"((unsigned)(q & 1)) : \"memory\");\n");
+  for (int b = 0; b < n; ++b)
+    for (int q = 0; q < P; ++q) emit("    const %s w%d_%d = s_w[%d + lane];\n", S, b, q, b * PW + 32 * q);
+  emit("    __syncwarp();\n");
+  emit("    issue_w(gof(q + 1), b1);\n");
+  emit("    const %s* sv = s_v[b0];\n", S);
+  emit("    const int* sc = s_c[b0];\n");
+  if (!same) emit("    const %s* Up = U + p0;\n", S);
+  emit("    {\n");
+  emit_body(o, pt, S, P, same, true, IL, nv, "      ");
   for (int m = 0; m < g; ++m) {
     emit("      { %s* rr = R + (long long)__ldg(grows + gi * %d + %d) * B + p0;\n", S, g, m);
-    for (int q = 0; q < P; ++q) {
-      if (full)
-        emit("        rr[%d] = r%d_%d;\n", 32 * q, m, q);
-      else
-        emit("        if (ok%d) rr[%d] = r%d_%d;\n", q, 32 * q, m, q);
-    }
+    for (int q = 0; q < P; ++q) emit("        rr[%d] = r%d_%d;\n", 32 * q, m, q);
     emit("      }\n");
   }
   emit("    }\n");
+  emit("    asm volatile(\"cp.async.wait_group 0;\" ::: \"memory\");\n");
   emit("    __syncthreads();\n");
+  emit("    b0 = b1;\n");
   emit("  }\n}\n");
   return o;
 }
@@ -336,6 +556,9 @@ void free_group_plan(GroupPlan* gp) {
   }
   if (gp->fb_rows) cudaFree(gp->fb_rows);
   for (cudaLibrary_t l : gp->libs) cudaLibraryUnload(l);
+  for (cudaStream_t x : gp->side) cudaStreamDestroy(x);
+  for (cudaEvent_t x : gp->side_done) cudaEventDestroy(x);
+  if (gp->fork) cudaEventDestroy(gp->fork);
   delete gp;
 }
 
@@ -347,9 +570,9 @@ egfem_status make_groups(egfem_tensor* t, const std::vector<int64_t>& hrf) {
   if (!t->blk || !t->w_is_v || t->n_u <= 0 || t->nnz <= 0) return EGFEM_OK;
   if (const char* e = getenv("EGFEM_GROUPS"))
     if (e[0] == '0') return EGFEM_OK;
-  int P = 2;
+  int P = 4;
   if (const char* e = getenv("EGFEM_GROUP_P")) P = std::max(1, std::min(4, atoi(e)));
-  int run = 4;
+  int run = 1;
   if (const char* e = getenv("EGFEM_GROUP_RUN")) run = std::max(1, atoi(e));
   const int64_t n_u = t->n_u, n_fib = t->n_fib, nnz = t->nnz;
   std::vector<int32_t> fj(n_fib);
@@ -448,6 +671,13 @@ egfem_status make_groups(egfem_tensor* t, const std::vector<int64_t>& hrf) {
   auto* gp = new GroupPlan();
   gp->pairs_per_lane = P;
   gp->run = run;
+  gp->interleave = 4;
+  if (const char* e = getenv("EGFEM_GROUP_IL")) gp->interleave = std::max(1, atoi(e));
+  if (const char* e = getenv("EGFEM_GROUP_PF")) gp->prefetch = atoi(e);
+  if (const char* e = getenv("EGFEM_GROUP_STAGED")) gp->staged = e[0] != '0';
+  if (const char* e = getenv("EGFEM_GROUP_PERSIST")) gp->persistent = e[0] != '0';
+  if (const char* e = getenv("EGFEM_GROUP_CAP")) gp->cap = std::max(1, atoi(e));
+  if (const char* e = getenv("EGFEM_GROUP_CARVE")) gp->carveout = atoi(e);
   gp->f64 = f64;
   for (size_t x = 0; x < chosen.size(); ++x) {
     GroupClass gc;
@@ -563,7 +793,10 @@ egfem_status group_compile_key(const int32_t* key, int32_t len, int P, int f64, 
   }
   if (x != len) return EGFEM_ERR_INVALID_ARGUMENT;
   const int v = std::getenv("EGFEM_GROUP_VARIANT") ? std::atoi(std::getenv("EGFEM_GROUP_VARIANT")) : 0;
-  const std::string src = kernel_source(pt, "egfem_grp_test", f64 ? "double" : "float", P, v & 1, (v >> 1) & 1);
+  const int il = std::getenv("EGFEM_GROUP_IL") ? std::max(1, std::atoi(std::getenv("EGFEM_GROUP_IL"))) : 2;
+  const bool stg = ((v >> 1) & 1) && !(std::getenv("EGFEM_GROUP_STAGED") && std::getenv("EGFEM_GROUP_STAGED")[0] == '0');
+  const std::string src = stg ? kernel_source_staged(pt, "egfem_grp_test", f64 ? "double" : "float", P, v & 1, il)
+                              : kernel_source(pt, "egfem_grp_test", f64 ? "double" : "float", P, v & 1, (v >> 1) & 1, il);
   std::vector<char> cubin;
   egfem_status st = compile_cubin(src, &cubin, log);
   if (const char* d = getenv("EGFEM_GROUP_DUMP")) {
@@ -598,8 +831,10 @@ egfem_status ensure_variant(GroupPlan* gp, int v) {
   std::vector<egfem_status> sts(nc, EGFEM_OK);
   for (size_t c = 0; c < nc; ++c) {
     names[c] = "egfem_grp_" + std::to_string(c) + "_v" + std::to_string(v);
-    srcs[c] = kernel_source(pattern_from_key(gp->classes[c].key), names[c], gp->f64 ? "double" : "float",
-                            gp->pairs_per_lane, same, full);
+    const Pattern pt = pattern_from_key(gp->classes[c].key);
+    const char* S = gp->f64 ? "double" : "float";
+    srcs[c] = full && gp->staged ? kernel_source_staged(pt, names[c], S, gp->pairs_per_lane, same, gp->interleave)
+                                 : kernel_source(pt, names[c], S, gp->pairs_per_lane, same, full, gp->interleave);
   }
   std::vector<std::thread> th;
   std::atomic<size_t> next{0};
@@ -635,6 +870,26 @@ egfem_status ensure_variant(GroupPlan* gp, int v) {
   return EGFEM_OK;
 }
 
+constexpr int kSideStreams = 4;
+
+egfem_status ensure_side(GroupPlan* gp, int dev) {
+  std::lock_guard<std::mutex> lk(gp->mu);
+  if (gp->side_dev == dev) return EGFEM_OK;
+  gp->side.resize(kSideStreams);
+  gp->side_done.resize(kSideStreams);
+  for (int k = 0; k < kSideStreams; ++k) {
+    EGFEM_CUDA_TRY(cudaStreamCreateWithFlags(&gp->side[k], cudaStreamNonBlocking));
+    EGFEM_CUDA_TRY(cudaEventCreateWithFlags(&gp->side_done[k], cudaEventDisableTiming));
+  }
+  EGFEM_CUDA_TRY(cudaEventCreateWithFlags(&gp->fork, cudaEventDisableTiming));
+  gp->side_dev = dev;
+  return EGFEM_OK;
+}
+
+// The largest class runs on the caller's stream; the other classes and the fallback rows run
+// concurrently on side streams (fork / join by events, so the call stays stream-ordered and
+// CUDA-graph capturable): their launches are small and latency-bound, serialized they cost
+// ≈ 20 % of the cfg5 action.
 egfem_status launch_groups(const egfem_tensor* t, int32_t batch, const void* U, const void* W, void* R,
                            cudaStream_t s) {
   GroupPlan* gp = t->grp;
@@ -645,20 +900,92 @@ egfem_status launch_groups(const egfem_tensor* t, int32_t batch, const void* U, 
   const int v = (U == W ? 1 : 0) | (batch % (32 * P) == 0 ? 2 : 0);
   egfem_status st = ensure_variant(gp, v);
   if (st) return st;
-  const int threads = 32 * std::min(4, nch);
-  for (const auto& gc : gp->classes) {
+  const size_t nc = gp->classes.size();
+  const bool fork = nc + (gp->fb_count > 0 ? 1 : 0) > 1;
+  if (fork) {
+    if ((st = ensure_side(gp, t->device))) return st;
+    EGFEM_CUDA_TRY(cudaEventRecord(gp->fork, s));
+    for (int k = 0; k < kSideStreams; ++k) EGFEM_CUDA_TRY(cudaStreamWaitEvent(gp->side[k], gp->fork, 0));
+  }
+  const bool staged = gp->staged && (v & 2);
+  const size_t vsz0 = gp->f64 ? 8 : 4;
+  int nw = std::min(4, nch);
+  if (staged) {  // warps per CTA: a divisor of the chunk count whose W tiles fit 48 KB
+    int maxn = 1;
+    for (const auto& gc : gp->classes) maxn = std::max(maxn, gc.n);
+    nw = 1;
+    for (int d = std::min(4, nch); d >= 1; --d)
+      if (nch % d == 0 && (size_t)d * maxn * 32 * P * vsz0 <= 48 * 1024) {
+        nw = d;
+        break;
+      }
+  }
+  const int threads = 32 * nw;
+  const int pblocks = staged ? nch / nw : 1;
+  int next_side = 0;
+  // bulk L2 prefetch needs 16-byte rows and 16-byte aligned arrays
+  const size_t vsz = gp->f64 ? 8 : 4;
+  const int pf = gp->prefetch == 1 ? (((size_t)batch * vsz) % 16 == 0 && ((uintptr_t)U % 16) == 0 &&
+                                       ((uintptr_t)W % 16) == 0)
+                                    : gp->prefetch;
+  auto launch_class = [&](size_t c, cudaStream_t str) -> egfem_status {
+    GroupClass& gc = gp->classes[c];
     const int64_t runs = (gc.ninst + gp->run - 1) / gp->run;
-    const int64_t ctas = std::max<int64_t>(1, std::min<int64_t>(runs, (int64_t)g_sms_grp[dev] * 32));
+    if (gc.per_sm[v] == 0) {  // persistent grid: the resident CTAs walk the runs round-robin
+      cudaFuncAttributes fa{};
+      int per = 1;
+      if (cudaFuncGetAttributes(&fa, (const void*)gc.fn[v]) == cudaSuccess && fa.numRegs > 0)
+        per = std::max(1, std::min(32, 65536 / (std::max(fa.numRegs, 1) * threads)));
+      else
+        cudaGetLastError();
+      gc.per_sm[v] = per;
+    }
+    const int64_t ctas =
+        std::max<int64_t>(1, std::min<int64_t>(runs, (int64_t)g_sms_grp[dev] * (gp->persistent ? gc.per_sm[v] : gp->cap)));
     long long ninst = gc.ninst;
-    int B = batch, run = gp->run;
-    void* args[] = {(void*)&gc.cols, (void*)&gc.rows, (void*)&gc.vals, &ninst, &B, &run, (void*)&U, (void*)&W, &R};
-    EGFEM_CUDA_TRY(cudaLaunchKernel((const void*)gc.fn[v], dim3((unsigned)ctas), dim3(threads), args, 0, s));
+    int B = batch, run = gp->run, pfl = pf;
+    void* args[] = {(void*)&gc.cols, (void*)&gc.rows, (void*)&gc.vals, &ninst, &B, &run, &pfl, (void*)&U, (void*)&W, &R};
+    const size_t dyn = staged ? (size_t)nw * gc.n * 32 * P * vsz0 : 0;
+    if (!gc.carve_set[v]) {  // L1 over shared memory: consecutive instances of a run share stencil rows
+      if (gp->carveout >= 0)
+        cudaFuncSetAttribute((const void*)gc.fn[v], cudaFuncAttributePreferredSharedMemoryCarveout, gp->carveout);
+      cudaGetLastError();
+      gc.carve_set[v] = 1;
+    }
+    if (dyn > 0 && gc.dyn_set[v] < dyn) {
+      cudaError_t ce = cudaFuncSetAttribute((const void*)gc.fn[v], cudaFuncAttributeMaxDynamicSharedMemorySize, (int)dyn);
+      if (ce != cudaSuccess) {
+        set_error(std::string("cudaFuncSetAttribute(dynamic smem ") + std::to_string(dyn) + "): " + cudaGetErrorString(ce));
+        return EGFEM_ERR_CUDA;
+      }
+      gc.dyn_set[v] = dyn;
+    }
+    cudaError_t ce = cudaLaunchKernel((const void*)gc.fn[v], dim3((unsigned)ctas, (unsigned)pblocks), dim3(threads), args,
+                                      dyn, str);
+    if (ce != cudaSuccess) {
+      set_error(std::string("grouped batched kernel launch (grid ") + std::to_string(ctas) + "x" +
+                std::to_string(pblocks) + ", block " + std::to_string(threads) + ", dyn smem " + std::to_string(dyn) +
+                "): " + cudaGetErrorString(ce));
+      return EGFEM_ERR_CUDA;
+    }
     count_launch();
+    return EGFEM_OK;
+  };
+  // side work first (its CTAs are placed before the big class fills the machine)
+  for (size_t c = 1; c < nc; ++c) {
+    if ((st = launch_class(c, gp->side[next_side]))) return st;
+    next_side = (next_side + 1) % kSideStreams;
   }
   if (gp->fb_count > 0) {
-    st = launch_dense_rows(t, batch, gp->fb_rows, gp->fb_classes, U, W, R, s);
-    if (st) return st;
+    cudaStream_t fs = fork ? gp->side[next_side] : s;
+    if ((st = launch_dense_rows(t, batch, gp->fb_rows, gp->fb_classes, U, W, R, fs))) return st;
   }
+  if (nc > 0 && (st = launch_class(0, s))) return st;
+  if (fork)
+    for (int k = 0; k < kSideStreams; ++k) {
+      EGFEM_CUDA_TRY(cudaEventRecord(gp->side_done[k], gp->side[k]));
+      EGFEM_CUDA_TRY(cudaStreamWaitEvent(s, gp->side_done[k], 0));
+    }
   return EGFEM_OK;
 }
 

@@ -612,3 +612,41 @@ def test_cuda_graph_replay_bitwise(eg, name):
     g.replay()
     torch.cuda.synchronize()
     assert torch.equal(r, r0) and torch.equal(J, J0)
+
+
+@pytest.mark.parametrize("same", [True, False])
+def test_batched_groups_graph_and_shards(eg, orc, same):
+    """cfg5's batched action through the compiled row groups (fork/join over side streams):
+    captured into a CUDA graph and replayed it is bitwise the eager result; batch shards (the
+    multi-GPU split of the batch: pairs are independent) run as separate calls
+    reproduce the full-batch columns bitwise; U ≠ W (the non-aliased kernel variant) and a batch
+    that is not a multiple of the pair chunk (the guarded variant) match the oracle."""
+    import torch
+    pr = I.make_problem("cfg5", n=24, batch=96)
+    t = eg.egfem_tensor_build(pr.mesh, pr.V, pr.W, pr.form, device=0)
+    assert "egfem_grp" in eg.egfem_kernel_name(t, 3)
+    o = orc.OracleTensor(pr.mesh, pr.V, pr.W, pr.form)
+    U = torch.tensor(np.ascontiguousarray(pr.u.T), device="cuda")
+    Wt = U if same else U * 0.5 + 0.25
+    R = torch.empty_like(U)
+    eg.egfem_apply_batched(t, 96, eg.LAYOUT_NODE_MAJOR, U, Wt, R)
+    torch.cuda.synchronize()
+    R0 = R.clone()
+    Wn = Wt.cpu().numpy().T
+    ref = o.apply_batched(pr.u, Wn)
+    assert rel_l2(R0.cpu().numpy().T, ref) <= FP64_TOL
+    R.zero_()
+    g = torch.cuda.CUDAGraph()
+    with torch.cuda.graph(g):
+        eg.egfem_apply_batched(t, 96, eg.LAYOUT_NODE_MAJOR, U, Wt, R, torch.cuda.current_stream())
+    g.replay()
+    torch.cuda.synchronize()
+    assert torch.equal(R, R0)
+    # shards of the batch (as bench.py deals them to ranks) = the full batch's columns, bitwise
+    for lo, hi in ((0, 64), (64, 96), (0, 37), (37, 96)):
+        Us = U[:, lo:hi].contiguous()
+        Ws = Us if same else Wt[:, lo:hi].contiguous()
+        Rs = torch.empty_like(Us)
+        eg.egfem_apply_batched(t, hi - lo, eg.LAYOUT_NODE_MAJOR, Us, Ws, Rs)
+        torch.cuda.synchronize()
+        assert torch.equal(Rs, R0[:, lo:hi]), (lo, hi)
