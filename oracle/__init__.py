@@ -33,7 +33,7 @@ _lib = None
 def build(force: bool = False) -> str:
     """Compile liboracle.so with the host C++ compiler (plain -O2, no fast-math)."""
     if force or not os.path.exists(_LIB) or os.path.getmtime(_LIB) < os.path.getmtime(_SRC):
-        subprocess.check_call(["g++", "-O2", "-std=c++17", "-shared", "-fPIC", "-o", _LIB, _SRC])
+        subprocess.check_call(["g++", "-O2", "-std=c++17", "-fopenmp", "-shared", "-fPIC", "-o", _LIB, _SRC])
     return _LIB
 
 
@@ -61,6 +61,10 @@ def lib():
         L.oracle_bilinear.restype = i32
         L.oracle_rule.argtypes = [i32, i32, i32, P, P]
         L.oracle_rule.restype = i32
+        L.oracle_interp_range.argtypes = [P, i32, ctypes.c_double, P, P, i64, i64]
+        L.oracle_interp_range.restype = i32
+        L.oracle_set_threads.argtypes = [i32]
+        L.oracle_set_threads(1)  # the plain sequential oracle unless a caller asks (bench all-cores timing)
         _lib = L
     return _lib
 
@@ -76,6 +80,11 @@ def rule(dim, degree):
     w = np.zeros(nq, np.float64)
     L.oracle_rule(dim, degree, nq, bary.ctypes.data_as(ctypes.c_void_p), w.ctypes.data_as(ctypes.c_void_p))
     return bary, w
+
+
+def set_threads(n):
+    """OpenMP threads of the row / cell loops (default 1; results are bitwise independent of n)."""
+    lib().oracle_set_threads(int(n))
 
 
 def _p(a):
@@ -114,12 +123,12 @@ class OracleTensor:
             _lib.oracle_free(self.h)
             self.h = None
 
-    def export(self, slot_ik=False, loc=False):
+    def export(self, slot_ik=False, loc=False, maps=True):
         L = lib()
         out = dict(t_row_ptr=np.zeros(self.n_u + 1, np.int64), t_j=np.zeros(self.nnz, np.int32),
                    t_k=np.zeros(self.nnz, np.int32), t_val=np.zeros(self.nnz, np.float64),
                    csr_row_ptr=np.zeros(self.n_u + 1, np.int64), csr_col=np.zeros(self.nnz_csr, np.int32),
-                   slot_ij=np.zeros(self.nnz, np.int32))
+                   slot_ij=np.zeros(self.nnz, np.int32) if maps else None)
         out["slot_ik"] = np.zeros(self.nnz, np.int32) if slot_ik else None
         out["loc"] = np.zeros(self.nnz, np.uint8) if loc else None
         keys = ["t_row_ptr", "t_j", "t_k", "t_val", "csr_row_ptr", "csr_col", "slot_ij", "slot_ik", "loc"]
@@ -128,10 +137,13 @@ class OracleTensor:
             raise ValueError(f"oracle_export failed rc={rc}")
         return {k: v for k, v in out.items() if v is not None}
 
-    def interp(self, kind, p, u):
+    def interp(self, kind, p, u, items=None):
+        """w at the W-DOFs; items=(c0, c1) restricts to cells [c0, c1) (cell-wise kinds) or
+        W-DOFs [c0, c1) (nodal kinds), the rest of w stays 0."""
         w = np.zeros(self.n_f, np.float64)
         u = np.ascontiguousarray(u, np.float64)
-        rc = lib().oracle_interp(self.h, kind, float(p), _p(u), _p(w))
+        c0, c1 = (0, -1) if items is None else items
+        rc = lib().oracle_interp_range(self.h, kind, float(p), _p(u), _p(w), int(c0), int(c1))
         if rc != 0:
             raise ValueError(f"oracle_interp failed rc={rc}")
         return w

@@ -5,7 +5,11 @@
 // legs.  It shares no code, header, table or constant generator with the CUDA
 // path (paper_2005_06193_b200/csrc) and neither side includes the other.
 //
-// Everything is fp64, single-threaded, sequential, in the paper's order:
+// Everything is fp64, sequential, in the paper's order.  It runs single-threaded unless
+// oracle_set_threads(n > 1) is called (only bench.py's all-cores cpu_baseline timing does):
+// then the row loops of apply / jacobian and the cell loops of interp are split across OpenMP
+// threads, every row (cell) still computed alone and in its sequential order, so the results
+// are bitwise those of one thread.
 //   * T_ijk = ∫ (slot_a φ_i)(slot_b φ_j)(slot_c η_k) dx assembled element by
 //     element with a quadrature rule (eq. (egfem_terms);
 //     L253 K_a; L327 M; L400 N), duplicates summed in emission order, stored as
@@ -21,6 +25,8 @@
 // Pinned by tests/test_oracle_*.py (closed forms, brute force, partition of unity,
 // symmetry, Euler homogeneity, finite differences, Case-1 exactness).
 // =============================================================================
+#include <omp.h>
+
 #include <algorithm>
 #include <cmath>
 #include <cstdint>
@@ -557,14 +563,21 @@ int oracle_export(const void* h, int64_t* t_row_ptr, int32_t* t_j, int32_t* t_k,
 //   MINSURF_P0:      a(∇u) = (1 + ‖∇u‖²)^{-1/2} at the P0 DOF of each cell (minimal surface, L605, L609)
 //   RECIPROCAL:      c̃(u) = σ/(k + u) with σ = 1, k = p (biochemical, L520–535) at the W-DOFs:
 //                    the nodes (W = V) or the cell centroid (W = P0, V = P1: u_h(x_K) = Σ_a u_a λ_a(x_K))
-int oracle_interp(const void* h, int kind, double p, const double* u, double* w) {
+// Work items [c0, c1): cells for the cell-wise kinds, W-DOFs for the nodal ones (c1 < 0: all).
+int oracle_interp_range(const void* h, int kind, double p, const double* u, double* w, int64_t c0, int64_t c1) {
   const OTensor* T = static_cast<const OTensor*>(h);
   const int d = T->dim;
+  const bool nodal = (kind == OK_IDENTITY || kind == OK_SQUARE ||
+                      (kind == OK_RECIPROCAL && T->W.family == T->V.family && T->W.n_dofs == T->V.n_dofs)) &&
+                     T->W.family != OF_QUAD;
+  const int64_t n_items = nodal ? T->W.n_dofs : T->n_cells;
+  if (c1 < 0 || c1 > n_items) c1 = n_items;
+  if (c0 < 0) c0 = 0;
   if (T->W.family == OF_QUAD && (kind == OK_SQUARE || kind == OK_RECIPROCAL)) {
     // Case 3: f evaluated at the quadrature points, u_h(x_ℓ) = Σ_a λ_a(x_ℓ) u_a
     if (T->V.family != OF_P1) return -2;
     const int nq = T->W.n_loc;
-    for (int64_t K = 0; K < T->n_cells; ++K) {
+    for (int64_t K = c0; K < c1; ++K) {
       const int32_t* I = &T->V.cell_dofs[K * T->V.n_loc];
       for (int l = 0; l < nq; ++l) {
         double uh = 0;
@@ -576,16 +589,16 @@ int oracle_interp(const void* h, int kind, double p, const double* u, double* w)
   }
   if (kind == OK_IDENTITY || kind == OK_SQUARE) {
     if (T->W.n_dofs != T->V.n_dofs) return -1;
-    for (int64_t k = 0; k < T->W.n_dofs; ++k) w[k] = (kind == OK_IDENTITY) ? u[k] : u[k] * u[k];
+    for (int64_t k = c0; k < c1; ++k) w[k] = (kind == OK_IDENTITY) ? u[k] : u[k] * u[k];
     return 0;
   }
   if (kind == OK_RECIPROCAL) {
     if (T->W.family == T->V.family && T->W.n_dofs == T->V.n_dofs) {
-      for (int64_t k = 0; k < T->W.n_dofs; ++k) w[k] = 1.0 / (p + u[k]);
+      for (int64_t k = c0; k < c1; ++k) w[k] = 1.0 / (p + u[k]);
       return 0;
     }
     if (T->W.family != OF_P0 || T->V.family != OF_P1) return -2;
-    for (int64_t K = 0; K < T->n_cells; ++K) {
+    for (int64_t K = c0; K < c1; ++K) {
       const int32_t* I = &T->V.cell_dofs[K * T->V.n_loc];
       double uc = 0;  // u_h at the centroid: λ_a = 1/(d+1)
       for (int a = 0; a <= d; ++a) uc += u[I[a]] / (d + 1);
@@ -595,7 +608,8 @@ int oracle_interp(const void* h, int kind, double p, const double* u, double* w)
   }
   if (kind == OK_MINSURF_P0) {
     if ((T->W.family != OF_P0 && T->W.family != OF_QUAD) || T->V.family != OF_P1) return -2;
-    for (int64_t K = 0; K < T->n_cells; ++K) {
+#pragma omp parallel for schedule(static)
+    for (int64_t K = c0; K < c1; ++K) {
       Geo g = geometry(*T, K);
       const int32_t* I = &T->V.cell_dofs[K * T->V.n_loc];
       double gu[3] = {0, 0, 0};  // (Π_∇u ·₂ u) at the cell's DOF
@@ -610,7 +624,8 @@ int oracle_interp(const void* h, int kind, double p, const double* u, double* w)
   if (kind == OK_GRADPOW_P0) {
     // W = P0, or QUAD (∇u_h of P1 is the same at every quadrature point of the cell)
     if ((T->W.family != OF_P0 && T->W.family != OF_QUAD) || T->V.family != OF_P1) return -2;
-    for (int64_t K = 0; K < T->n_cells; ++K) {
+#pragma omp parallel for schedule(static)
+    for (int64_t K = c0; K < c1; ++K) {
       Geo g = geometry(*T, K);
       const int32_t* I = &T->V.cell_dofs[K * T->V.n_loc];
       double gu[3] = {0, 0, 0};  // (Π_∇u ·₂ u) at the cell's DOF
@@ -627,7 +642,7 @@ int oracle_interp(const void* h, int kind, double p, const double* u, double* w)
     if (T->W.family != OF_P2 || T->V.family != OF_P1 || d != 2) return -2;
     // DOF bary points of P2 local order v0,v1,v2,m01,m12,m20
     const double beta[6][3] = {{1, 0, 0}, {0, 1, 0}, {0, 0, 1}, {0.5, 0.5, 0}, {0, 0.5, 0.5}, {0.5, 0, 0.5}};
-    for (int64_t K = 0; K < T->n_cells; ++K) {
+    for (int64_t K = c0; K < c1; ++K) {
       const int32_t* I = &T->V.cell_dofs[K * 3];
       const int32_t* Wd = &T->W.cell_dofs[K * 6];
       for (int l = 0; l < 6; ++l) {
@@ -641,10 +656,17 @@ int oracle_interp(const void* h, int kind, double p, const double* u, double* w)
   return -3;
 }
 
+int oracle_interp(const void* h, int kind, double p, const double* u, double* w) {
+  return oracle_interp_range(h, kind, p, u, w, 0, -1);
+}
+
+void oracle_set_threads(int n) { omp_set_num_threads(n < 1 ? 1 : n); }
+
 // ---------------------------------------------------------------- apply
 // r_i = Σ_{(j,k)} T_ijk u_j w_k, sequential in canonical order.
 void oracle_apply(const void* h, const double* u, const double* w, double* r) {
   const OTensor* T = static_cast<const OTensor*>(h);
+#pragma omp parallel for schedule(static)
   for (int64_t i = 0; i < T->V.n_dofs; ++i) {
     double acc = 0;
     for (int64_t e = T->t_row_ptr[i]; e < T->t_row_ptr[i + 1]; ++e)
@@ -670,6 +692,8 @@ static int build_Duw(const OTensor* T, int kind, double p, const double* u, std:
   if (T->W.family == OF_QUAD && (kind == OK_SQUARE || kind == OK_RECIPROCAL)) {
     // w_ℓ = f(u_h(x_ℓ)), u_h(x_ℓ) = Σ_a λ_a(x_ℓ) u_a  ⇒  ∂w_ℓ/∂u_a = f'(u_h(x_ℓ)) λ_a(x_ℓ)
     const int nq = T->W.n_loc;
+    D.resize((size_t)T->n_cells * nq * (d + 1));  // entry order: cell, point, vertex (as a sequential push)
+#pragma omp parallel for schedule(static)
     for (int64_t K = 0; K < T->n_cells; ++K) {
       const int32_t* I = &T->V.cell_dofs[K * T->V.n_loc];
       for (int l = 0; l < nq; ++l) {
@@ -677,7 +701,8 @@ static int build_Duw(const OTensor* T, int kind, double p, const double* u, std:
         for (int a = 0; a <= d; ++a) uh += T->wbary[l * (d + 1) + a] * u[I[a]];
         const double df = (kind == OK_SQUARE) ? 2.0 * uh : -1.0 / ((p + uh) * (p + uh));
         for (int a = 0; a <= d; ++a)
-          D.push_back({(int64_t)T->W.cell_dofs[K * nq + l], I[a], df * T->wbary[l * (d + 1) + a]});
+          D[((size_t)K * nq + l) * (d + 1) + a] = {(int64_t)T->W.cell_dofs[K * nq + l], I[a],
+                                                    df * T->wbary[l * (d + 1) + a]};
       }
     }
     return 0;
@@ -693,6 +718,9 @@ static int build_Duw(const OTensor* T, int kind, double p, const double* u, std:
   if (kind == OK_GRADPOW_P0) {
     // w_K = |g|^{p-2}, g = Σ_a u_a ∇λ_a  ⇒  ∂w_K/∂u_a = (p-2)|g|^{p-4} (g·∇λ_a);
     // at g = 0 the value 0 is used (reading C11).  W = QUAD: the same for every point of K.
+    const int nl = T->W.n_loc;
+    D.resize((size_t)T->n_cells * nl * (d + 1));  // entry order: cell, W-DOF, vertex (as a sequential push)
+#pragma omp parallel for schedule(static)
     for (int64_t K = 0; K < T->n_cells; ++K) {
       Geo g = geometry(*T, K);
       const int32_t* I = &T->V.cell_dofs[K * T->V.n_loc];
@@ -702,17 +730,20 @@ static int build_Duw(const OTensor* T, int kind, double p, const double* u, std:
       double gg = 0;
       for (int x = 0; x < d; ++x) gg += gu[x] * gu[x];
       double fac = (gg == 0.0) ? 0.0 : (p - 2.0) * std::pow(std::sqrt(gg), p - 4.0);
-      for (int l = 0; l < T->W.n_loc; ++l)
+      for (int l = 0; l < nl; ++l)
         for (int a = 0; a <= d; ++a) {
           double gdot = 0;
           for (int x = 0; x < d; ++x) gdot += gu[x] * g.grad[a][x];
-          D.push_back({(int64_t)T->W.cell_dofs[K * T->W.n_loc + l], I[a], fac * gdot});
+          D[((size_t)K * nl + l) * (d + 1) + a] = {(int64_t)T->W.cell_dofs[K * nl + l], I[a], fac * gdot};
         }
     }
     return 0;
   }
   if (kind == OK_MINSURF_P0) {
     // a_K = (1 + |g|²)^{-1/2}, g = Σ_a u_a ∇λ_a  ⇒  ∂a_K/∂u_a = −(1 + |g|²)^{-3/2} (g·∇λ_a)
+    const int nl = T->W.n_loc;
+    D.resize((size_t)T->n_cells * nl * (d + 1));
+#pragma omp parallel for schedule(static)
     for (int64_t K = 0; K < T->n_cells; ++K) {
       Geo g = geometry(*T, K);
       const int32_t* I = &T->V.cell_dofs[K * T->V.n_loc];
@@ -722,11 +753,11 @@ static int build_Duw(const OTensor* T, int kind, double p, const double* u, std:
       double gg = 0;
       for (int x = 0; x < d; ++x) gg += gu[x] * gu[x];
       const double fac = -std::pow(1.0 + gg, -1.5);
-      for (int l = 0; l < T->W.n_loc; ++l)
+      for (int l = 0; l < nl; ++l)
         for (int a = 0; a <= d; ++a) {
           double gdot = 0;
           for (int x = 0; x < d; ++x) gdot += gu[x] * g.grad[a][x];
-          D.push_back({(int64_t)T->W.cell_dofs[K * T->W.n_loc + l], I[a], fac * gdot});
+          D[((size_t)K * nl + l) * (d + 1) + a] = {(int64_t)T->W.cell_dofs[K * nl + l], I[a], fac * gdot};
         }
     }
     return 0;
@@ -810,12 +841,18 @@ int oracle_jacobian(const void* h, int mode, int kind, double p, const double* u
                     double* vals) {
   const OTensor* T = static_cast<const OTensor*>(h);
   std::fill(vals, vals + T->csr_col.size(), 0.0);
+  int bad = 0;
+#pragma omp parallel for schedule(static) reduction(|| : bad)
   for (int64_t i = 0; i < T->V.n_dofs; ++i)
     for (int64_t e = T->t_row_ptr[i]; e < T->t_row_ptr[i + 1]; ++e) {
       int64_t s = csr_find(T, i, T->t_j[e]);
-      if (s < 0) return -3;
+      if (s < 0) {
+        bad = 1;
+        break;
+      }
       vals[s] += T->t_val[e] * w[T->t_k[e]];
     }
+  if (bad) return -3;
   if (mode == OJ_PICARD) return 0;
   std::vector<DEntry> D;
   int rc = build_Duw(T, kind, p, u, D);
@@ -829,6 +866,7 @@ int oracle_jacobian(const void* h, int mode, int kind, double p, const double* u
     std::vector<int64_t> fill(dptr.begin(), dptr.end() - 1);
     for (auto& de : D) Ds[fill[de.k]++] = de;
   }
+#pragma omp parallel for schedule(static) reduction(|| : bad)
   for (int64_t i = 0; i < T->V.n_dofs; ++i) {
     // B_{i,k} = (T ·₂ u)_{ik} = Σ_j T_ijk u_j
     std::map<int64_t, double> B;
@@ -837,11 +875,14 @@ int oracle_jacobian(const void* h, int mode, int kind, double p, const double* u
     for (auto& kv : B)
       for (int64_t q = dptr[kv.first]; q < dptr[kv.first + 1]; ++q) {
         int64_t s = csr_find(T, i, Ds[q].m);
-        if (s < 0) return -6;
+        if (s < 0) {
+          bad = 1;
+          continue;
+        }
         vals[s] += kv.second * Ds[q].v;
       }
   }
-  return 0;
+  return bad ? -6 : 0;
 }
 
 }  // extern "C"

@@ -773,3 +773,35 @@ def test_gradient_u_slot_contracts_to_zero(oracle_mod):
     T = oracle_mod.OracleTensor(m, V, V, I.FORM_CONV_J)
     B = T.jacobian(I.JAC_NEWTON, I.INTERP_IDENTITY, 0.0, np.ones(T.n_u), np.zeros(T.n_f))
     assert np.abs(B).max() < 1e-15
+
+
+@pytest.mark.parametrize("name", ["cfg2", "cfg4", "minsurf2d", "biochem_p0", "quadratic_i4"])
+def test_oracle_threads_bitwise(oracle_mod, name):
+    """the all-cores oracle timing splits the row / cell loops over OpenMP
+    threads, each row still summed alone in its sequential order, so every output is bitwise the
+    single-thread result; a cell-range interp equals the whole interp on its cells."""
+    pr = I.make_problem(name, n=I.SMALL_N[name] + 2)
+    o = oracle_mod.OracleTensor(pr.mesh, pr.V, pr.W, pr.form)
+    outs = []
+    for nt in (1, 4):
+        oracle_mod.set_threads(nt)
+        try:
+            w = o.interp(pr.interp, pr.p, pr.u)
+            outs.append((w, o.apply(pr.u, w), o.jacobian(0, pr.interp, pr.p, pr.u, w),
+                         o.jacobian(1, pr.interp, pr.p, pr.u, w)))
+        finally:
+            oracle_mod.set_threads(1)
+    for a, b in zip(*outs):
+        assert np.array_equal(a, b)
+    w = outs[0][0]
+    cell_wise = pr.W.family in (I.P0, I.QUAD) or pr.interp == I.INTERP_P1_TO_P2_SQUARE
+    n_items = pr.mesh.n_cells if cell_wise else pr.W.n_dofs
+    c0, c1 = n_items // 3, 2 * n_items // 3
+    wp = o.interp(pr.interp, pr.p, pr.u, items=(c0, c1))
+    if cell_wise:
+        dofs = np.asarray(pr.W.cell_dofs)[c0:c1].ravel()
+    else:
+        dofs = np.arange(c0, c1)
+    assert np.array_equal(wp[dofs], w[dofs])
+    rest = np.setdiff1d(np.arange(len(w)), dofs)
+    assert np.all(wp[rest] == 0)

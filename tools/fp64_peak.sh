@@ -20,7 +20,7 @@ out = {"fp64_fma_tflops": max(r["fp64_fma_tflops"] for r in runs), "runs": [r["f
        "per thread, best of 5 launches, best of 3 runs",
        "clocks": {"sm_mhz_median_under_load": statistics.median(busy), "sm_max_mhz": float(clk[0][1]),
                   "samples": len(clk), "reasons": sorted({c[2].strip() for c in clk})}}
-json.dump(out, open("profiles/fp64_peak.json", "w"), indent=1)
+json.dump(out, open("gpurun_out/fp64_peak.json", "w"), indent=1)  # copy to profiles/ by hand
 print(json.dumps(out))
 PY
 cat gpurun_out/fp64_sweep.jsonl
