@@ -57,7 +57,7 @@ struct CellArgs {
   S* csr;
   int64_t diag_off;        // column of row i's diagonal = i + diag_off (local tensors of a partition)
   bool chain32;            // chain is 32-byte aligned (one 256-bit load per cell row)
-  int pf;                  // rows ahead whose value span is bulk-prefetched into L2 (0: none)
+  int pf;                  // apply-only kernel: prefetch the value span of the warp's rows 2 steps ahead
 };
 
 __device__ __forceinline__ uint32_t smem_u32(const void* p) { return (uint32_t)__cvta_generic_to_shared(p); }
@@ -408,21 +408,15 @@ __global__ void __launch_bounds__(cell_threads<S, JAC>(),
     int fj_nn[FREG], fb_nn[FREG];
     fibers(nn, fj_nn, fb_nn);
     const Meta n3 = meta(A, row + 3 * NG);
-    if constexpr (!WB) {
-      // the values of a row go straight to registers when its turn comes: one bulk L2 prefetch
-      // of the contiguous value span of the row A.pf steps ahead, so that load waits on L2, not HBM
-      // (A.pf > 0: per group; A.pf < 0: one prefetch per warp of its groups' contiguous span)
-      if (A.pf != 0) {
-        const int ahead = A.pf > 0 ? A.pf : -A.pf;
-        const Meta& mp = ahead == 2 ? nn : (ahead == 3 ? n3 : nxt);
-        uint32_t pe0 = mp.e0, pe1 = mp.e1;
-        bool issue = lane == 0;
-        if (A.pf < 0) {
-          pe0 = __shfl_sync(FM, mp.e0, 0);
-          pe1 = __reduce_max_sync(FM, mp.e1);
-          issue = (threadIdx.x & 31) == 0;
-        }
-        if (issue && pe1 > pe0) {
+    if constexpr (!WB && JAC == kJacNone) {
+      // apply-only: the values of a row go straight to registers when its turn comes; one bulk L2
+      // prefetch per warp of its rows' contiguous value span two steps ahead, so that load waits
+      // on L2, not HBM (cfg4 fp64 apply 0.411 -> 0.373 ms).  The Jacobian kernels are LSU-bound,
+      // not waiting on HBM: the same prefetch measured slower there (fused 0.715 -> 0.72-0.795 ms).
+      if (A.pf) {
+        const uint32_t pe0 = __shfl_sync(FM, nn.e0, 0);
+        const uint32_t pe1 = __reduce_max_sync(FM, nn.e1);
+        if ((threadIdx.x & 31) == 0 && pe1 > pe0) {
           const char* lo;
           uint32_t nb;
           span16(A.ck_val + pe0, (int)(pe1 - pe0), &lo, &nb);
@@ -735,11 +729,8 @@ egfem_status cells_dispatch(const egfem_tensor* t, bool do_r, int jac, const voi
   A.diag_off = t->row_begin - t->col_begin;
   A.chain32 = (reinterpret_cast<uintptr_t>(chain) & 31u) == 0;
   static int pf_env = -1;
-  if (pf_env < 0) pf_env = getenv("EGFEM_CELLS_PF") ? atoi(getenv("EGFEM_CELLS_PF")) + 100 : 0;
-  // measured on cfg4 fp64: one prefetch per warp 2 rows ahead speeds the apply-only kernel up
-  // (0.411 -> 0.373 ms); the Jacobian kernels are not waiting on HBM (LSU-bound) and per-group or
-  // 1/3-rows-ahead prefetches slow them down (fused 0.715 -> 0.72-0.795 ms)
-  A.pf = pf_env ? pf_env - 100 : (jac == kJacNone ? -2 : 0);
+  if (pf_env < 0) pf_env = getenv("EGFEM_CELLS_PF") ? (atoi(getenv("EGFEM_CELLS_PF")) != 0) : 1;
+  A.pf = pf_env;
   CellCfg c{};
   if (!pick_cells(t, &c)) {
     set_error("no cell-major configuration");
