@@ -1,4 +1,4 @@
-"""Online Picard iteration of the EGFEM (§4 Example L235–270, §5).
+"""Online Picard and Newton iterations of the EGFEM (§4, §5).
 
 For a problem of the form
 
@@ -26,8 +26,8 @@ from dataclasses import dataclass
 
 import numpy as np
 
-from . import (F64, FORM_MASS3, FORM_PLAP, INTERP_IDENTITY, JAC_PICARD, Tensor, egfem_bilinear_build,
-               egfem_csr_spmv, egfem_interp, egfem_jacobian, egfem_tensor_build)
+from . import (F64, FORM_MASS3, FORM_PLAP, INTERP_IDENTITY, JAC_NEWTON, JAC_PICARD, Tensor, egfem_apply,
+               egfem_bilinear_build, egfem_csr_spmv, egfem_interp, egfem_jacobian, egfem_tensor_build)
 
 
 @dataclass
@@ -168,4 +168,234 @@ def biochemical_problem(n: int, device: int = 0, W: str = "P1"):
     d_nodal = -(2 * x[:, 0] + 2 * x[:, 1]) + ue / (1.0 + ue)
     from . import INTERP_RECIPROCAL
     s = PicardEGFEM(mesh, V, T, INTERP_RECIPROCAL, 1.0, nu=1.0, device=device)
+    return s, s.source(d_nodal), ue
+
+
+# ----------------------------------------------------------------------------- Newton (F4)
+@dataclass
+class NewtonResult:
+    u: np.ndarray
+    iterations: int
+    converged: bool
+    status: str                 # "converged" | "diverged" | "maxit" | "krylov"
+    residuals: list             # ‖F(u^n)‖₂ over the free rows, before each step
+    increments: list            # ‖δ^n‖_∞
+    damping: list               # step length taken (1 = full Newton step)
+    krylov_iterations: list
+
+
+class NewtonEGFEM(PicardEGFEM):
+    """Newton's method for ν K u + T:(u ⊗ w(u)) = d with Dirichlet data.
+
+    Per iteration, on the device:
+        w = interp(u) with D_u w                    egfem_interp (+ chain)          (step 1)
+        F = ν K u + T:(u ⊗ w) − d                   egfem_apply + CSR SpMV           (step 2)
+        J = ν K + T·w + (T·₂u)·D_u w                egfem_jacobian(NEWTON)           (step 3)
+        J δ = −F on the free rows (Dirichlet rows / columns eliminated, δ = 0 on Γ),
+        right-Jacobi-preconditioned restarted GMRES whose products are egfem_csr_spmv
+        u ← u + λ δ with λ = 1, halved while ‖F(u + λδ)‖ does not decrease (backtracking;
+        PAPER.md L296 leaves damping open — reading F4 in DESIGN.md)
+    The reduced Jacobian is the Schur complement of the paper's block Jacobian D_z F̃ (L290) once
+    the identity blocks of the intermediate variables are eliminated (reading C10); it needs
+    no integration, only the precomputed tensor and the pointwise D_u w (L292).  Stops when
+    ‖δ‖_∞ ≤ tol (L304: O(1e-12)); reports "diverged" when ‖F‖ becomes non-finite or exceeds
+    `div_factor`·‖F(u⁰)‖, or the line search fails."""
+
+    def __init__(self, mesh, V, T: Tensor, kind: int, p: float, nu: float = 1.0, device: int = 0,
+                 cell_wise: bool | None = None):
+        super().__init__(mesh, V, T, kind, p, nu=nu, device=device)
+        torch = self.torch
+        # cell-wise W (P0 / QUAD) carries D_u w as chain rows (include/egfem.h egfem_interp)
+        cell_wise = (T.n_f != T.n_u) if cell_wise is None else cell_wise
+        self.chain = (torch.empty(T.n_f * (mesh.dim + 1), dtype=torch.float64, device=self.dev)
+                      if cell_wise else None)
+        self.free = (~self.bnd).to(torch.float64)
+
+    def residual(self, u, d_vec, w):
+        """F(u) = ν K u + T:(u ⊗ w(u)) − d (w from egfem_interp of u); zero on the Dirichlet rows."""
+        torch = self.torch
+        egfem_interp(self.T, self.kind, self.p, u, w, self.chain)
+        r = torch.empty_like(u)
+        egfem_apply(self.T, u, w, r)
+        if self.nu != 0.0:
+            ku = torch.empty_like(u)
+            egfem_csr_spmv(self.T, self.K, u, ku)
+            r = r + self.nu * ku
+        return (r - d_vec) * self.free
+
+    def _gmres(self, A, b, tol, restart, maxit):
+        """Right-Jacobi-preconditioned restarted GMRES(m) for A x = b (A on the CSR pattern,
+        eliminated).  Arnoldi with classical Gram-Schmidt twice, Givens rotations."""
+        torch = self.torch
+        dinv = 1.0 / self._diag(A)
+        n = b.numel()
+        x = torch.zeros_like(b)
+        bnorm = torch.linalg.vector_norm(b).item()
+        if bnorm == 0.0:
+            return x, 0, True
+        total = 0
+        Av = torch.empty_like(b)
+        while total < maxit:
+            egfem_csr_spmv(self.T, A, x, Av)
+            r = b - Av
+            beta = torch.linalg.vector_norm(r).item()
+            if beta <= tol * bnorm:
+                return x, total, True
+            m = min(restart, maxit - total)
+            Vb = torch.empty((m + 1, n), dtype=b.dtype, device=b.device)
+            Hm = np.zeros((m + 1, m))
+            Vb[0] = r / beta
+            cs, sn = np.zeros(m), np.zeros(m)
+            g = np.zeros(m + 1)
+            g[0] = beta
+            k_done = 0
+            for k in range(m):
+                egfem_csr_spmv(self.T, A, Vb[k] * dinv, Av)
+                wv = Av.clone()
+                for _ in range(2):  # CGS2
+                    h = Vb[:k + 1] @ wv
+                    wv -= h @ Vb[:k + 1]
+                    Hm[:k + 1, k] += h.cpu().numpy()
+                hn = torch.linalg.vector_norm(wv).item()
+                Hm[k + 1, k] = hn
+                if hn > 0:
+                    Vb[k + 1] = wv / hn
+                for i in range(k):  # apply the previous rotations to column k
+                    t0 = cs[i] * Hm[i, k] + sn[i] * Hm[i + 1, k]
+                    Hm[i + 1, k] = -sn[i] * Hm[i, k] + cs[i] * Hm[i + 1, k]
+                    Hm[i, k] = t0
+                den = np.hypot(Hm[k, k], Hm[k + 1, k])
+                cs[k], sn[k] = (1.0, 0.0) if den == 0 else (Hm[k, k] / den, Hm[k + 1, k] / den)
+                Hm[k, k] = cs[k] * Hm[k, k] + sn[k] * Hm[k + 1, k]
+                Hm[k + 1, k] = 0.0
+                g[k + 1] = -sn[k] * g[k]
+                g[k] = cs[k] * g[k]
+                total += 1
+                k_done = k + 1
+                if abs(g[k + 1]) <= tol * bnorm or hn == 0:
+                    break
+            y = np.linalg.solve(np.triu(Hm[:k_done, :k_done]), g[:k_done]) if k_done else np.zeros(0)
+            yt = torch.tensor(y, dtype=b.dtype, device=b.device)
+            x += (yt @ Vb[:k_done]) * dinv
+            if abs(g[k_done]) <= tol * bnorm:
+                egfem_csr_spmv(self.T, A, x, Av)
+                return x, total, bool(torch.linalg.vector_norm(b - Av).item() <= 10 * tol * bnorm)
+        return x, total, False
+
+    def solve(self, d_vec, g_nodal: np.ndarray, u0: np.ndarray | None = None, tol: float = 1e-12,
+              maxit: int = 50, krylov_tol: float = 1e-13, restart: int = 60, krylov_maxit: int = 3000,
+              div_factor: float = 1e6, max_halvings: int = 30, damping: bool = True,
+              initial: str = "laplace") -> NewtonResult:
+        """u0: initial guess (its boundary values are replaced by g); None and initial="laplace":
+        the solution of K u = d with the same Dirichlet data (the p = 2 / a ≡ 1 problem — the
+        degenerate p-Laplacian has a singular Jacobian at ∇u = 0, so u0 = 0 cannot start it);
+        initial="zero": u0 = 0 in the interior."""
+        torch = self.torch
+        T = self.T
+        g = torch.tensor(g_nodal, dtype=torch.float64, device=self.dev)
+        if u0 is not None:
+            u = torch.tensor(u0, dtype=torch.float64, device=self.dev)
+        elif initial == "laplace":
+            lift = torch.empty_like(g)
+            egfem_csr_spmv(T, self.K * self.lift, g, lift)
+            b = torch.where(self.bnd, g, d_vec - lift)
+            u, _ = self._cg(self.K * self.keep + self.dbnd, b, torch.where(self.bnd, g, torch.zeros_like(g)),
+                            1e-14, 20000)
+        else:
+            u = torch.zeros_like(g)
+        u = torch.where(self.bnd, g, u)
+        w = torch.empty(T.n_f, dtype=torch.float64, device=self.dev)
+        J = torch.empty(T.nnz_csr, dtype=torch.float64, device=self.dev)
+        F = self.residual(u, d_vec, w)
+        f0 = torch.linalg.vector_norm(F).item()
+        res, incs, lams, kits = [f0], [], [], []
+        status = "maxit"
+        if not np.isfinite(f0):
+            return NewtonResult(u.cpu().numpy(), 0, False, "diverged", res, incs, lams, kits)
+        for n in range(1, maxit + 1):
+            # J at u (the last residual evaluated w and the chain at u)
+            egfem_jacobian(T, JAC_NEWTON, self.kind, self.p, u, w, self.chain, J)
+            A = J + self.nu * self.K if self.nu != 0.0 else J
+            Ae = A * self.keep + self.dbnd
+            delta, it, ok = self._gmres(Ae, -F, krylov_tol, restart, krylov_maxit)
+            kits.append(it)
+            if not ok:
+                status = "krylov"
+                break
+            fn = res[-1]
+            lam = 1.0
+            for _ in range(max_halvings + 1):
+                u_try = u + lam * delta
+                F_try = self.residual(u_try, d_vec, w)
+                f_try = torch.linalg.vector_norm(F_try).item()
+                if not damping or (np.isfinite(f_try) and (f_try < fn or f_try <= 1e-12 * f0)):
+                    break
+                lam *= 0.5
+            else:
+                status = "diverged"
+                break
+            inc = lam * torch.max(torch.abs(delta)).item()
+            u, F = u_try, F_try
+            res.append(f_try)
+            incs.append(inc)
+            lams.append(lam)
+            if not np.isfinite(f_try) or f_try > div_factor * max(f0, 1e-300):
+                status = "diverged"
+                break
+            if inc <= tol:
+                status = "converged"
+                break
+        return NewtonResult(u.cpu().numpy(), len(incs), status == "converged", status, res, incs, lams, kits)
+
+
+def _square_source(name: str, x: np.ndarray, p: float = 4.0) -> np.ndarray:
+    """Manufactured sources on the unit square for u = x1 x2 (x1 + x2):
+    g = ∇u = (2 x1 x2 + x2², x1² + 2 x1 x2), H = ∇²u = [[2 x2, 2(x1+x2)], [2(x1+x2), 2 x1]].
+      minsurf:  d = −∇·(g / √(1+|g|²)) = −Δu/√s + gᵀHg / s^{3/2},  s = 1 + |g|²   (L600–605)
+      plap:     d = −∇·(|g|^{p−2} g) = −|g|^{p−2} Δu − (p−2)|g|^{p−4} gᵀHg          (L568–574)"""
+    x1, x2 = x[:, 0], x[:, 1]
+    g1, g2 = 2 * x1 * x2 + x2 ** 2, x1 ** 2 + 2 * x1 * x2
+    h11, h12, h22 = 2 * x2, 2 * (x1 + x2), 2 * x1
+    lap = h11 + h22
+    gHg = g1 * g1 * h11 + 2 * g1 * g2 * h12 + g2 * g2 * h22
+    gg = g1 * g1 + g2 * g2
+    if name == "minsurf":
+        s = 1.0 + gg
+        return -lap / np.sqrt(s) + gHg / s ** 1.5
+    gn = np.sqrt(gg)
+    with np.errstate(divide="ignore", invalid="ignore"):
+        t = np.where(gg > 0, (p - 2) * gn ** (p - 4) * gHg, 0.0)
+    return -(gn ** (p - 2)) * lap - t
+
+
+def quasilinear_problem(name: str, n: int, p: float | None = 4.0, device: int = 0):
+    """PAPER.md §5.5 / §5.6 on the unit square with the manufactured solution u = x1 x2 (x1+x2)
+    (the paper's §5.6 boundary data, L601; §5.5's disk solution needs a curved mesh, so the
+    p-Laplace source is manufactured the same way): T = K_a (PLAP, W = P0), a = |∇u|^{p−2}
+    (GRADPOW_P0) or (1+|∇u|²)^{−1/2} (MINSURF_P0), ν = 0, d = M d_h.  Returns (solver, d, u_exact)."""
+    import egfem_inputs as I
+    from . import INTERP_GRADPOW_P0, INTERP_MINSURF_P0
+    mesh = I.mesh_square(n)
+    V = I.space_p1(mesh)
+    T = egfem_tensor_build(mesh, V, I.space_p0(mesh), FORM_PLAP, dtype=F64, device=device)
+    x = mesh.coords
+    ue = x[:, 0] * x[:, 1] * (x[:, 0] + x[:, 1])
+    kind = INTERP_MINSURF_P0 if name == "minsurf" else INTERP_GRADPOW_P0
+    p = 4.0 if p is None else float(p)  # ignored by MINSURF_P0
+    s = NewtonEGFEM(mesh, V, T, kind, p, nu=0.0, device=device)
+    return s, s.source(_square_source(name, x, p)), ue
+
+
+def biochemical_newton(n: int, device: int = 0, W: str = "P1"):
+    """The §5.4 biochemical problem (see biochemical_problem) solved by Newton."""
+    import egfem_inputs as I
+    from . import INTERP_RECIPROCAL
+    mesh = I.mesh_square(n)
+    V = I.space_p1(mesh)
+    Wsp = V if W == "P1" else I.space_p0(mesh)
+    T = egfem_tensor_build(mesh, V, Wsp, FORM_MASS3, dtype=F64, device=device)
+    x = mesh.coords
+    ue = x[:, 0] * x[:, 1] * (x[:, 0] + x[:, 1])
+    d_nodal = -(2 * x[:, 0] + 2 * x[:, 1]) + ue / (1.0 + ue)
+    s = NewtonEGFEM(mesh, V, T, INTERP_RECIPROCAL, 1.0, nu=1.0, device=device)
     return s, s.source(d_nodal), ue
