@@ -770,7 +770,7 @@ egfem_status launch_cells(const egfem_tensor* t, bool do_r, int jac, const void*
 // silently skipped otherwise (the canonical row / tile kernels then serve the tensor).
 egfem_status make_p0_cells(egfem_tensor* t) {
   if (!t->has_mesh || !t->w_p0 || !t->nz_aux || (t->dim != 2 && t->dim != 3) || t->n_u <= 0 || t->nnz <= 0 ||
-      t->max_row_nnz > kRowsMaxNnz)
+      t->max_row_nnz > kCellsMaxNnz)
     return EGFEM_OK;
   const int d1 = t->dim + 1;
   const size_t vs = t->dtype == EGFEM_F64 ? 8 : 4;

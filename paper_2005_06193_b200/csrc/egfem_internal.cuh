@@ -35,7 +35,9 @@ constexpr uint32_t kKMask = (1u << kKShift) - 1u;   // k of a P0-W tensor
 constexpr uint32_t kKMaskAny = 0x7FFFFFFFu;          // k of any other tensor
 constexpr uint32_t kHead = 0x80000000u;              // bit 31: first nonzero of a fiber
 constexpr int kMaxQuad = 16;
-constexpr int kRowsMaxNnz = 256;  // rows up to this length take the row-group path
+constexpr int kRowsMaxNnz = 512;   // rows up to this length take the row-group path (k_seg)
+constexpr int kCellsMaxNnz = 256;  // cell-major copy: canonical position in a row fits 8 bits
+constexpr int kWVMaxNnz = 256;     // W = V Newton transpose data: position in a row fits 8 bits
 
 void set_error(const std::string& msg);
 void count_launch(int n = 1);

@@ -133,7 +133,7 @@ struct SegSmem {
 };
 
 template <typename S, int G, int NCH, int FREG, bool DO_R, int JAC, int D1>
-__global__ void __launch_bounds__(256, (JAC == kJacNewtonP0 || JAC == kJacNewtonWV) ? 3 : 4) k_seg(const RowArgs<S> A) {
+__global__ void __launch_bounds__(256, NCH > 8 ? 2 : ((JAC == kJacNewtonP0 || JAC == kJacNewtonWV) ? 3 : 4)) k_seg(const RowArgs<S> A) {
   using L = SegSmem<S, G, NCH, JAC>;
   constexpr int GPB = 256 / G;
   constexpr bool kP0 = L::kP0, kWV = L::kWV;
@@ -443,7 +443,9 @@ void rows_config(const egfem_tensor* t, int* G, int* NCH) {
   else if (mx <= 64) { *G = 16; *NCH = 4; }
   else if (mx <= 96) { *G = 16; *NCH = 6; }  // two rows per warp instruction
   else if (mx <= 128) { *G = 32; *NCH = 4; }
-  else { *G = 32; *NCH = 8; }
+  else if (mx <= 256) { *G = 32; *NCH = 8; }
+  else if (mx <= 384) { *G = 32; *NCH = 12; }  // 3D quadrature-point W (I_2: 384 per row)
+  else { *G = 32; *NCH = 16; }
 }
 
 template <typename S>
@@ -482,6 +484,8 @@ egfem_status rows_dispatch(const egfem_tensor* t, bool do_r, int jac, egfem_inte
   EGFEM_RC(32, 3)
   EGFEM_RC(32, 4)
   EGFEM_RC(32, 8)
+  EGFEM_RC(32, 12)
+  EGFEM_RC(32, 16)
 #undef EGFEM_RC
   set_error("no row-group configuration");
   return EGFEM_ERR_UNSUPPORTED;
@@ -505,9 +509,9 @@ egfem_status launch_rows(const egfem_tensor* t, bool do_r, int jac, egfem_interp
   return rows_dispatch<float>(t, do_r, jac, kind, p, u, w, chain, r, csr_vals, s);
 }
 
-// Offline W = V Newton data for the row kernels (rows of at most kRowsMaxNnz nonzeros).
+// Offline W = V Newton data for the row kernels (rows of at most kWVMaxNnz nonzeros).
 egfem_status make_wv_aux(egfem_tensor* t) {
-  if (!t->w_is_v || !t->newton_wv_ok || t->n_u <= 0 || t->max_row_nnz > kRowsMaxNnz) return EGFEM_OK;
+  if (!t->w_is_v || !t->newton_wv_ok || t->n_u <= 0 || t->max_row_nnz > kWVMaxNnz) return EGFEM_OK;
   EGFEM_CUDA_TRY(dmalloc_padded((void**)&t->nz_kpos, std::max<int64_t>(t->nnz, 1)));
   EGFEM_CUDA_TRY(dmalloc_padded((void**)&t->fib_kr, std::max<int64_t>(t->n_fib, 1)));
   k_wv_aux<<<(int)((t->n_u + 127) / 128), 128>>>(t->n_u, t->row_fib, t->fib_nz, t->fib_j, t->nz_k, t->nz_kpos,
