@@ -290,7 +290,7 @@ egfem_status egfem_interp_range(const egfem_tensor* t, egfem_interp_kind kind, d
 
 /* egfem_apply_jacobian restricted to rows [row_lo, row_hi) (r and csr_vals are the
  * whole-tensor buffers; only those rows' entries are written).  A proper sub-range needs
- * one of the row-group kernels (rows of at most 256 nonzeros); the general tile path
+ * one of the row-group kernels (rows of at most 512 nonzeros); the general tile path
  * returns UNSUPPORTED for it. */
 egfem_status egfem_apply_jacobian_rows(const egfem_tensor* t, egfem_jac_mode mode, egfem_interp_kind kind,
                                        double p, const void* u, const void* w, const void* chain, void* r,
