@@ -185,8 +185,13 @@ egfem_status egfem_tensor_export(const egfem_tensor* t, int64_t* t_row_ptr, int3
 /* ---------------------------------------------------------------- per iteration
  * (1) w = f(Π_u u, Π_∇u ·₂ u) at every W-DOF.
  * u: device [N_u]; w: device [N_f].  chain (nullable; cell-wise W = P0 or QUAD only):
- * device [N_f*(d+1)], chain[k*(d+1)+m] = ∂w_k/∂u_{v_m} for the cell K owning W-DOF k (the
- * pointwise D_u w of PAPER.md L292), consumed by egfem_jacobian NEWTON.  p > 1 required for GRADPOW_P0; p is k of RECIPROCAL (any value; p + u = 0
+ * device [N_f*(d+1)], the pointwise D_u w of PAPER.md L292 for the cell K owning W-DOF k
+ * (v_0..v_d its vertices), consumed by egfem_jacobian NEWTON with the same kind:
+ *   RECIPROCAL, SQUARE:        chain[k*(d+1)+m] = ∂w_k/∂u_{v_m}, m = 0..d;
+ *   GRADPOW_P0, MINSURF_P0:    chain[k*(d+1)] = w_k and chain[k*(d+1)+1+m] = ∂w_k/∂u_{v_m},
+ *                              m = 0..d−1 (packed: ∂w_k/∂u_{v_d} = −Σ_{m<d} ∂w_k/∂u_{v_m},
+ *                              exact because w depends on u through ∇u_h and Σ_m ∇λ_m = 0),
+ *                              so the Newton kernel reads a cell's w and D_u w with one gather.  p > 1 required for GRADPOW_P0; p is k of RECIPROCAL (any value; p + u = 0
  * gives ±inf); p ignored otherwise.  At ∇u_h|_K = 0 and p < 4 the GRADPOW derivative is
  * taken as 0 (reading C11). */
 egfem_status egfem_interp(const egfem_tensor* t, egfem_interp_kind kind, double p, const void* u,

@@ -31,7 +31,9 @@
 namespace egfem {
 namespace {
 
-enum { kJacNone = 0, kJacPicard = 1, kJacNewtonP0 = 3 };
+// kJacNewtonPK: P0 Newton with the packed chain of the gradient kinds (include/egfem.h
+// egfem_interp: [w_K, ∂w/∂u_0 .. ∂w/∂u_{d−1}], ∂w/∂u_d = −Σ: one gather per cell)
+enum { kJacNone = 0, kJacPicard = 1, kJacNewtonP0 = 3, kJacNewtonPK = 4 };
 // threads per CTA: 256 for the fp64 Newton / apply kernels (2-3 CTAs/SM), 128 for fp32 and for
 // the fp64 Picard matrix (measured on cfg4: fp32 fused 0.51 -> 0.47 ms, fp64 Picard 0.51 ->
 // 0.48 ms; fp64 fused is faster with 256)
@@ -301,11 +303,12 @@ template <typename S, int D1, int G, int CPL, int FREG, bool DO_R, int JAC, bool
 __global__ void __launch_bounds__(cell_threads<S, JAC>(),
                                   (JAC == kJacNone || G >= 16) ? 3 * 256 / cell_threads<S, JAC>() : 2 * 256 / cell_threads<S, JAC>())
     k_cell(const CellArgs<S> A) {
-  constexpr bool SU = cells_su<S, FREG, JAC>() && (DO_R || JAC == kJacNewtonP0);
+  constexpr bool kN = JAC == kJacNewtonP0 || JAC == kJacNewtonPK;
+  constexpr bool kPK = JAC == kJacNewtonPK;
+  constexpr bool SU = cells_su<S, FREG, JAC>() && (DO_R || kN);
   using L = CellSmem<S, D1, G, CPL, JAC != kJacNone, SU ? G * FREG : 0>;
   constexpr int GPB = cell_threads<S, JAC>() / G;
   constexpr bool kJ = JAC != kJacNone;
-  constexpr bool kN = JAC == kJacNewtonP0;
   constexpr bool kU = DO_R || kN;  // u (and B_iK) needed; the Picard matrix alone reads no u
   // Control flow is warp-uniform (a group past the last row runs on an empty one), so
   // every shuffle uses the full mask with width G.
@@ -454,7 +457,7 @@ __global__ void __launch_bounds__(cell_threads<S, JAC>(),
       const int q = lane + c * G;
       const bool ok = q < nc;
       const uint32_t K = ok ? bk[q] : 0u;
-      wk[c] = ok ? __ldg(A.w + K) : S(0);
+      if constexpr (!kPK) wk[c] = ok ? __ldg(A.w + K) : S(0);
       if constexpr (kN) {
         // the cell's D1 values (16-byte vector loads); a lane past the row's cells loads cell 0's
         // row and never uses it (no select on the loaded value)
@@ -463,6 +466,16 @@ __global__ void __launch_bounds__(cell_threads<S, JAC>(),
         } else {
 #pragma unroll
           for (int m = 0; m < D1; ++m) dd[c][m] = __ldg(A.chain + (size_t)K * D1 + m);
+        }
+        if constexpr (kPK) {  // packed record [w_K, D_0 .. D_{d−1}]: D_d = −Σ_{m<d} D_m
+          wk[c] = ok ? dd[c][0] : S(0);
+          S sd = S(0);
+#pragma unroll
+          for (int m = 0; m + 1 < D1; ++m) {
+            dd[c][m] = dd[c][m + 1];
+            sd = xadd(sd, dd[c][m]);
+          }
+          dd[c][D1 - 1] = -sd;
         }
       }
     }
@@ -649,11 +662,11 @@ bool cells_warp_bulk(int G, int vbytes) {
 
 template <typename S, int D1, int G, int CPL, int FREG, bool DO_R, int JAC>
 egfem_status run_cells(const egfem_tensor* t, const CellArgs<S>& A, cudaStream_t s) {
-  constexpr bool SU = cells_su<S, FREG, JAC>() && (DO_R || JAC == kJacNewtonP0);
+  constexpr bool SU = cells_su<S, FREG, JAC>() && (DO_R || JAC == kJacNewtonP0 || JAC == kJacNewtonPK);
   using L = CellSmem<S, D1, G, CPL, JAC != kJacNone, SU ? G * FREG : 0>;
   const bool wb = cells_warp_bulk(G, (int)sizeof(S));
   auto fn = wb ? k_cell<S, D1, G, CPL, FREG, DO_R, JAC, true> : k_cell<S, D1, G, CPL, FREG, DO_R, JAC, false>;
-  if constexpr (JAC == kJacNewtonP0 && D1 == 4 && sizeof(S) == 8) {
+  if constexpr ((JAC == kJacNewtonP0 || JAC == kJacNewtonPK) && D1 == 4 && sizeof(S) == 8) {
     if (A.chain32)
       fn = wb ? k_cell<S, D1, G, CPL, FREG, DO_R, JAC, true, true> : k_cell<S, D1, G, CPL, FREG, DO_R, JAC, false, true>;
   }
@@ -674,13 +687,16 @@ egfem_status run_cells(const egfem_tensor* t, const CellArgs<S>& A, cudaStream_t
 }
 
 template <typename S, int D1, int G, int CPL, int FREG>
-egfem_status cells_mode(const egfem_tensor* t, const CellArgs<S>& A, bool do_r, int jac, cudaStream_t s) {
+egfem_status cells_mode(const egfem_tensor* t, const CellArgs<S>& A, bool do_r, int jac, bool packed,
+                        cudaStream_t s) {
   if (do_r) {
     if (jac == kJacNone) return run_cells<S, D1, G, CPL, FREG, true, kJacNone>(t, A, s);
     if (jac == kJacPicard) return run_cells<S, D1, G, CPL, FREG, true, kJacPicard>(t, A, s);
+    if (packed) return run_cells<S, D1, G, CPL, FREG, true, kJacNewtonPK>(t, A, s);
     return run_cells<S, D1, G, CPL, FREG, true, kJacNewtonP0>(t, A, s);
   }
   if (jac == kJacPicard) return run_cells<S, D1, G, CPL, FREG, false, kJacPicard>(t, A, s);
+  if (packed) return run_cells<S, D1, G, CPL, FREG, false, kJacNewtonPK>(t, A, s);
   return run_cells<S, D1, G, CPL, FREG, false, kJacNewtonP0>(t, A, s);
 }
 
@@ -710,7 +726,7 @@ bool pick_cells(const egfem_tensor* t, CellCfg* out) {
 }
 
 template <typename S>
-egfem_status cells_dispatch(const egfem_tensor* t, bool do_r, int jac, const void* u, const void* w,
+egfem_status cells_dispatch(const egfem_tensor* t, bool do_r, int jac, bool packed, const void* u, const void* w,
                             const void* chain, void* r, void* csr, cudaStream_t s) {
   CellArgs<S> A;
   A.n_u = t->n_u;
@@ -739,7 +755,7 @@ egfem_status cells_dispatch(const egfem_tensor* t, bool do_r, int jac, const voi
   if (getenv("EGFEM_DEBUG"))
     fprintf(stderr, "[egfem] k_cell d1=%d G=%d CPL=%d FREG=%d do_r=%d jac=%d\n", c.d1, c.G, c.CPL, c.FREG, (int)do_r, jac);
 #define EGFEM_CC(D_, G_, C_, F_) \
-  if (c.d1 == D_ && c.G == G_ && c.CPL == C_) return cells_mode<S, D_, G_, C_, F_>(t, A, do_r, jac, s);
+  if (c.d1 == D_ && c.G == G_ && c.CPL == C_) return cells_mode<S, D_, G_, C_, F_>(t, A, do_r, jac, packed, s);
   EGFEM_CC(3, 2, 3, 4)
   EGFEM_CC(3, 4, 4, 8)
   EGFEM_CC(3, 16, 3, 1)
@@ -759,11 +775,11 @@ bool cells_path_ok(const egfem_tensor* t, int jac) {
   return pick_cells(t, &c);
 }
 
-egfem_status launch_cells(const egfem_tensor* t, bool do_r, int jac, const void* u, const void* w, const void* chain,
-                          void* r, void* csr_vals, cudaStream_t s) {
+egfem_status launch_cells(const egfem_tensor* t, bool do_r, int jac, bool packed, const void* u, const void* w,
+                          const void* chain, void* r, void* csr_vals, cudaStream_t s) {
   if (t->n_u <= 0) return EGFEM_OK;
-  if (t->dtype == EGFEM_F64) return cells_dispatch<double>(t, do_r, jac, u, w, chain, r, csr_vals, s);
-  return cells_dispatch<float>(t, do_r, jac, u, w, chain, r, csr_vals, s);
+  if (t->dtype == EGFEM_F64) return cells_dispatch<double>(t, do_r, jac, packed, u, w, chain, r, csr_vals, s);
+  return cells_dispatch<float>(t, do_r, jac, packed, u, w, chain, r, csr_vals, s);
 }
 
 // Offline: cell-major copy for P0-W tensors of 2D/3D meshes whose rows fit the kernel;

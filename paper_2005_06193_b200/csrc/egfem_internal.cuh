@@ -135,8 +135,8 @@ egfem_status launch_rows(const egfem_tensor* t, bool do_r, int jac, egfem_interp
 bool rows_path_ok(const egfem_tensor* t, int jac);
 egfem_status make_wv_aux(egfem_tensor* t);
 bool cells_path_ok(const egfem_tensor* t, int jac);
-egfem_status launch_cells(const egfem_tensor* t, bool do_r, int jac, const void* u, const void* w, const void* chain,
-                          void* r, void* csr_vals, cudaStream_t s);
+egfem_status launch_cells(const egfem_tensor* t, bool do_r, int jac, bool packed, const void* u, const void* w,
+                          const void* chain, void* r, void* csr_vals, cudaStream_t s);
 egfem_status make_p0_cells(egfem_tensor* t);
 bool dense_path_ok(const egfem_tensor* t);
 bool dense1_path_ok(const egfem_tensor* t, int jac);
@@ -155,6 +155,11 @@ bool group_path_ok(const egfem_tensor* t, egfem_layout layout);
 egfem_status launch_groups(const egfem_tensor* t, int32_t batch, const void* U, const void* W, void* R,
                            cudaStream_t s);
 const char* group_plan_info(const egfem_tensor* t);
+// the gradient kinds' Newton data is the packed chain record [w_k, ∂w/∂u_0 .. ∂w/∂u_{d−1}]
+// (include/egfem.h egfem_interp); the other cell-wise kinds store D_u w in full
+inline bool packed_chain_kind(egfem_interp_kind kind) {
+  return kind == EGFEM_INTERP_GRADPOW_P0 || kind == EGFEM_INTERP_MINSURF_P0;
+}
 egfem_status group_compile_key(const int32_t* key, int32_t len, int P, int f64, std::string* log);
 // the kernel family an entry point dispatches to (0 apply, 1 jacobian, 2 apply_jacobian,
 // 3 apply_batched node-major; jac = the Jacobian mode code)

@@ -43,7 +43,8 @@ __global__ void k_interp_copy(const S* __restrict__ u, S* __restrict__ w, int64_
 }
 
 // GRADPOW_P0: g_K = Σ_a u_{v_a} ∇λ_a (Π_∇u ·₂ u at the cell's DOF), w_K = ‖g_K‖^{p−2},
-// chain[K][m] = ∂w_K/∂u_{v_m} = (p−2)‖g‖^{p−4} g·∇λ_m (reading C11).
+// ∂w_K/∂u_{v_m} = (p−2)‖g‖^{p−4} g·∇λ_m (reading C11); chain[K] = [w_K, ∂w_K/∂u_{v_0}
+// .. ∂w_K/∂u_{v_{d−1}}] (packed: the last derivative is −Σ of the others).
 // Thread per cell; 3D reads the cell as one int4 and each vertex as two double2 from the
 // 32-byte padded coordinate array, and writes the chain row as two 16-byte stores.
 template <int D>
@@ -178,14 +179,18 @@ __device__ __forceinline__ void gradpow_cell(const CellIn<S, D>& in, int64_t c, 
     wk = pow(gg, 0.5 * (p - 2.0));
     fac = gg > 0.0 ? (p - 2.0) * pow(gg, 0.5 * (p - 4.0)) : 0.0;
   }
+  // the packed chain record (include/egfem.h egfem_interp): [w_K, ∂w/∂u_{v_0} .. ∂w/∂u_{v_{d−1}}];
+  // ∂w/∂u_{v_d} = −Σ_{m<d} (Σ_m ∇λ_m = 0), rebuilt by the Jacobian kernels — so the Newton kernel
+  // reads w and D_u w of a cell with one gather
   S dm[D + 1];
   if (chain) {
+    dm[0] = (S)wk;
 #pragma unroll
-    for (int a = 0; a <= D; ++a) {
+    for (int a = 0; a < D; ++a) {
       double s = 0.0;
 #pragma unroll
       for (int q = 0; q < D; ++q) s += gu[q] * g[a][q];
-      dm[a] = (S)(fac * s);
+      dm[a + 1] = (S)(fac * s);
     }
   }
   // the cell's W DOFs (P0: one; QUAD: N_q points, ∇u_h is constant on the cell)
@@ -359,6 +364,7 @@ struct TileArgs {
   S* r;
   S* csr;
   int d1;       // d+1 (GRADPOW chain stride)
+  int packed;   // P0 Newton: packed chain record [w, D_0 .. D_{d−1}], D_d = −Σ (gradient kinds)
   int dmode;    // W = V Newton factor ∂w_m/∂u_m: 0 → 1, 1 → 2u_m (SQUARE), 2 → −1/(pk+u_m)² (RECIPROCAL)
   double pk;
   uint32_t kmask;  // kKMask for P0 W (loc bits), ~0 otherwise
@@ -529,7 +535,19 @@ __device__ __forceinline__ void tile_prepare(const TileArgs<S>& A, const TileGeo
     const uint32_t kr = v.k[y];
     const uint32_t k = kr & A.kmask;
     cp_async_s(v.w + y, A.w + k);
-    if (L::kP0) cp_async_s(v.d + y, A.chain + (int64_t)k * A.d1 + ((kr >> kKShift) & 3u));
+    if (L::kP0) {
+      const uint32_t lc = (kr >> kKShift) & 3u;
+      const S* cr = A.chain + (int64_t)k * A.d1;
+      if (!A.packed) {
+        cp_async_s(v.d + y, cr + lc);
+      } else if ((int)lc + 1 < A.d1) {  // packed record: D_m at 1 + m
+        cp_async_s(v.d + y, cr + 1 + lc);
+      } else {  // D_d = −Σ_{m<d} D_m (a plain store; visible after the stage barrier)
+        S sd = S(0);
+        for (int m = 1; m < A.d1; ++m) sd = sd + __ldg(cr + m);
+        v.d[y] = -sd;
+      }
+    }
   }
   if (L::kNeedU) {
     for (int x = tid; x < g.nf; x += kThreads) cp_async_s(v.uj + x, A.u + v.fj[x]);
@@ -730,6 +748,7 @@ egfem_status tile_dispatch(const egfem_tensor* t, bool do_r, int jac, egfem_inte
   A.r = static_cast<S*>(r);
   A.csr = static_cast<S*>(csr);
   A.d1 = t->dim + 1;
+  A.packed = jac == kJacNewtonP0 && packed_chain_kind(kind);
   A.dmode = kind == EGFEM_INTERP_SQUARE ? 1 : (kind == EGFEM_INTERP_RECIPROCAL ? 2 : 0);
   A.pk = p;
   A.kmask = t->kmask();
@@ -936,7 +955,7 @@ egfem_status launch_tile(const egfem_tensor* t, bool do_r, int jac, egfem_interp
   const bool tile = force && force[0] == 't';
   const bool rows_only = force && force[0] == 'r';
   if (!tile && !rows_only && cells_path_ok(t, jac))
-    return launch_cells(t, do_r, jac, u, w, chain, r, csr_vals, s);
+    return launch_cells(t, do_r, jac, jac == 3 && packed_chain_kind(kind), u, w, chain, r, csr_vals, s);
   if (!tile && !rows_only && dense1_path_ok(t, jac))
     return launch_dense1(t, 0, t->n_u, do_r, jac, kind, p, u, w, r, csr_vals, s);
   if (!tile && rows_path_ok(t, jac)) return launch_rows(t, do_r, jac, kind, p, u, w, chain, r, csr_vals, s);
@@ -1014,7 +1033,7 @@ egfem_status launch_tile_rows(const egfem_tensor* t, int64_t lo, int64_t hi, boo
   v.row_begin = t->row_begin + lo;
   v.col_begin = t->col_begin;
   void* rl = r ? (char*)r + (t->dtype == EGFEM_F64 ? 8 : 4) * lo : nullptr;
-  if (cells) return launch_cells(&v, do_r, jac, u, w, chain, rl, csr_vals, s);
+  if (cells) return launch_cells(&v, do_r, jac, jac == 3 && packed_chain_kind(kind), u, w, chain, rl, csr_vals, s);
   return launch_rows(&v, do_r, jac, kind, p, u, w, chain, rl, csr_vals, s);
 }
 

@@ -44,6 +44,7 @@ struct RowArgs {
   S* r;
   S* csr;
   int d1;
+  int packed;  // P0 Newton: the gradient kinds' packed chain record [w, D_0 .. D_{d−1}], D_d = −Σ
   int dmode;   // W = V Newton factor: 0 → 1, 1 → 2u (SQUARE), 2 → −1/(pk+u)² (RECIPROCAL)
   double pk;
   uint32_t kmask;
@@ -260,8 +261,23 @@ __global__ void __launch_bounds__(256, NCH > 8 ? 2 : ((JAC == kJacNewtonP0 || JA
     }
     if constexpr (kP0) {  // (D_u w)_{K, loc(j)}: issued here, consumed after the per-cell pass
 #pragma unroll
-      for (int c = 0; c < NCH; ++c)
-        dd[c] = (c < nl) ? __ldg(A.chain + (size_t)kc[c] * D1 + ((locs >> (2 * c)) & 3u)) : S(0);
+      for (int c = 0; c < NCH; ++c) {
+        const uint32_t lc = (locs >> (2 * c)) & 3u;
+        if (!A.packed) {
+          dd[c] = (c < nl) ? __ldg(A.chain + (size_t)kc[c] * D1 + lc) : S(0);
+        } else if (c < nl) {  // packed record: D_m at 1 + m, D_d = −Σ_{m<d} D_m
+          const S* cr = A.chain + (size_t)kc[c] * D1;
+          if (lc + 1 < (uint32_t)D1) {
+            dd[c] = __ldg(cr + 1 + lc);
+          } else {
+            S sd = S(0);
+            for (int m = 1; m < D1; ++m) sd = add_(sd, __ldg(cr + m));
+            dd[c] = -sd;
+          }
+        } else {
+          dd[c] = S(0);
+        }
+      }
     }
     if constexpr (DO_R) {
 #pragma unroll
@@ -466,6 +482,7 @@ egfem_status rows_dispatch(const egfem_tensor* t, bool do_r, int jac, egfem_inte
   A.r = static_cast<S*>(r);
   A.csr = static_cast<S*>(csr);
   A.d1 = t->dim + 1;
+  A.packed = jac == kJacNewtonP0 && packed_chain_kind(kind);
   A.dmode = kind == EGFEM_INTERP_SQUARE ? 1 : (kind == EGFEM_INTERP_RECIPROCAL ? 2 : 0);
   A.pk = p;
   A.kmask = t->kmask();
