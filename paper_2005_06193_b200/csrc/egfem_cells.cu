@@ -288,13 +288,13 @@ __device__ __forceinline__ Meta meta(const CellArgs<S>& A, int64_t row) {
   return m;
 }
 
-// u at a nonzero's column: from a per-group shared copy of the row's fiber u (one shared load)
-// or by shuffles from the fiber lanes (FREG shuffles + selects, 2 instructions each for fp64).
-// Measured on cfg3/cfg4: the shared copy wins for FREG >= 4, for fp32 and for the apply-only
-// kernel; fp64 Newton with FREG = 2 is faster with shuffles (bank conflicts between groups).
+// u at a nonzero's column: from a per-group shared copy of the row's fiber u (one shared load
+// per nonzero).  Round 1 measured shuffles from the fiber lanes faster for fp64 Newton with
+// FREG = 2 (0.84 vs 0.92 ms); with the packed Newton record (one gather per cell) the shared
+// copy wins there too (cfg4 fused 0.675 -> 0.649 ms), so every instance uses it.
 template <typename S, int FREG, int JAC>
 __host__ __device__ constexpr bool cells_su() {
-  return FREG >= 4 || sizeof(S) == 4 || JAC == kJacNone;
+  return true;
 }
 
 // C32: the D_u w rows are 32-byte aligned and read with one 256-bit load each (a compile-time
