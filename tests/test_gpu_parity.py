@@ -650,3 +650,34 @@ def test_batched_groups_graph_and_shards(eg, orc, same):
         eg.egfem_apply_batched(t, hi - lo, eg.LAYOUT_NODE_MAJOR, Us, Ws, Rs)
         torch.cuda.synchronize()
         assert torch.equal(Rs, R0[:, lo:hi]), (lo, hi)
+
+
+@pytest.mark.parametrize("config", ["cfg1", "cfg5"])
+def test_bench_line_contract(config):
+    """bench.py on the GPU prints one JSON line with the contract's keys: value, roofline (named
+    kernel, §8(d) bytes or flops, frac), e2e with its copy bytes, clocks, gpu_launches > 0 and a
+    cpu_baseline whose parity against the GPU outputs is within tolerance."""
+    import json
+    import os
+    import subprocess
+    import sys
+    root = os.path.dirname(os.path.dirname(os.path.abspath(__file__)))
+    env = dict(os.environ)
+    env.pop("WORLD_SIZE", None)
+    extra = ["--batch", "64"] if config == "cfg5" else []
+    out = subprocess.run([sys.executable, os.path.join(root, "bench.py"), "--config", config, "--steps", "3",
+                          "--warmup", "3", *extra], capture_output=True, text=True, timeout=900, env=env, cwd=root)
+    assert out.returncode == 0, out.stderr[-3000:]
+    lines = [l for l in out.stdout.splitlines() if l.startswith("{")]
+    assert len(lines) == 1
+    d = json.loads(lines[0])
+    for k in ("metric", "value", "unit", "n_gpus", "steps", "warmup", "ms_per_step", "roofline", "e2e", "clocks",
+              "gpu_launches", "cpu_baseline", "dtype", "config"):
+        assert k in d, k
+    assert d["value"] > 0 and d["gpu_launches"] > 0 and d["n_gpus"] == 1
+    r = d["roofline"]
+    assert r["kernel"] and r["frac"] > 0 and r["peak"] > 0
+    assert d["e2e"]["h2d_bytes_per_step"] > 0 and d["e2e"]["d2h_bytes_per_step"] > 0
+    cb = d["cpu_baseline"]
+    assert cb["kind"] == "oracle" and cb["cores"] == 1 and cb["all_cores"]["bitwise_equal_to_1_thread"]
+    assert all(v <= 1e-12 for k, v in cb["parity_rel_l2"].items() if k not in ("rows", "pairs")), cb["parity_rel_l2"]
