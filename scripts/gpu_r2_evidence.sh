@@ -20,5 +20,15 @@ timeout 900 ncu --metrics gpu__time_duration.sum --clock-control none -c 400 --c
 timeout 900 ncu --set full --clock-control none --import-source on -k 'regex:k_cell$|k_interp' -c 5 -o $O/prof_cfg4 -f python scripts/profile_cfg4_jac.py > $O/ncu_full.log 2>&1; echo "ncu rc=$?" >> $O/ncu_full.log
 timeout 900 ncu --set full --clock-control none --import-source on -k 'regex:k_cell$|k_interp' -c 5 -o $O/prof_cfg4_f32 -f python scripts/profile_cfg4_jac.py f32 > $O/ncu_full32.log 2>&1
 timeout 900 ncu --set full --clock-control none --import-source on -k 'regex:egfem_grp_0' -c 1 -o $O/prof_cfg5 -f python scripts/profile_cfg5.py > $O/ncu_full5.log 2>&1
+# summaries on the box (gpurun copies back at most 64 MiB): text summaries, SASS stall tables,
+# traffic.json; the full reports of cfg4 are dropped after summarising
+for r in prof_cfg4 prof_cfg4_f32 prof_cfg5; do python scripts/ncu_summary.py $O/$r.ncu-rep > $O/$r.txt 2>&1; done
+ncu -i $O/prof_cfg4.ncu-rep --page source --csv --print-source sass > $O/sass_cfg4.csv 2>/dev/null
+python scripts/sass_stalls.py $O/sass_cfg4.csv 30 > $O/sass_cfg4_stalls.txt 2>&1
+ncu -i $O/prof_cfg5.ncu-rep --page source --csv --print-source sass > $O/sass_cfg5.csv 2>/dev/null
+python scripts/sass_stalls.py $O/sass_cfg5.csv 30 > $O/sass_cfg5_stalls.txt 2>&1
+python scripts/make_traffic.py $O/prof_cfg4.ncu-rep $O/prof_cfg4_f32.ncu-rep $O/prof_cfg5.ncu-rep r2 $O/traffic.json > /dev/null 2>&1
+rm -f $O/prof_cfg4.ncu-rep $O/prof_cfg4_f32.ncu-rep $O/sass_cfg4.csv $O/sass_cfg5.csv
 fi
+du -sh gpurun_out
 ls -la $O

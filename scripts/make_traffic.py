@@ -1,5 +1,5 @@
 """Write profiles/traffic.json (read by bench.py for roofline.traffic / l2_hit / fp64 pipe) from
-ncu --set full captures:  python scripts/make_traffic.py <cfg4 f64 rep> <cfg4 f32 rep> <cfg5 rep>
+ncu --set full captures:  python scripts/make_traffic.py <cfg4 f64 rep> <cfg4 f32 rep> <cfg5 rep> [round] [out]
 cfg4 captures are of scripts/profile_cfg4_jac.py (interp, apply, Picard, Newton, fused in that
 order); the cfg5 capture is of scripts/profile_cfg5.py (the largest class kernel egfem_grp_0)."""
 import csv
@@ -45,7 +45,7 @@ def main():
         out[wl] = {k: entry(d, summ[wl]) for k, d in zip(keys, rs)}
     rs = rows(sys.argv[3])
     out["cfg5-f64"] = {"batched": entry(rs[0], summ["cfg5-f64"])}
-    json.dump(out, open("profiles/traffic.json", "w"), indent=1)
+    json.dump(out, open(sys.argv[5] if len(sys.argv) > 5 else "profiles/traffic.json", "w"), indent=1)
     print(json.dumps(out, indent=1)[:1500])
 
 
