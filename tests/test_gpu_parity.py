@@ -681,3 +681,21 @@ def test_bench_line_contract(config):
     cb = d["cpu_baseline"]
     assert cb["kind"] == "oracle" and cb["cores"] == 1 and cb["all_cores"]["bitwise_equal_to_1_thread"]
     assert all(v <= 1e-12 for k, v in cb["parity_rel_l2"].items() if k not in ("rows", "pairs")), cb["parity_rel_l2"]
+
+
+@pytest.mark.parametrize("B", [128, 96])
+def test_batched_groups_fp32(eg, orc, B):
+    """The compiled row-group kernels in fp32 (float records, float4 / float2 vectors): the batched
+    action of the fp32 handle (fp64 build rounded once, reading C16) vs the fp64 oracle ≤ 2e-5,
+    for a full (B = 128) and a guarded (B = 96) pair chunking."""
+    import torch
+    pr = I.make_problem("cfg5", n=20, batch=B)
+    t = eg.egfem_tensor_build(pr.mesh, pr.V, pr.W, pr.form, dtype=1, device=0)
+    assert "egfem_grp" in eg.egfem_kernel_name(t, 3)
+    o = orc.OracleTensor(pr.mesh, pr.V, pr.W, pr.form)
+    U = torch.tensor(np.ascontiguousarray(pr.u.T), dtype=torch.float32, device="cuda")
+    R = torch.empty_like(U)
+    eg.egfem_apply_batched(t, B, eg.LAYOUT_NODE_MAJOR, U, U, R)
+    torch.cuda.synchronize()
+    ref = o.apply_batched(pr.u, pr.u)
+    assert rel_l2(R.double().cpu().numpy().T, ref) <= FP32_TOL
