@@ -240,8 +240,9 @@ egfem_status egfem_apply_jacobian(const egfem_tensor* t, egfem_jac_mode mode, eg
  * egfem_bilinear_build: b_vals device [nnz_csr] ← B.  Needs W = V numbering whose T·₂u fits
  * the pattern (else DIMENSION_MISMATCH / UNSUPPORTED) and a value u-slot (MASS3, CONV_I,
  * CONV_K; CONV_J and PLAP differentiate it, T·₂1 = 0: UNSUPPORTED; a from_coo tensor is taken
- * as is).  Runs T·₂1 through the Newton kernel (offline; allocates and frees two device
- * vectors, synchronizes the stream). */
+ * as is; a partitioned local tensor: UNSUPPORTED).  Runs T·₂1 through the Newton kernel
+ * (offline; two stream-ordered temporary vectors over the column space, cudaMallocAsync /
+ * cudaFreeAsync: no synchronization, capturable in a CUDA graph). */
 egfem_status egfem_bilinear_build(const egfem_tensor* t, void* b_vals, egfem_stream_t stream);
 
 /* y = A x for any values `vals` [nnz_csr] on the tensor's CSR pattern (x: [N_u], y: [N_u], all

@@ -544,6 +544,8 @@ egfem_status egfem_bilinear_build(const egfem_tensor* t, void* b_vals, egfem_str
   if ((st = check_dev_ptr(t, b_vals, "b_vals", true))) return st;
   if (!t->w_is_v) return fail(EGFEM_ERR_DIMENSION_MISMATCH, "bilinear form needs W = V numbering");
   if (!t->newton_wv_ok) return fail(EGFEM_ERR_UNSUPPORTED, "T·₂1 has entries outside the CSR pattern");
+  if (t->int_row_lo >= 0)  // a local tensor of a partition: its columns are window indices
+    return fail(EGFEM_ERR_UNSUPPORTED, "bilinear form of a partitioned tensor: build it on the global tensor");
   if (t->has_mesh && (t->form == EGFEM_FORM_CONV_J || t->form == EGFEM_FORM_PLAP))
     return fail(EGFEM_ERR_UNSUPPORTED, "the u-slot of this form is differentiated: T·₂1 = 0 (Σ_j ∇φ_j = 0)");
   DeviceGuard g(t->device);

@@ -93,27 +93,28 @@ egfem_status launch_scale_cols(const egfem_tensor* t, const void* b, int mode, d
 }
 
 // B = T·₂1: the IDENTITY Newton Jacobian T·w + T·₂u at w = 0, u = 1.
+// The ones / zeros vectors span the column space (max(n_u, n_f)) and are stream-ordered
+// allocations (cudaMallocAsync / cudaFreeAsync), so the call neither synchronizes nor breaks a
+// CUDA-graph capture.
 egfem_status launch_bilinear_build(const egfem_tensor* t, void* b_vals, cudaStream_t s) {
   const size_t vs = t->dtype == EGFEM_F64 ? 8 : 4;
+  const int64_t ncol = std::max<int64_t>(std::max<int64_t>(t->n_u, t->n_f), 1);
   void* ones = nullptr;
   void* zeros = nullptr;
-  EGFEM_CUDA_TRY(cudaMalloc(&ones, vs * std::max<int64_t>(t->n_u, 1)));
-  if (cudaMalloc(&zeros, vs * std::max<int64_t>(t->n_f, 1)) != cudaSuccess) {
-    cudaFree(ones);
-    set_error("cudaMalloc failed");
+  EGFEM_CUDA_TRY(cudaMallocAsync(&ones, vs * ncol, s));
+  if (cudaMallocAsync(&zeros, vs * ncol, s) != cudaSuccess) {
+    cudaFreeAsync(ones, s);
+    set_error("cudaMallocAsync failed");
     return EGFEM_ERR_OUT_OF_MEMORY;
   }
-  cudaMemsetAsync(zeros, 0, vs * std::max<int64_t>(t->n_f, 1), s);
-  const int nb = (int)((t->n_u + 255) / 256);
-  if (t->n_u > 0) {
-    if (t->dtype == EGFEM_F64) k_fill<<<nb, 256, 0, s>>>((double*)ones, t->n_u, 1.0);
-    else k_fillf<<<nb, 256, 0, s>>>((float*)ones, t->n_u, 1.0f);
-    count_launch();
-  }
+  cudaMemsetAsync(zeros, 0, vs * ncol, s);
+  const int nb = (int)((ncol + 255) / 256);
+  if (t->dtype == EGFEM_F64) k_fill<<<nb, 256, 0, s>>>((double*)ones, ncol, 1.0);
+  else k_fillf<<<nb, 256, 0, s>>>((float*)ones, ncol, 1.0f);
+  count_launch();
   egfem_status st = launch_tile(t, false, 2, EGFEM_INTERP_IDENTITY, 0.0, ones, zeros, nullptr, nullptr, b_vals, s);
-  cudaStreamSynchronize(s);
-  cudaFree(ones);
-  cudaFree(zeros);
+  cudaFreeAsync(ones, s);
+  cudaFreeAsync(zeros, s);
   return st;
 }
 
