@@ -77,7 +77,8 @@ struct GroupPlan {
   bool f64 = true;
   std::vector<GroupClass> classes;
   std::vector<cudaLibrary_t> libs;
-  std::mutex mu;  // guards the lazily compiled variants and the side streams
+  std::mutex mu;         // guards the lazily compiled variants and the side streams
+  std::mutex launch_mu;  // one enqueue at a time: the fork event and side streams are shared
   // side streams for the small classes and the fallback rows (fork-join around the big class)
   int side_dev = -1;
   std::vector<cudaStream_t> side;
@@ -631,7 +632,6 @@ egfem_status make_groups(egfem_tensor* t, const std::vector<int64_t>& hrf) {
   std::unordered_map<std::vector<int32_t>, int, KeyHash> cls_of;
   std::vector<Pattern> cls_pat;
   std::vector<std::vector<int32_t>> cls_inst;
-  std::vector<int32_t> pos(0);
   for (int32_t l : leaders) {
     auto [lc, ln] = sten(l);
     Pattern pt;
@@ -902,6 +902,9 @@ egfem_status launch_groups(const egfem_tensor* t, int32_t batch, const void* U, 
   if (st) return st;
   const size_t nc = gp->classes.size();
   const bool fork = nc + (gp->fb_count > 0 ? 1 : 0) > 1;
+  // concurrent callers (other host threads, other streams) enqueue one after the other: the
+  // fork / join events and the side streams are per handle (results stay ordered per stream)
+  std::lock_guard<std::mutex> lk(gp->launch_mu);
   if (fork) {
     if ((st = ensure_side(gp, t->device))) return st;
     EGFEM_CUDA_TRY(cudaEventRecord(gp->fork, s));
