@@ -199,10 +199,10 @@ __device__ __forceinline__ void gradpow_cell(const CellIn<S, D>& in, int64_t c, 
     const int64_t K = IOTA ? c : (int64_t)__ldg(wdofs + c * nw + l);
     w[K] = (S)wk;
     if (chain) {
-      if constexpr (D == 3 && sizeof(S) == 8) {
-        double2* o = reinterpret_cast<double2*>(chain + K * 4);
-        o[0] = make_double2(dm[0], dm[1]);
-        o[1] = make_double2(dm[2], dm[3]);
+      if constexpr (D == 3 && sizeof(S) == 8) {  // one 32-byte store (sm_100 256-bit STG)
+        asm volatile("st.global.v4.f64 [%0], {%1, %2, %3, %4};" ::"l"(chain + K * 4), "d"(dm[0]), "d"(dm[1]),
+                     "d"(dm[2]), "d"(dm[3])
+                     : "memory");
       } else if constexpr (D == 3) {
         reinterpret_cast<float4*>(chain)[K] = make_float4(dm[0], dm[1], dm[2], dm[3]);
       } else {
