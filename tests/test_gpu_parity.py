@@ -699,3 +699,20 @@ def test_batched_groups_fp32(eg, orc, B):
     torch.cuda.synchronize()
     ref = o.apply_batched(pr.u, pr.u)
     assert rel_l2(R.double().cpu().numpy().T, ref) <= FP32_TOL
+
+
+@pytest.mark.parametrize("B,same", [(512, True), (300, False), (1000, True)])
+def test_batched_groups_wide_batches(eg, orc, B, same):
+    """Batches wider than one CTA's pairs: 512 (4 warps of 128 pairs, full variant), 300 and 1000
+    (guarded variant; warps loop over the pair chunks), U aliased to W or not."""
+    import torch
+    pr = I.make_problem("cfg5", n=10, batch=B)
+    t = eg.egfem_tensor_build(pr.mesh, pr.V, pr.W, pr.form, device=0)
+    o = orc.OracleTensor(pr.mesh, pr.V, pr.W, pr.form)
+    U = torch.tensor(np.ascontiguousarray(pr.u.T), device="cuda")
+    Wt = U if same else (0.5 * U - 0.125).contiguous()
+    R = torch.empty_like(U)
+    eg.egfem_apply_batched(t, B, eg.LAYOUT_NODE_MAJOR, U, Wt, R)
+    torch.cuda.synchronize()
+    ref = o.apply_batched(pr.u, Wt.cpu().numpy().T)
+    assert rel_l2(R.cpu().numpy().T, ref) <= FP64_TOL
