@@ -24,8 +24,10 @@
  *     Lengths are implied by egfem_tensor_info (N_u, N_f, nnz_csr).
  *   - Compute calls are asynchronous on the given cudaStream_t (0 = legacy default).
  *     Kernel faults surface at the next call or at the caller's stream sync.
- *   - The handle is immutable after build; interp/apply/jacobian are pure functions
- *     of their inputs and may run concurrently on different streams.
+ *   - The handle is immutable after build (its only lazily created state — the compiled
+ *     batched kernels and their side streams — is created under a lock on first use);
+ *     interp/apply/jacobian are pure functions of their inputs and may run concurrently
+ *     on different streams.
  *   - No floating-point atomics: results are bitwise reproducible run to run.
  *   - csr_vals is fully overwritten, never accumulated into.
  */
@@ -204,7 +206,13 @@ egfem_status egfem_apply(const egfem_tensor* t, const void* u, const void* w, vo
 
 /* (2b) the same for `batch` independent (u, w) pairs reusing each T nonzero:
  * R_p = T:(U_p ⊗ W_p).  Layout NODE_MAJOR: U[j*batch+p], W[k*batch+p], R[i*batch+p];
- * PAIR_MAJOR: U[p*N_u+j], ... (batch >= 1). */
+ * PAIR_MAJOR: U[p*N_u+j], ... (batch >= 1).  U may alias W (pairs (u, w = u): the u-slot
+ * values are then taken from the W registers).  W = V tensors with dense blocks run the
+ * compiled row-group kernels for NODE_MAJOR (egfem_group.cu): the kernel variant for
+ * (U aliases W, batch % 128 == 0) is NVRTC-compiled on its first use (a one-time host cost
+ * of ~1 s, cached process-wide), and the call forks its small pattern classes onto the
+ * handle's side streams and joins them back into `stream` with events (stream-ordered and
+ * CUDA-graph capturable; concurrent callers enqueue one after the other). */
 egfem_status egfem_apply_batched(const egfem_tensor* t, int32_t batch, egfem_layout layout,
                                  const void* U, const void* W, void* R, egfem_stream_t stream);
 
