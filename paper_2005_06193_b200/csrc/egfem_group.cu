@@ -33,6 +33,7 @@
 #include <cstdio>
 #include <cstdlib>
 #include <cstring>
+#include <functional>
 #include <map>
 #include <atomic>
 #include <mutex>
@@ -184,7 +185,8 @@ std::string vec_store(const char* S, int P, const std::string& ptr, const std::s
 }
 
 void emit_body(std::string& o, const Pattern& pt, const char* S, int P, bool same, bool full, int IL, int nv,
-               const char* indent, bool contig = false);
+               const char* indent, bool contig = false,
+               const std::function<std::string(int)>& lazy_w = std::function<std::string(int)>());
 
 // Straight-line kernel source for one pattern class.  P pairs per lane (lane, lane+32, ...).
 // A CTA walks runs of `run` consecutive instances (runs dealt round-robin, so the CTAs in flight
@@ -203,10 +205,23 @@ std::string kernel_source(const Pattern& pt, const std::string& name, const char
     std::snprintf(buf, sizeof(buf), fmt, a...);
     o += buf;
   };
-  emit("extern \"C\" __global__ void __launch_bounds__(128) %s(const int* __restrict__ gcols, "
-       "const int* __restrict__ grows, const %s* __restrict__ gvals, long long ninst, int B, int run, int pf, "
-       "const %s* __restrict__ U, const %s* __restrict__ W, %s* __restrict__ R) {\n",
-       name.c_str(), S, S, S, S);
+  // register cap: 120 registers give 4 resident 128-thread CTAs (16 warps/SM) — the DFMA chains
+  // and the W loads that start an instance need the extra warps (cfg5, P = 2: 130 → 120
+  // registers, 12 → 16 warps, 0.673 → 0.639 ms, no spills).  Applied when the instance state
+  // (W and the member accumulators, P doubles each) is small; EGFEM_GROUP_MAXREG overrides
+  // (0 = no cap).
+  static const int env_reg = std::getenv("EGFEM_GROUP_MAXREG") ? std::atoi(std::getenv("EGFEM_GROUP_MAXREG")) : -1;
+  const int maxnreg = env_reg >= 0 ? env_reg : (2 * P * (n + g) <= 96 && P <= 2 ? 120 : 0);
+  if (maxnreg > 0)
+    emit("extern \"C\" __global__ void __maxnreg__(%d) %s(const int* __restrict__ gcols, "
+         "const int* __restrict__ grows, const %s* __restrict__ gvals, long long ninst, int B, int run, int pf, "
+         "const %s* __restrict__ U, const %s* __restrict__ W, %s* __restrict__ R) {\n",
+         maxnreg, name.c_str(), S, S, S, S);
+  else
+    emit("extern \"C\" __global__ void __launch_bounds__(128) %s(const int* __restrict__ gcols, "
+         "const int* __restrict__ grows, const %s* __restrict__ gvals, long long ninst, int B, int run, int pf, "
+         "const %s* __restrict__ U, const %s* __restrict__ W, %s* __restrict__ R) {\n",
+         name.c_str(), S, S, S, S);
   emit("  __shared__ __align__(16) %s s_v[2][%d];\n", S, nv);
   emit("  __shared__ __align__(16) int s_c[2][%d];\n", ncp);
   emit("  const int lane = threadIdx.x & 31, warp = threadIdx.x >> 5, nw = blockDim.x >> 5;\n");
@@ -255,17 +270,31 @@ std::string kernel_source(const Pattern& pt, const std::string& name, const char
   if (!same) emit("      const %s* Up = U + p0;\n", S);
   if (!full)
     for (int q = 0; q < P; ++q) emit("      const bool ok%d = p0 + %d < B;\n", q, 32 * q);
-  for (int b = 0; b < n; ++b) {
-    emit("      const %s* wc%d = Wp + (long long)sc[%d] * B;\n", S, b, b);
-    if (full) {
-      o += "      " + vec_load(S, P, "w" + std::to_string(b), "wc" + std::to_string(b)) + "\n";
-      continue;
+  static const bool lazy = std::getenv("EGFEM_GROUP_LAZY") && std::getenv("EGFEM_GROUP_LAZY")[0] == '1';
+  std::function<std::string(int)> lazy_w;
+  if (full && lazy) {  // W loads emitted before their first use (the compiler hoists as registers allow)
+    for (int b = 0; b < n; ++b)
+      for (int q = 0; q < P; ++q) emit("      %s w%d_%d;\n", S, b, q);
+    lazy_w = [&, S, P](int b) {
+      std::string bs = std::to_string(b);
+      std::string l = vec_load(S, P, "lw" + bs, "(Wp + (long long)sc[" + bs + "] * B)");
+      std::string a = "{ " + l;
+      for (int q = 0; q < P; ++q) a += " w" + bs + "_" + std::to_string(q) + " = lw" + bs + "_" + std::to_string(q) + ";";
+      return a + " }";
+    };
+  } else {
+    for (int b = 0; b < n; ++b) {
+      emit("      const %s* wc%d = Wp + (long long)sc[%d] * B;\n", S, b, b);
+      if (full) {
+        o += "      " + vec_load(S, P, "w" + std::to_string(b), "wc" + std::to_string(b)) + "\n";
+        continue;
+      }
+      for (int q = 0; q < P; ++q)
+        emit("      const %s w%d_%d = ok%d ? __ldg(wc%d + %d) : (%s)0;\n", S, b, q, q, b, 32 * q, S);
     }
-    for (int q = 0; q < P; ++q)
-      emit("      const %s w%d_%d = ok%d ? __ldg(wc%d + %d) : (%s)0;\n", S, b, q, q, b, 32 * q, S);
   }
   emit("      {\n");
-  emit_body(o, pt, S, P, same, full, IL, nv, "        ", full);
+  emit_body(o, pt, S, P, same, full, IL, nv, "        ", full, lazy_w);
   for (int m = 0; m < g; ++m) {
     emit("      { %s* rr = R + (long long)__ldg(grows + gi * %d + %d) * B + p0;\n", S, g, m);
     if (full) {
@@ -286,7 +315,7 @@ std::string kernel_source(const Pattern& pt, const std::string& name, const char
 // u values, the interleaved fiber chains and the accumulators r<m>_<q>.  `uload(a, q)` gives
 // the expression of U at stencil point a for pair slot q when U != W.
 void emit_body(std::string& o, const Pattern& pt, const char* S, int P, bool same, bool full, int IL, int nv,
-               const char* indent, bool contig) {
+               const char* indent, bool contig, const std::function<std::string(int)>& lazy_w) {
   const int n = pt.n, g = (int)pt.members.size();
   char buf[512];
   auto emit = [&](const char* fmt, auto... a) {
@@ -299,11 +328,25 @@ void emit_body(std::string& o, const Pattern& pt, const char* S, int P, bool sam
   for (int m = 0; m < g; ++m)
     for (int q = 0; q < P; ++q) emit("%s r%d_%d;\n", S, m, q);
   int e = 0;
+  std::vector<char> w_done(n, 0);
   for (int a = 0; a < n; ++a) {
     bool any = false;
     for (int m = 0; m < g; ++m)
       for (const auto& f : pt.members[m]) any |= f.first == a;
     if (!any) continue;
+    if (lazy_w) {  // W values first used at this stencil point: loaded here (shorter live ranges)
+      std::vector<int> need;
+      if (same) need.push_back(a);
+      for (int m = 0; m < g; ++m)
+        for (const auto& f : pt.members[m])
+          if (f.first == a) need.insert(need.end(), f.second.begin(), f.second.end());
+      for (int b : need)
+        if (!w_done[b]) {
+          w_done[b] = 1;
+          o += indent;
+          o += lazy_w(b) + "\n";
+        }
+    }
     emit("{\n");
     if (same) {
       for (int q = 0; q < P; ++q) emit("  const %s u%d = w%d_%d;\n", S, q, a, q);
@@ -571,9 +614,9 @@ egfem_status make_groups(egfem_tensor* t, const std::vector<int64_t>& hrf) {
   if (!t->blk || !t->w_is_v || t->n_u <= 0 || t->nnz <= 0) return EGFEM_OK;
   if (const char* e = getenv("EGFEM_GROUPS"))
     if (e[0] == '0') return EGFEM_OK;
-  int P = 4;
+  int P = 2;  // pairs per lane (measured on cfg5: P = 2 at 16 warps/SM beats P = 4 at 8)
   if (const char* e = getenv("EGFEM_GROUP_P")) P = std::max(1, std::min(4, atoi(e)));
-  int run = 1;
+  int run = 2;
   if (const char* e = getenv("EGFEM_GROUP_RUN")) run = std::max(1, atoi(e));
   const int64_t n_u = t->n_u, n_fib = t->n_fib, nnz = t->nnz;
   std::vector<int32_t> fj(n_fib);
