@@ -47,8 +47,10 @@
 namespace egfem {
 
 // Kernel variants of a class: bit 0 = U and W are the same array (the u-slot values are the
-// W registers already loaded: no U loads), bit 1 = batch is a multiple of 32·P (no pair guards).
-constexpr int kVariants = 4;
+// W registers already loaded: no U loads), bit 1 = batch is a multiple of 32·P (no pair guards),
+// bit 2 = one pair per lane (batches below 64 or odd multiples of 32: a rank's shard of a
+// sharded batch) instead of the plan's P.
+constexpr int kVariants = 8;
 
 struct GroupClass {
   int n = 0;       // group stencil width |N(leader)|
@@ -60,10 +62,10 @@ struct GroupClass {
   int32_t* rows = nullptr;  // ninst × g: member rows
   void* vals = nullptr;     // ninst × nv, dtype: T values in FMA program order
   std::vector<int32_t> key; // the pattern (Pattern::key), kept to generate variants on demand
-  cudaKernel_t fn[kVariants] = {nullptr, nullptr, nullptr, nullptr};
-  int per_sm[kVariants] = {0, 0, 0, 0};  // resident CTAs per SM (registers), for the persistent grid
-  size_t dyn_set[kVariants] = {0, 0, 0, 0};  // dynamic shared memory the kernel was opted in for
-  int carve_set[kVariants] = {0, 0, 0, 0};
+  cudaKernel_t fn[kVariants] = {};
+  int per_sm[kVariants] = {};     // resident CTAs per SM (registers), for the persistent grid
+  size_t dyn_set[kVariants] = {};  // dynamic shared memory the kernel was opted in for
+  int carve_set[kVariants] = {};
 };
 
 struct GroupPlan {
@@ -869,6 +871,7 @@ egfem_status ensure_variant(GroupPlan* gp, int v) {
   for (const auto& gc : gp->classes) all &= gc.fn[v] != nullptr;
   if (all) return EGFEM_OK;
   const bool same = v & 1, full = (v >> 1) & 1;
+  const int P = (v & 4) ? 1 : gp->pairs_per_lane;
   std::vector<std::string> names(nc), srcs(nc);
   std::vector<std::vector<char>> cubins(nc);
   std::vector<egfem_status> sts(nc, EGFEM_OK);
@@ -876,8 +879,8 @@ egfem_status ensure_variant(GroupPlan* gp, int v) {
     names[c] = "egfem_grp_" + std::to_string(c) + "_v" + std::to_string(v);
     const Pattern pt = pattern_from_key(gp->classes[c].key);
     const char* S = gp->f64 ? "double" : "float";
-    srcs[c] = full && gp->staged ? kernel_source_staged(pt, names[c], S, gp->pairs_per_lane, same, gp->interleave)
-                                 : kernel_source(pt, names[c], S, gp->pairs_per_lane, same, full, gp->interleave);
+    srcs[c] = full && gp->staged ? kernel_source_staged(pt, names[c], S, P, same, gp->interleave)
+                                 : kernel_source(pt, names[c], S, P, same, full, gp->interleave);
   }
   std::vector<std::thread> th;
   std::atomic<size_t> next{0};
@@ -938,9 +941,13 @@ egfem_status launch_groups(const egfem_tensor* t, int32_t batch, const void* U, 
   GroupPlan* gp = t->grp;
   const int dev = t->device & 63;
   if (!g_sms_grp[dev]) EGFEM_CUDA_TRY(cudaDeviceGetAttribute(&g_sms_grp[dev], cudaDevAttrMultiProcessorCount, t->device));
-  const int P = gp->pairs_per_lane;
+  // pairs per lane: the plan's P, or 1 for batches narrower than one 32·P chunk (e.g. a rank's
+  // 32-pair shard of the 256 cfg5 pairs: 0.221 -> 0.172 ms); wider batches keep P (B = 96 at
+  // P = 1 measured slower than B = 128 at P = 2)
+  int P = gp->pairs_per_lane;
+  if (P > 1 && batch < 32 * P) P = 1;
   const int nch = (batch + 32 * P - 1) / (32 * P);
-  const int v = (U == W ? 1 : 0) | (batch % (32 * P) == 0 ? 2 : 0);
+  const int v = (U == W ? 1 : 0) | (batch % (32 * P) == 0 ? 2 : 0) | (P == 1 && gp->pairs_per_lane != 1 ? 4 : 0);
   egfem_status st = ensure_variant(gp, v);
   if (st) return st;
   const size_t nc = gp->classes.size();
