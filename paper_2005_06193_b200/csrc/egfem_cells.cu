@@ -533,7 +533,7 @@ __global__ void __launch_bounds__(cell_threads<S, JAC>(),
       if constexpr (kU) {
 #pragma unroll
         for (int m = 0; m < D1; ++m) {
-          const int fid = (int)(bq[m] & 0xffu);
+          const int fid = (int)(bq[m] & kCkFibMask);
           S um;
           if constexpr (SU) {
             um = s_u[fid];
@@ -555,8 +555,8 @@ __global__ void __launch_bounds__(cell_threads<S, JAC>(),
           for (int m = 0; m < D1; ++m) {
             S t = xmul(tv[m], wk[c]);
             if constexpr (kN) t = xfma(B, dd[c][m], t);
-            if ((int)(bq[m] & 0xffu) == fd) dacc = xadd(dacc, t);
-            else s_t[bq[m] >> 8] = t;
+            if ((int)(bq[m] & kCkFibMask) == fd) dacc = xadd(dacc, t);
+            else s_t[bq[m] >> kCkPosShift] = t;
           }
         }
       }
@@ -623,7 +623,7 @@ __global__ void k_make_cells(int64_t n_u, const int64_t* __restrict__ row_fib, c
   if (i >= n_u) return;
   const int64_t f0 = row_fib[i], f1 = row_fib[i + 1];
   const uint32_t e0 = fib_nz[f0], e1 = fib_nz[f1];
-  if ((e1 - e0) % D1 != 0 || e0 % D1 != 0 || e1 - e0 > 256 || f1 - f0 > 256) {
+  if ((e1 - e0) % D1 != 0 || e0 % D1 != 0 || e1 - e0 > (uint32_t)kCellsMaxNnz || f1 - f0 > kCkFibMask + 1) {
     atomicExch(err, 1);
     return;
   }
@@ -637,7 +637,7 @@ __global__ void k_make_cells(int64_t n_u, const int64_t* __restrict__ row_fib, c
         return;
       }
       ck_val[idx] = nz_val[e];
-      ck_b[idx] = (uint16_t)((uint32_t)(f - f0) | ((e - e0) << 8));
+      ck_b[idx] = (uint16_t)((uint32_t)(f - f0) | ((e - e0) << kCkPosShift));
       if (loc == 0) ck_k[e0 / D1 + slot] = nz_k[e] & kKMask;
     }
 }
@@ -705,7 +705,8 @@ egfem_status cells_mode(const egfem_tensor* t, const CellArgs<S>& A, bool do_r, 
 struct CellCfg {
   int d1, G, CPL, FREG;
 };
-constexpr CellCfg kCellCfgs[] = {{3, 2, 3, 4}, {3, 4, 4, 8}, {3, 16, 3, 1}, {4, 8, 3, 2}, {4, 16, 3, 2}, {4, 16, 4, 4}};
+constexpr CellCfg kCellCfgs[] = {{3, 2, 3, 4}, {3, 4, 4, 8}, {3, 16, 3, 1}, {4, 8, 3, 2},
+                                 {4, 16, 3, 2}, {4, 16, 4, 4}, {4, 32, 3, 1}};
 
 bool pick_cells(const egfem_tensor* t, CellCfg* out) {
   static int envG = -1, envC = -1;
@@ -762,6 +763,7 @@ egfem_status cells_dispatch(const egfem_tensor* t, bool do_r, int jac, bool pack
   EGFEM_CC(4, 8, 3, 2)
   EGFEM_CC(4, 16, 3, 2)
   EGFEM_CC(4, 16, 4, 4)
+  EGFEM_CC(4, 32, 3, 1)
 #undef EGFEM_CC
   set_error("no cell-major configuration");
   return EGFEM_ERR_UNSUPPORTED;
@@ -785,8 +787,9 @@ egfem_status launch_cells(const egfem_tensor* t, bool do_r, int jac, bool packed
 // Offline: cell-major copy for P0-W tensors of 2D/3D meshes whose rows fit the kernel;
 // silently skipped otherwise (the canonical row / tile kernels then serve the tensor).
 egfem_status make_p0_cells(egfem_tensor* t) {
+  CellCfg cfg{};
   if (!t->has_mesh || !t->w_p0 || !t->nz_aux || (t->dim != 2 && t->dim != 3) || t->n_u <= 0 || t->nnz <= 0 ||
-      t->max_row_nnz > kCellsMaxNnz)
+      t->max_row_nnz > kCellsMaxNnz || !pick_cells(t, &cfg))
     return EGFEM_OK;
   const int d1 = t->dim + 1;
   const size_t vs = t->dtype == EGFEM_F64 ? 8 : 4;

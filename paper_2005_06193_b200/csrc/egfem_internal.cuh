@@ -36,7 +36,11 @@ constexpr uint32_t kKMaskAny = 0x7FFFFFFFu;          // k of any other tensor
 constexpr uint32_t kHead = 0x80000000u;              // bit 31: first nonzero of a fiber
 constexpr int kMaxQuad = 16;
 constexpr int kRowsMaxNnz = 512;   // rows up to this length take the row-group path (k_seg)
-constexpr int kCellsMaxNnz = 256;  // cell-major copy: canonical position in a row fits 8 bits
+// cell-major copy: ck_b packs the fiber index within the row (6 bits) and the canonical position
+// within the row (10 bits)
+constexpr int kCellsMaxNnz = 1024;
+constexpr uint32_t kCkFibMask = 63u;
+constexpr int kCkPosShift = 6;
 constexpr int kWVMaxNnz = 256;     // W = V Newton transpose data: position in a row fits 8 bits
 
 void set_error(const std::string& msg);
@@ -76,7 +80,7 @@ struct egfem_tensor {
   // P0 W only: the same nonzeros in cell-major order (rows -> cells K ascending -> local vertex m)
   uint32_t* ck_k = nullptr;     // nnz/(d+1): K of each row cell
   void* ck_val = nullptr;       // nnz, dtype: T_{i v_m K}
-  uint16_t* ck_b = nullptr;     // nnz: fiber index within the row | canonical position << 8
+  uint16_t* ck_b = nullptr;     // nnz: fiber index within the row | canonical position << 6
   // W = V only (batched action): per row the dense |N|x|N| block over its CSR stencil N(i)
   int64_t* blk_off = nullptr;   // n_u+1: block offsets (row stride |N| rounded up to even)
   void* blk = nullptr;          // dtype: M_i[a][b] = T_{i, N_a, N_b}
