@@ -236,6 +236,24 @@ egfem_status egfem_apply_jacobian(const egfem_tensor* t, egfem_jac_mode mode, eg
                                   double p, const void* u, const void* w, const void* chain, void* r,
                                   void* csr_vals, egfem_stream_t stream);
 
+/* One Newton iteration's tensor work (PAPER.md L165–169 step (1), L183
+ * and L290–292 steps (2)+(3)): exactly egfem_interp(t, kind, p, u, w, chain) followed by
+ * egfem_apply_jacobian(t, NEWTON, kind, p, u, w, chain, r, csr_vals) — same arguments, same
+ * checks, and w, chain, r, csr_vals bitwise identical to those two calls.  For the gradient
+ * kinds (GRADPOW_P0, MINSURF_P0) on a mesh tensor with canonical P1 V / P0 W numbering whose
+ * rows fit the cell-major kernel (and, 3D fp64, a 32-byte aligned chain) it runs as ONE
+ * launch: warps take interp items (cells) and row items (rows) from one work sequence, a row
+ * item starting once the records of its cells are written (release/acquire flags in the
+ * handle), so the records are gathered from L2 while the interp of later cells overlaps.
+ * The single-pass plan is opt-in — built with the tensor when EGFEM_STEP=1 is set — because
+ * on B200 it measured slower than the two launches (both halves are bound by the SM
+ * load/store pipe); otherwise, and for every other tensor / kind / a chain not
+ * 32-byte aligned, it issues the two launches.  The single-pass state lives in the handle: calls on
+ * one handle must be stream-ordered (not concurrent on two streams).  Stream-ordered and
+ * CUDA-graph capturable. */
+egfem_status egfem_step(const egfem_tensor* t, egfem_interp_kind kind, double p, const void* u, void* w,
+                        void* chain, void* r, void* csr_vals, egfem_stream_t stream);
+
 /* ---------------------------------------------------------------- bilinear GFEM forms
  * The matrix forms of PAPER.md L196–203 eq. (egfem_terms) and L402–409:
  *   M^c_ik = ∫ η_k φ_i   (the MASS3 tensor's form),   N^f_ik = ∫ η_k (∂x+∂y)φ_i   (CONV_I's),
@@ -326,10 +344,11 @@ egfem_status egfem_halo_unpack(const egfem_tensor* local, const int32_t* d_idx, 
 
 /* Name of the kernel family `entry` dispatches to for this handle (0 = egfem_apply,
  * 1 = egfem_jacobian, 2 = egfem_apply_jacobian with (mode, kind, p), 3 = egfem_apply_batched
- * NODE_MAJOR), written NUL-terminated into the host buffer buf[len] (truncated if short).
+ * NODE_MAJOR, 4 = egfem_step with (kind, p), a 32-byte aligned chain assumed), written
+ * NUL-terminated into the host buffer buf[len] (truncated if short).
  * Used by bench.py to name the kernel its roofline line measures.  No launch.
  * INVALID_ARGUMENT on NULL t/buf, len = 0 or a bad entry; the Jacobian checks of
- * egfem_jacobian (without the pointer checks) for entries 1 and 2. */
+ * egfem_jacobian (without the pointer checks) for entries 1, 2 and 4. */
 egfem_status egfem_kernel_name(const egfem_tensor* t, int32_t entry, egfem_jac_mode mode, egfem_interp_kind kind,
                                double p, char* buf, size_t len);
 

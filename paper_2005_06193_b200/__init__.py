@@ -42,7 +42,7 @@ EXPORTS = ("egfem_tensor_build", "egfem_tensor_from_coo", "egfem_tensor_destroy"
            "egfem_partition_rows", "egfem_halo_pack", "egfem_halo_unpack", "egfem_launch_count",
            "egfem_status_string", "egfem_last_error", "egfem_bilinear_build", "egfem_csr_spmv",
            "egfem_bilinear_jacobian", "egfem_interior", "egfem_interp_range", "egfem_apply_jacobian_rows",
-           "egfem_interior_rows", "egfem_kernel_name", "egfem_group_compile")
+           "egfem_interior_rows", "egfem_kernel_name", "egfem_group_compile", "egfem_step")
 
 
 class EgfemError(RuntimeError):
@@ -95,6 +95,7 @@ def _load():
         "egfem_interior_rows": [i64, P, P, i64, i64, P, P],
         "egfem_kernel_name": [P, i32, st, st, ctypes.c_double, ctypes.c_char_p, ctypes.c_size_t],
         "egfem_group_compile": [P, i32, i32, i32],
+        "egfem_step": [P, st, ctypes.c_double, P, P, P, P, P, P],
     }
     for name, args in sig.items():
         f = getattr(L, name)
@@ -310,6 +311,14 @@ def egfem_apply_jacobian(t: Tensor, mode, kind, p, u, w, chain, r, csr_vals, str
                                                              _stream(stream, t)))
 
 
+def egfem_step(t: Tensor, kind, p, u, w, chain, r, csr_vals, stream=None):
+    """One Newton step's tensor work: egfem_interp then egfem_apply_jacobian(NEWTON) — in one
+    launch (the single-pass kernel) where the tensor allows it."""
+    _check("egfem_step", _lib.egfem_step(t.h, kind, float(p), _buf(t, u, t.n_u, "u"), _buf(t, w, t.n_f, "w"),
+                                         _buf(t, chain, _chain_len(t), "chain", False), _buf(t, r, t.n_u, "r"),
+                                         _buf(t, csr_vals, t.nnz_csr, "csr_vals"), _stream(stream, t)))
+
+
 def egfem_interp_range(t: Tensor, kind, p, u, w, chain, lo, hi, stream=None):
     _check("egfem_interp_range", _lib.egfem_interp_range(t.h, kind, float(p), _buf(t, u, t.n_u, "u"),
                                                          _buf(t, w, t.n_f, "w"),
@@ -375,7 +384,7 @@ def egfem_halo_unpack(t: Tensor, idx, recv_buf, u_local, stream=None):
 
 def egfem_kernel_name(t: Tensor, entry, mode=JAC_NEWTON, kind=INTERP_IDENTITY, p=0.0) -> str:
     """Kernel family an entry point runs for this handle (0 apply, 1 jacobian, 2 apply_jacobian,
-    3 apply_batched node-major); bench.py names its roofline kernel with it."""
+    3 apply_batched node-major, 4 step); bench.py names its roofline kernel with it."""
     buf = ctypes.create_string_buffer(512)
     _check("egfem_kernel_name", _lib.egfem_kernel_name(t.h, int(entry), mode, kind, float(p), buf, 512))
     return buf.value.decode()

@@ -444,8 +444,14 @@ egfem_status egfem_kernel_name(const egfem_tensor* t, int32_t entry, egfem_jac_m
   egfem_status st;
   if (entry == 1 || entry == 2)
     if ((st = jac_mode_code(t, mode, kind, p, nullptr, nullptr, &code, false))) return st;
-  if (entry < 0 || entry > 3) return fail(EGFEM_ERR_INVALID_ARGUMENT, "entry must be 0..3");
-  const std::string name = dispatch_name(t, entry, code);
+  if (entry == 4 && (st = jac_mode_code(t, EGFEM_JAC_NEWTON, kind, p, nullptr, nullptr, &code, false))) return st;
+  if (entry < 0 || entry > 4) return fail(EGFEM_ERR_INVALID_ARGUMENT, "entry must be 0..4");
+  std::string name;
+  if (entry == 4)  // egfem_step (a 32-byte aligned chain assumed)
+    name = step_path_ok(t, kind, nullptr) ? "k_step (single-pass interp + apply + Newton Jacobian, egfem_cells.cu)"
+                                          : "k_interp_* + " + dispatch_name(t, 2, code);
+  else
+    name = dispatch_name(t, entry, code);
   std::snprintf(buf, len, "%s", name.c_str());
   return EGFEM_OK;
 }
@@ -482,6 +488,22 @@ egfem_status egfem_apply_jacobian(const egfem_tensor* t, egfem_jac_mode mode, eg
   if ((st = jac_mode_code(t, mode, kind, p, u, chain, &code))) return st;
   DeviceGuard g(t->device);
   return launch_tile(t, true, code, kind, p, u, w, chain, r, csr_vals, (cudaStream_t)stream);
+}
+
+egfem_status egfem_step(const egfem_tensor* t, egfem_interp_kind kind, double p, const void* u, void* w, void* chain,
+                        void* r, void* csr_vals, egfem_stream_t stream) {
+  egfem_status st = interp_check(t, kind, p, u, w, chain);
+  if (st) return st;
+  if ((st = check_dev_ptr(t, r, "r", true)) || (st = check_dev_ptr(t, csr_vals, "csr_vals", true))) return st;
+  int code = 0;
+  if ((st = jac_mode_code(t, EGFEM_JAC_NEWTON, kind, p, u, chain, &code))) return st;
+  DeviceGuard g(t->device);
+  const cudaStream_t s = (cudaStream_t)stream;
+  st = launch_step(t, kind, p, u, w, chain, r, csr_vals, s);
+  if (st != EGFEM_ERR_UNSUPPORTED) return st;
+  // the tensor, kind or chain alignment does not fit the single-pass kernel: the two launches
+  if ((st = launch_interp(t, kind, p, u, w, chain, 0, interp_items(t, kind), s))) return st;
+  return launch_tile(t, true, code, kind, p, u, w, chain, r, csr_vals, s);
 }
 
 egfem_status egfem_apply_jacobian_rows(const egfem_tensor* t, egfem_jac_mode mode, egfem_interp_kind kind, double p,

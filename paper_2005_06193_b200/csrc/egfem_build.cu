@@ -801,6 +801,7 @@ egfem_status build_from_triples(egfem_tensor* t, int64_t m, uint64_t* d_key_ij, 
   if (st) return st;
   if ((st = make_wv_aux(t))) return st;
   if ((st = make_p0_cells(t))) return st;
+  if ((st = make_step_plan(t))) return st;
   if ((st = make_dense_blocks(t, hrf))) return st;
   if ((st = make_groups(t, hrf))) return st;
   EGFEM_CUDA_TRY(cudaDeviceSynchronize());
@@ -936,6 +937,8 @@ void free_tensor(egfem_tensor* t) {
     if (p) cudaFree(p);
   free_group_plan(t->grp);
   t->grp = nullptr;
+  free_step_plan(t->step);
+  t->step = nullptr;
 }
 
 }  // namespace egfem

@@ -27,6 +27,7 @@
 #include <cstdlib>
 
 #include "egfem_internal.cuh"
+#include "egfem_interp.cuh"
 
 namespace egfem {
 namespace {
@@ -219,6 +220,27 @@ __device__ __forceinline__ void load_cell_ldg(const S* p, S* out, bool a32 = fal
     }
   }
 }
+// the same through L2 only (data written earlier in the same launch by another SM)
+template <typename S, int D1>
+__device__ __forceinline__ void load_cell_cg(const S* p, S* out, bool a32 = false) {
+  if constexpr (sizeof(S) == 8 && D1 == 4) {
+    if (a32) {
+      // address dependent on shared-memory data read after the launch's acquire: never hoisted
+      asm("ld.global.cg.v4.f64 {%0,%1,%2,%3}, [%4];" : "=d"(out[0]), "=d"(out[1]), "=d"(out[2]), "=d"(out[3]) : "l"(p));
+      return;
+    }
+  }
+  if constexpr (sizeof(S) == 4 && D1 == 4) {  // one 16-byte load (the chain rows are 16-byte aligned)
+    const float4 x = __ldcg(reinterpret_cast<const float4*>(p));
+    out[0] = x.x;
+    out[1] = x.y;
+    out[2] = x.z;
+    out[3] = x.w;
+    return;
+  }
+#pragma unroll
+  for (int m = 0; m < D1; ++m) out[m] = __ldcg(p + m);
+}
 // the D1 values of one cell from global memory, streaming (evict-first) loads; 16-byte vectors
 // when D1·sizeof(S) is a multiple of 16 (cells start at multiples of D1 values)
 template <typename S, int D1>
@@ -277,9 +299,9 @@ struct Meta {
   uint32_t e0, e1, f0, f1;
 };
 template <typename S>
-__device__ __forceinline__ Meta meta(const CellArgs<S>& A, int64_t row) {
+__device__ __forceinline__ Meta meta(const CellArgs<S>& A, int64_t row, int64_t lim) {
   Meta m{0u, 0u, 0u, 0u};
-  if (row < A.n_u) {
+  if (row < lim) {
     m.e0 = (uint32_t)__ldg(A.row_nz + row);
     m.e1 = (uint32_t)__ldg(A.row_nz + row + 1);
     m.f0 = (uint32_t)__ldg(A.row_fib + row);
@@ -299,15 +321,16 @@ __host__ __device__ constexpr bool cells_su() {
 
 // C32: the D_u w rows are 32-byte aligned and read with one 256-bit load each (a compile-time
 // choice: a runtime branch between load widths makes the merged result wait on the load at once)
-template <typename S, int D1, int G, int CPL, int FREG, bool DO_R, int JAC, bool WB, bool C32 = false>
-__global__ void __launch_bounds__(cell_threads<S, JAC>(),
-                                  (JAC == kJacNone || G >= 16) ? 3 * 256 / cell_threads<S, JAC>() : 2 * 256 / cell_threads<S, JAC>())
-    k_cell(const CellArgs<S> A) {
+// COH: the chain records are read through L2 only (ld.global.cg), not the non-coherent
+// read-only path — the single-pass step kernel writes them during the same launch.
+// Rows row, row + NG, ... < lim of one group; wrow0 is the first row of the group's warp.
+template <typename S, int D1, int G, int CPL, int FREG, bool DO_R, int JAC, bool WB, bool C32, bool COH>
+__device__ __forceinline__ void cell_rows(const CellArgs<S>& A, int64_t row, const int64_t wrow0, const int64_t NG,
+                                          const int64_t lim) {
   constexpr bool kN = JAC == kJacNewtonP0 || JAC == kJacNewtonPK;
   constexpr bool kPK = JAC == kJacNewtonPK;
   constexpr bool SU = cells_su<S, FREG, JAC>() && (DO_R || kN);
   using L = CellSmem<S, D1, G, CPL, JAC != kJacNone, SU ? G * FREG : 0>;
-  constexpr int GPB = cell_threads<S, JAC>() / G;
   constexpr bool kJ = JAC != kJacNone;
   constexpr bool kU = DO_R || kN;  // u (and B_iK) needed; the Picard matrix alone reads no u
   // Control flow is warp-uniform (a group past the last row runs on an empty one), so
@@ -325,10 +348,6 @@ __global__ void __launch_bounds__(cell_threads<S, JAC>(),
   constexpr int STG = WB ? L::wstage : L::stage;
   constexpr int SK = WB ? L::w_k : L::st_k, SV = WB ? L::w_v : L::st_v, SB = WB ? L::w_b : L::st_b;
   const uint64_t pol = evict_first_policy();
-  const int64_t NG = (int64_t)gridDim.x * GPB;
-  int64_t row = (int64_t)blockIdx.x * GPB + grp;
-  const int64_t wrow0 = (int64_t)blockIdx.x * GPB + (threadIdx.x >> 5) * (32 / G);
-  if (wrow0 >= A.n_u) return;
 
   // fiber lanes: lane f holds fiber f (+ G, + 2G, ...): its column and canonical start (loaded
   // two rows ahead) and u at its column (one row ahead), so no load waits on another in-row
@@ -388,9 +407,9 @@ __global__ void __launch_bounds__(cell_threads<S, JAC>(),
   }
   uint32_t phase = 0;  // WB: parity bit per buffer
 
-  Meta cur = meta(A, row);
-  Meta nxt = meta(A, row + NG);
-  Meta nn = meta(A, row + 2 * NG);
+  Meta cur = meta(A, row, lim);
+  Meta nxt = meta(A, row + NG, lim);
+  Meta nn = meta(A, row + 2 * NG, lim);
   int shk, shv, shb;
   stage_in(0, cur, shk, shv, shb);
   S uj_cur[FREG], uj_nxt[FREG];
@@ -399,18 +418,18 @@ __global__ void __launch_bounds__(cell_threads<S, JAC>(),
   fibers(nxt, fj_nxt, fb_nxt);
   ucols(fj_cur, uj_cur);
   int st = 0;
-  for (int64_t wr = wrow0; wr < A.n_u; wr += NG, row += NG) {
+  for (int64_t wr = wrow0; wr < lim; wr += NG, row += NG) {
     const int ne = (int)(cur.e1 - cur.e0);
     const int nc = ne / D1;
     const int nf = (int)(cur.f1 - cur.f0);
     // ---- prefetch: the next row's stream (async) and fiber data, metadata two rows ahead
     int nshk = 0, nshv = 0, nshb = 0;
-    if (WB || row + NG < A.n_u) stage_in(st ^ 1, nxt, nshk, nshv, nshb);  // WB: 0-byte arrive past the end
+    if (WB || row + NG < lim) stage_in(st ^ 1, nxt, nshk, nshv, nshb);  // WB: 0-byte arrive past the end
     else commit();
     ucols(fj_nxt, uj_nxt);
     int fj_nn[FREG], fb_nn[FREG];
     fibers(nn, fj_nn, fb_nn);
-    const Meta n3 = meta(A, row + 3 * NG);
+    const Meta n3 = meta(A, row + 3 * NG, lim);
     if constexpr (!WB && JAC == kJacNone) {
       // apply-only: the values of a row go straight to registers when its turn comes; one bulk L2
       // prefetch per warp of its rows' contiguous value span two steps ahead, so that load waits
@@ -461,7 +480,9 @@ __global__ void __launch_bounds__(cell_threads<S, JAC>(),
       if constexpr (kN) {
         // the cell's D1 values (16-byte vector loads); a lane past the row's cells loads cell 0's
         // row and never uses it (no select on the loaded value)
-        if constexpr ((D1 * sizeof(S)) % 16 == 0) {
+        if constexpr (COH) {
+          load_cell_cg<S, D1>(A.chain + (size_t)K * D1, dd[c], C32);
+        } else if constexpr ((D1 * sizeof(S)) % 16 == 0) {
           load_cell_ldg<S, D1>(A.chain + (size_t)K * D1, dd[c], C32);
         } else {
 #pragma unroll
@@ -564,7 +585,7 @@ __global__ void __launch_bounds__(cell_threads<S, JAC>(),
     if constexpr (DO_R) {
 #pragma unroll
       for (int o = G / 2; o > 0; o >>= 1) acc = xadd(acc, __shfl_xor_sync(FM, acc, o, G));
-      if (lane == 0 && row < A.n_u) A.r[row] = acc;
+      if (lane == 0 && row < lim) A.r[row] = acc;
     }
     if constexpr (kJ) {
       // ---- diagonal: lane partials (cell order) + butterfly; the other fibers: their lane sums
@@ -612,6 +633,18 @@ __global__ void __launch_bounds__(cell_threads<S, JAC>(),
     }
     st ^= 1;
   }
+}
+
+template <typename S, int D1, int G, int CPL, int FREG, bool DO_R, int JAC, bool WB, bool C32 = false>
+__global__ void __launch_bounds__(cell_threads<S, JAC>(),
+                                  (JAC == kJacNone || G >= 16) ? 3 * 256 / cell_threads<S, JAC>() : 2 * 256 / cell_threads<S, JAC>())
+    k_cell(const CellArgs<S> A) {
+  constexpr int GPB = cell_threads<S, JAC>() / G;
+  const int64_t NG = (int64_t)gridDim.x * GPB;
+  const int64_t row = (int64_t)blockIdx.x * GPB + threadIdx.x / G;
+  const int64_t wrow0 = (int64_t)blockIdx.x * GPB + (threadIdx.x >> 5) * (32 / G);
+  if (wrow0 >= A.n_u) return;
+  cell_rows<S, D1, G, CPL, FREG, DO_R, JAC, WB, C32, false>(A, row, wrow0, NG, A.n_u);
 }
 
 // Offline: the cell-major copy of a P0-W tensor's rows (one thread per row).
@@ -769,6 +802,132 @@ egfem_status cells_dispatch(const egfem_tensor* t, bool do_r, int jac, bool pack
   return EGFEM_ERR_UNSUPPORTED;
 }
 
+
+// ------------------------------------------------------------------ single-pass Newton step
+// step (1) of the gradient kinds and steps (2)+(3)
+// (L183, L290–292) in ONE launch.  The work is a fixed sequence of items (StepPlan.seq): interp
+// items (CI consecutive cells: w_K and the packed record [w_K, ∂w/∂u_0..∂w/∂u_{d−1}]) and row
+// items (RI consecutive rows: r and the Newton Jacobian row values from the records of the
+// rows' cells).  Warps take items in sequence order from a global counter.  A row item is placed
+// after every interp item that produces a record it reads (+ a lag), waits on those items'
+// release flags and reads the records through L2 (COH loads).  Deadlock-free for any residency:
+// an item waits only on items earlier in the sequence, which were taken by warps that are
+// already running and never wait on later items.  The records a row item reads were written
+// moments earlier (one mesh layer ahead), so they are gathered from L2, and the interp's
+// gathers and FP64 work overlap the row items' streaming in the same SMs.  The flags carry the
+// launch's epoch (no reset between launches, so the step is CUDA-graph capturable); the last
+// warp to finish rewinds the counters and advances the epoch.
+template <typename S>
+struct StepArgs {
+  const double* coords;
+  const float* coordsf;
+  const int32_t* cells;
+  int64_t n_cells;
+  S* w;
+  S* chain;
+  double p;
+  bool minsurf;
+  const int32_t* seq;   // item order: >= 0 interp item, < 0 row item ~r
+  const int32_t* need;  // per row item: first and last interp item it reads
+  uint32_t* sync;       // [0] item counter, [1] finished warps, [2] epoch, [4..] interp item flags
+  int n_items;
+  int CI, RI;
+  bool nowait;          // diagnostics (EGFEM_STEP_MODE=2: row items only, no waiting)
+};
+
+__device__ __forceinline__ uint32_t ld_acquire(const uint32_t* p) {
+  uint32_t v;
+  asm volatile("ld.acquire.gpu.global.u32 %0, [%1];" : "=r"(v) : "l"(p) : "memory");
+  return v;
+}
+__device__ __forceinline__ void st_release(uint32_t* p, uint32_t v) {
+  asm volatile("st.release.gpu.global.u32 [%0], %1;" ::"l"(p), "r"(v) : "memory");
+}
+
+template <typename S, int D1, int G, int CPL, int FREG, bool C32, bool CF>
+__global__ void __launch_bounds__(cell_threads<S, kJacNewtonPK>(), 2 * 256 / cell_threads<S, kJacNewtonPK>())
+    k_step(const CellArgs<S> A, const StepArgs<S> B) {
+  constexpr int D = D1 - 1;
+  constexpr int WPG = 32 / G;
+  constexpr unsigned FM = 0xffffffffu;
+  const int wl = threadIdx.x & 31;
+  uint32_t* const flags = B.sync + 4;
+  const uint32_t ep = *reinterpret_cast<volatile uint32_t*>(B.sync + 2) + 1u;
+  for (;;) {
+    uint32_t it = 0;
+    if (wl == 0) it = atomicAdd(B.sync, 1u);
+    it = __shfl_sync(FM, it, 0);
+    if (it >= (uint32_t)B.n_items) break;
+    const int code = __ldg(B.seq + it);
+    if (code >= 0) {
+      const int64_t c0 = (int64_t)code * B.CI;
+      const int64_t c1 = min(c0 + (int64_t)B.CI, B.n_cells);
+      ip::interp_cells<S, D, true, true, CF>(B.coords, B.coordsf, B.cells, B.cells, nullptr, c0 + wl, c1, 32, A.u,
+                                               B.w, B.chain, B.p, B.minsurf, 1);
+      __syncwarp();  // every lane's records are written (the release below is cumulative over them)
+      if (wl == 0) st_release(flags + code, ep);
+    } else {
+      const int r = ~code;
+      const int lo = __ldg(B.need + 2 * r), hi = __ldg(B.need + 2 * r + 1);
+      if (!B.nowait)
+        for (int q = lo + wl; q <= hi; q += 32)
+          while (ld_acquire(flags + q) != ep) __nanosleep(64);
+      __syncwarp();
+      const int64_t base = (int64_t)r * B.RI;
+      const int64_t lim = min(base + (int64_t)B.RI, A.n_u);
+      cell_rows<S, D1, G, CPL, FREG, true, kJacNewtonPK, false, C32, true>(A, base + wl / G, base, WPG, lim);
+    }
+  }
+  __syncwarp();
+  if (wl == 0) {
+    const uint32_t total = gridDim.x * (blockDim.x / 32);
+    __threadfence();
+    if (atomicAdd(B.sync + 1, 1u) == total - 1u) {  // every other warp has left the item loop
+      B.sync[0] = 0u;
+      B.sync[1] = 0u;
+      __threadfence();
+      atomicAdd(B.sync + 2, 1u);
+    }
+  }
+}
+
+// per row item: the first and last interp item whose records its rows read
+__global__ void k_step_need(int64_t n_u, const int64_t* __restrict__ row_nz, const uint32_t* __restrict__ ck_k, int d1,
+                            int RI, int CI, int n_ritems, int32_t* need) {
+  const int r = blockIdx.x * blockDim.x + threadIdx.x;
+  if (r >= n_ritems) return;
+  uint32_t lo = 0xffffffffu, hi = 0u;
+  bool any = false;
+  for (int64_t i = (int64_t)r * RI; i < min((int64_t)(r + 1) * RI, n_u); ++i) {
+    const int64_t a = row_nz[i] / d1, b = row_nz[i + 1] / d1;
+    if (b <= a) continue;
+    any = true;
+    lo = min(lo, ck_k[a]);       // a row's cells are in ascending K
+    hi = max(hi, ck_k[b - 1]);
+  }
+  need[2 * r] = any ? (int32_t)(lo / (uint32_t)CI) : 0;
+  need[2 * r + 1] = any ? (int32_t)(hi / (uint32_t)CI) : -1;
+}
+
+template <typename S, int D1, int G, int CPL, int FREG, bool C32>
+egfem_status run_step(const egfem_tensor* t, const CellArgs<S>& A, const StepArgs<S>& B, cudaStream_t s) {
+  using L = CellSmem<S, D1, G, CPL, true, G * FREG>;
+  auto fn = B.coordsf ? k_step<S, D1, G, CPL, FREG, C32, true> : k_step<S, D1, G, CPL, FREG, C32, false>;
+  constexpr int CT = cell_threads<S, kJacNewtonPK>();
+  const int smem = L::bytes * (CT / G);
+  if (smem > 48 * 1024) EGFEM_CUDA_TRY(cudaFuncSetAttribute(fn, cudaFuncAttributeMaxDynamicSharedMemorySize, smem));
+  const int dev = t->device & 63;
+  if (!g_sm_count[dev])
+    EGFEM_CUDA_TRY(cudaDeviceGetAttribute(&g_sm_count[dev], cudaDevAttrMultiProcessorCount, t->device));
+  int per_sm = 0;
+  EGFEM_CUDA_TRY(cudaOccupancyMaxActiveBlocksPerMultiprocessor(&per_sm, fn, CT, smem));
+  const int grid = std::max(per_sm, 1) * g_sm_count[dev];
+  fn<<<grid, CT, smem, s>>>(A, B);
+  count_launch();
+  EGFEM_CUDA_TRY(cudaGetLastError());
+  return EGFEM_OK;
+}
+
 }  // namespace
 
 bool cells_path_ok(const egfem_tensor* t, int jac) {
@@ -824,5 +983,180 @@ egfem_status make_p0_cells(egfem_tensor* t) {
   }
   return EGFEM_OK;
 }
+
+
+struct StepPlan {
+  int CI = 0, RI = 0, n_interp = 0, n_ritems = 0, n_items = 0, mode = 0;
+  int32_t* seq = nullptr;
+  int32_t* need = nullptr;
+  uint32_t* sync = nullptr;
+};
+
+void free_step_plan(StepPlan* sp) {
+  if (!sp) return;
+  cudaFree(sp->seq);
+  cudaFree(sp->need);
+  cudaFree(sp->sync);
+  delete sp;
+}
+
+// The item sequence of the single-pass step: interp items in cell order; row item r right after
+// interp item need_hi(r) + lag (EGFEM_STEP_LAG, default 2048 items), so its records were
+// produced a while before it is taken.  Opt-in: EGFEM_STEP=1 when the tensor is built (measured
+// slower than the two launches on B200 — both halves are bound by the same load/store pipe,
+// so egfem_step issues the two launches by default).  EGFEM_STEP_CI = cells per
+// lane of an interp item (default 32: 1024 cells), EGFEM_STEP_RI = rows per row item (default 64).
+egfem_status make_step_plan(egfem_tensor* t) {
+  const char* en = getenv("EGFEM_STEP");
+  if (!en || en[0] != '1') return EGFEM_OK;
+  if (!t->ck_val || !t->has_mesh || !t->w_p0 || t->nwc != 1 || !t->wdofs_is_iota || !t->vdofs_is_cells ||
+      (t->dim != 2 && t->dim != 3) || t->n_f != t->n_cells || t->row_begin != 0 ||
+      t->col_begin != 0 || t->int_row_lo >= 0 || t->n_u <= 0 || t->n_cells <= 0)
+    return EGFEM_OK;
+  CellCfg c{};
+  if (!pick_cells(t, &c)) return EGFEM_OK;
+  const int m = getenv("EGFEM_STEP_CI") ? std::max(1, atoi(getenv("EGFEM_STEP_CI"))) : 32;
+  int RI = getenv("EGFEM_STEP_RI") ? std::max(1, atoi(getenv("EGFEM_STEP_RI"))) : 64;
+  RI = (RI + 15) / 16 * 16;  // a multiple of the groups per warp of every configuration
+  const int lag = getenv("EGFEM_STEP_LAG") ? std::max(0, atoi(getenv("EGFEM_STEP_LAG"))) : 2048;
+  const int64_t CI = 32LL * m;
+  const int64_t n_interp = (t->n_cells + CI - 1) / CI, n_ritems = (t->n_u + RI - 1) / RI;
+  if (n_interp + n_ritems >= (int64_t(1) << 31) - 1) return EGFEM_OK;
+  StepPlan* sp = new StepPlan;
+  sp->CI = (int)CI;
+  sp->RI = RI;
+  sp->n_interp = (int)n_interp;
+  sp->n_ritems = (int)n_ritems;
+  sp->n_items = (int)(n_interp + n_ritems);
+  auto bail = [&](cudaError_t e) {
+    free_step_plan(sp);
+    set_error(std::string("step plan: ") + cudaGetErrorString(e));
+    return EGFEM_ERR_CUDA;
+  };
+  cudaError_t e;
+  if ((e = cudaMalloc(&sp->need, sizeof(int32_t) * 2 * n_ritems))) return bail(e);
+  if ((e = cudaMalloc(&sp->seq, sizeof(int32_t) * sp->n_items))) return bail(e);
+  if ((e = cudaMalloc(&sp->sync, sizeof(uint32_t) * (4 + n_interp)))) return bail(e);
+  if ((e = cudaMemset(sp->sync, 0, sizeof(uint32_t) * (4 + n_interp)))) return bail(e);
+  k_step_need<<<(int)((n_ritems + 127) / 128), 128>>>(t->n_u, t->row_nz, t->ck_k, t->dim + 1, RI, (int)CI,
+                                                      (int)n_ritems, sp->need);
+  count_launch();
+  std::vector<int32_t> need(2 * n_ritems);
+  if ((e = cudaMemcpy(need.data(), sp->need, sizeof(int32_t) * 2 * n_ritems, cudaMemcpyDeviceToHost))) return bail(e);
+  // bucket the row items by the interp item they follow (-1: before every interp item)
+  std::vector<int64_t> start(n_interp + 2, 0);
+  auto key = [&](int64_t r) -> int64_t {
+    const int64_t h = need[2 * r + 1];
+    return h < 0 ? -1 : std::min<int64_t>(h + lag, n_interp - 1);
+  };
+  for (int64_t r = 0; r < n_ritems; ++r) ++start[key(r) + 2];
+  for (int64_t q = 1; q < n_interp + 2; ++q) start[q] += start[q - 1];
+  std::vector<int32_t> byk(n_ritems);
+  {
+    std::vector<int64_t> fill(start.begin(), start.end());
+    for (int64_t r = 0; r < n_ritems; ++r) byk[fill[key(r) + 1]++] = (int32_t)r;
+  }
+  std::vector<int32_t> seq;
+  seq.reserve(sp->n_items);
+  for (int64_t x = start[0]; x < start[1]; ++x) seq.push_back(~byk[x]);
+  for (int64_t q = 0; q < n_interp; ++q) {
+    seq.push_back((int32_t)q);
+    for (int64_t x = start[q + 1]; x < start[q + 2]; ++x) seq.push_back(~byk[x]);
+  }
+  if ((int64_t)seq.size() != sp->n_items) {  // cannot happen: every item is placed once
+    free_step_plan(sp);
+    return EGFEM_OK;
+  }
+  // diagnostics: EGFEM_STEP_MODE=1 runs the interp items only, =2 the row items only (no waits;
+  // the records must exist from an earlier full step) — incomplete steps, for timing the parts
+  sp->mode = getenv("EGFEM_STEP_MODE") ? atoi(getenv("EGFEM_STEP_MODE")) : 0;
+  if (sp->mode == 1 || sp->mode == 2) {
+    std::vector<int32_t> part;
+    for (int32_t x : seq)
+      if ((x >= 0) == (sp->mode == 1)) part.push_back(x);
+    seq.swap(part);
+    sp->n_items = (int)seq.size();
+  }
+  if ((e = cudaMemcpy(sp->seq, seq.data(), sizeof(int32_t) * seq.size(), cudaMemcpyHostToDevice))) return bail(e);
+  if (getenv("EGFEM_DEBUG"))
+    fprintf(stderr, "[egfem] step plan: %d interp items of %d cells, %d row items of %d rows, lag %d\n", sp->n_interp,
+            sp->CI, sp->n_ritems, sp->RI, lag);
+  t->step = sp;
+  return EGFEM_OK;
+}
+
+bool step_path_ok(const egfem_tensor* t, egfem_interp_kind kind, const void* chain) {
+  if (!t->step || !packed_chain_kind(kind)) return false;
+  static const char* force = getenv("EGFEM_PATH");
+  if (force && (force[0] == 't' || force[0] == 'r')) return false;
+  // the 3D fp64 instances read each record with one 256-bit load: 32-byte aligned chain
+  if (t->dim == 3 && t->dtype == EGFEM_F64 && (reinterpret_cast<uintptr_t>(chain) & 31u)) return false;
+  CellCfg c{};
+  return pick_cells(t, &c);
+}
+
+template <typename S>
+egfem_status step_dispatch(const egfem_tensor* t, egfem_interp_kind kind, double p, const void* u, void* w,
+                           void* chain, void* r, void* csr, cudaStream_t s) {
+  CellArgs<S> A;
+  A.n_u = t->n_u;
+  A.row_nz = t->row_nz;
+  A.row_fib = t->row_fib;
+  A.fib_j = t->fib_j;
+  A.fib_nz = t->fib_nz;
+  A.ck_k = t->ck_k;
+  A.ck_val = static_cast<const S*>(t->ck_val);
+  A.ck_b = t->ck_b;
+  A.u = static_cast<const S*>(u);
+  A.w = static_cast<const S*>(w);
+  A.chain = static_cast<const S*>(chain);
+  A.r = static_cast<S*>(r);
+  A.csr = static_cast<S*>(csr);
+  A.diag_off = 0;
+  A.chain32 = (reinterpret_cast<uintptr_t>(chain) & 31u) == 0;
+  A.pf = 0;
+  StepArgs<S> B;
+  B.coords = t->dim == 3 ? t->coords4 : t->coords;
+  B.coordsf = t->coordsf;
+  B.cells = t->cells;
+  B.n_cells = t->n_cells;
+  B.w = static_cast<S*>(w);
+  B.chain = static_cast<S*>(chain);
+  B.p = p;
+  B.minsurf = kind == EGFEM_INTERP_MINSURF_P0;
+  B.seq = t->step->seq;
+  B.need = t->step->need;
+  B.sync = t->step->sync;
+  B.n_items = t->step->n_items;
+  B.CI = t->step->CI;
+  B.RI = t->step->RI;
+  B.nowait = t->step->mode == 2;
+  CellCfg c{};
+  if (!pick_cells(t, &c)) return EGFEM_ERR_UNSUPPORTED;
+  if (getenv("EGFEM_DEBUG"))
+    fprintf(stderr, "[egfem] k_step d1=%d G=%d CPL=%d FREG=%d\n", c.d1, c.G, c.CPL, c.FREG);
+#define EGFEM_SC(D_, G_, C_, F_)                                                     \
+  if (c.d1 == D_ && c.G == G_ && c.CPL == C_) {                                      \
+    if constexpr (D_ == 4 && sizeof(S) == 8) return run_step<S, D_, G_, C_, F_, true>(t, A, B, s); \
+    else return run_step<S, D_, G_, C_, F_, false>(t, A, B, s);                      \
+  }
+  EGFEM_SC(3, 2, 3, 4)
+  EGFEM_SC(3, 4, 4, 8)
+  EGFEM_SC(3, 16, 3, 1)
+  EGFEM_SC(4, 8, 3, 2)
+  EGFEM_SC(4, 16, 3, 2)
+  EGFEM_SC(4, 16, 4, 4)
+  EGFEM_SC(4, 32, 3, 1)
+#undef EGFEM_SC
+  return EGFEM_ERR_UNSUPPORTED;
+}
+
+egfem_status launch_step(const egfem_tensor* t, egfem_interp_kind kind, double p, const void* u, void* w, void* chain,
+                         void* r, void* csr_vals, cudaStream_t s) {
+  if (!step_path_ok(t, kind, chain)) return EGFEM_ERR_UNSUPPORTED;
+  if (t->dtype == EGFEM_F64) return step_dispatch<double>(t, kind, p, u, w, chain, r, csr_vals, s);
+  return step_dispatch<float>(t, kind, p, u, w, chain, r, csr_vals, s);
+}
+
 
 }  // namespace egfem

@@ -25,6 +25,7 @@
 
 namespace egfem {
 struct GroupPlan;  // egfem_group.cu: compiled row-group kernels of the batched action
+struct StepPlan;   // egfem_cells.cu: work order of the single-pass Newton step kernel
 
 constexpr int kTileNnz = 1024;   // max nonzeros per tile
 constexpr int kTileFib = 512;    // max fibers per tile
@@ -87,6 +88,7 @@ struct egfem_tensor {
   int32_t* dense_rows = nullptr;  // n_u: rows grouped by stencil width |N(i)| (row order within a width)
   std::vector<std::array<int64_t, 4>> dense_classes;  // host: (width, first entry in dense_rows, count, first block value)
   egfem::GroupPlan* grp = nullptr;  // W = V batched action: row groups with compiled-in patterns (egfem_group.cu)
+  egfem::StepPlan* step = nullptr;  // canonical P0 W: single-pass interp + Newton step (egfem_cells.cu)
 
   // tiles (device + host copy of the count)
   int32_t n_tiles = 0;
@@ -142,6 +144,14 @@ bool cells_path_ok(const egfem_tensor* t, int jac);
 egfem_status launch_cells(const egfem_tensor* t, bool do_r, int jac, bool packed, const void* u, const void* w,
                           const void* chain, void* r, void* csr_vals, cudaStream_t s);
 egfem_status make_p0_cells(egfem_tensor* t);
+// single-pass Newton step (interp of the gradient kinds + fused apply / Newton Jacobian in one
+// launch, egfem_cells.cu): the plan is built with the tensor when it applies; launch_step returns
+// EGFEM_ERR_UNSUPPORTED (nothing launched) when the tensor, kind or pointers do not fit it
+egfem_status make_step_plan(egfem_tensor* t);
+void free_step_plan(StepPlan* sp);
+bool step_path_ok(const egfem_tensor* t, egfem_interp_kind kind, const void* chain);
+egfem_status launch_step(const egfem_tensor* t, egfem_interp_kind kind, double p, const void* u, void* w, void* chain,
+                         void* r, void* csr_vals, cudaStream_t s);
 bool dense_path_ok(const egfem_tensor* t);
 bool dense1_path_ok(const egfem_tensor* t, int jac);
 egfem_status launch_dense1(const egfem_tensor* t, int64_t lo, int64_t hi, bool do_r, int jac, egfem_interp_kind kind,

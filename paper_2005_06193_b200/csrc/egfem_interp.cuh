@@ -1,0 +1,217 @@
+// Step (1) of the gradient kinds, shared by the interp kernel (egfem_kernels.cu) and the
+// single-pass Newton step kernel (egfem_cells.cu).  Internal to libegfem.so.
+#pragma once
+
+#include <cuda_runtime.h>
+#include <stdint.h>
+
+namespace egfem {
+namespace ip {
+
+// GRADPOW_P0: g_K = Σ_a u_{v_a} ∇λ_a (Π_∇u ·₂ u at the cell's DOF), w_K = ‖g_K‖^{p−2},
+// ∂w_K/∂u_{v_m} = (p−2)‖g‖^{p−4} g·∇λ_m (reading C11); chain[K] = [w_K, ∂w_K/∂u_{v_0}
+// .. ∂w_K/∂u_{v_{d−1}}] (packed: the last derivative is −Σ of the others).
+// Thread per cell; 3D reads the cell as one int4 and each vertex as two double2 from the
+// 32-byte padded coordinate array, and writes the chain row as two 16-byte stores.
+template <int D>
+struct CellIdx {
+  int32_t v[D + 1];
+};
+template <int D>
+__device__ __forceinline__ CellIdx<D> load_cidx(const int32_t* __restrict__ t, int64_t c) {
+  CellIdx<D> r;
+  if constexpr (D == 3) {
+    const int4 q = __ldg(reinterpret_cast<const int4*>(t) + c);
+    r.v[0] = q.x;
+    r.v[1] = q.y;
+    r.v[2] = q.z;
+    r.v[3] = q.w;
+  } else {
+#pragma unroll
+    for (int a = 0; a <= D; ++a) r.v[a] = __ldg(t + c * (D + 1) + a);
+  }
+  return r;
+}
+
+// One cell's gathered inputs: vertex coordinates and u at its V DOFs.
+template <typename S, int D>
+struct CellIn {
+  double x[D + 1][D];
+  double uv[D + 1];
+};
+template <typename S, int D, bool SAME, bool CF>
+__device__ __forceinline__ void gather_cell(const double* __restrict__ coords, const float* __restrict__ coordsf,
+                                            const CellIdx<D>& cv, const CellIdx<D>& dv, const S* __restrict__ u,
+                                            CellIn<S, D>& in) {
+#pragma unroll
+  for (int a = 0; a <= D; ++a) {
+    const int64_t v = cv.v[a];
+    if constexpr (D == 3 && CF) {  // exact float copy of the coordinates: one 16-byte load
+      const float4 q = __ldg(reinterpret_cast<const float4*>(coordsf) + v);
+      in.x[a][0] = (double)q.x;
+      in.x[a][1] = (double)q.y;
+      in.x[a][2] = (double)q.z;
+    } else if constexpr (D == 2 && CF) {  // exact float copy: one 8-byte load
+      const float2 q = __ldg(reinterpret_cast<const float2*>(coordsf) + v);
+      in.x[a][0] = (double)q.x;
+      in.x[a][1] = (double)q.y;
+    } else if constexpr (D == 3) {
+      const double2 xy = __ldg(reinterpret_cast<const double2*>(coords + v * 4));
+      in.x[a][0] = xy.x;
+      in.x[a][1] = xy.y;
+      in.x[a][2] = __ldg(coords + v * 4 + 2);
+    } else if constexpr (D == 2) {
+      const double2 xy = __ldg(reinterpret_cast<const double2*>(coords + v * 2));
+      in.x[a][0] = xy.x;
+      in.x[a][1] = xy.y;
+    } else {
+      in.x[a][0] = __ldg(coords + v);
+    }
+    in.uv[a] = (double)__ldg(u + dv.v[a]);
+  }
+}
+
+template <typename S, int D, bool IOTA>
+__device__ __forceinline__ void gradpow_cell(const CellIn<S, D>& in, int64_t c, const int32_t* __restrict__ wdofs,
+                                             S* __restrict__ w, S* __restrict__ chain, double p, bool minsurf,
+                                             int nw) {
+  const auto& x = in.x;
+  const auto& uv = in.uv;
+  // barycentric gradients of vertices 1..D from the edge vectors e_a = x_a − x_0
+  double g[D + 1][D];
+  if constexpr (D == 1) {
+    g[1][0] = 1.0 / (x[1][0] - x[0][0]);
+  } else if constexpr (D == 2) {
+    const double e1x = x[1][0] - x[0][0], e1y = x[1][1] - x[0][1];
+    const double e2x = x[2][0] - x[0][0], e2y = x[2][1] - x[0][1];
+    const double inv = 1.0 / (e1x * e2y - e1y * e2x);
+    g[1][0] = e2y * inv;
+    g[1][1] = -e2x * inv;
+    g[2][0] = -e1y * inv;
+    g[2][1] = e1x * inv;
+  } else {
+    double e[3][3];
+#pragma unroll
+    for (int a = 0; a < 3; ++a)
+#pragma unroll
+      for (int q = 0; q < 3; ++q) e[a][q] = x[a + 1][q] - x[0][q];
+    const double c23[3] = {e[1][1] * e[2][2] - e[1][2] * e[2][1], e[1][2] * e[2][0] - e[1][0] * e[2][2],
+                           e[1][0] * e[2][1] - e[1][1] * e[2][0]};
+    const double c31[3] = {e[2][1] * e[0][2] - e[2][2] * e[0][1], e[2][2] * e[0][0] - e[2][0] * e[0][2],
+                           e[2][0] * e[0][1] - e[2][1] * e[0][0]};
+    const double c12[3] = {e[0][1] * e[1][2] - e[0][2] * e[1][1], e[0][2] * e[1][0] - e[0][0] * e[1][2],
+                           e[0][0] * e[1][1] - e[0][1] * e[1][0]};
+    const double inv = 1.0 / (e[0][0] * c23[0] + e[0][1] * c23[1] + e[0][2] * c23[2]);
+#pragma unroll
+    for (int q = 0; q < 3; ++q) {
+      g[1][q] = c23[q] * inv;
+      g[2][q] = c31[q] * inv;
+      g[3][q] = c12[q] * inv;
+    }
+  }
+#pragma unroll
+  for (int q = 0; q < D; ++q) {
+    double s = 0.0;
+#pragma unroll
+    for (int a = 1; a <= D; ++a) s += g[a][q];
+    g[0][q] = -s;
+  }
+  double gu[D];
+#pragma unroll
+  for (int q = 0; q < D; ++q) {
+    double s = 0.0;
+#pragma unroll
+    for (int a = 0; a <= D; ++a) s += uv[a] * g[a][q];
+    gu[q] = s;
+  }
+  double gg = 0.0;
+#pragma unroll
+  for (int q = 0; q < D; ++q) gg += gu[q] * gu[q];
+  double wk, fac;
+  if (minsurf) {  // a = (1 + ‖g‖²)^{−1/2}, ∂a/∂u_m = −(1 + ‖g‖²)^{−3/2} g·∇λ_m
+    wk = 1.0 / sqrt(1.0 + gg);
+    fac = -(wk * wk * wk);
+  } else if (p == 4.0) {
+    wk = gg;
+    fac = 2.0;
+  } else if (p == 3.0) {
+    const double nrm = sqrt(gg);
+    wk = nrm;
+    fac = gg > 0.0 ? 1.0 / nrm : 0.0;
+  } else if (p == 2.0) {
+    wk = 1.0;
+    fac = 0.0;
+  } else {
+    wk = pow(gg, 0.5 * (p - 2.0));
+    fac = gg > 0.0 ? (p - 2.0) * pow(gg, 0.5 * (p - 4.0)) : 0.0;
+  }
+  // the packed chain record (include/egfem.h egfem_interp): [w_K, ∂w/∂u_{v_0} .. ∂w/∂u_{v_{d−1}}];
+  // ∂w/∂u_{v_d} = −Σ_{m<d} (Σ_m ∇λ_m = 0), rebuilt by the Jacobian kernels — so the Newton kernel
+  // reads w and D_u w of a cell with one gather
+  S dm[D + 1];
+  if (chain) {
+    dm[0] = (S)wk;
+#pragma unroll
+    for (int a = 0; a < D; ++a) {
+      double s = 0.0;
+#pragma unroll
+      for (int q = 0; q < D; ++q) s += gu[q] * g[a][q];
+      dm[a + 1] = (S)(fac * s);
+    }
+  }
+  // the cell's W DOFs (P0: one; QUAD: N_q points, ∇u_h is constant on the cell)
+  if (IOTA) nw = 1;  // canonical P0 (the IOTA instance is only launched for it)
+  for (int l = 0; l < nw; ++l) {
+    const int64_t K = IOTA ? c : (int64_t)__ldg(wdofs + c * nw + l);
+    w[K] = (S)wk;
+    if (chain) {
+      if constexpr (D == 3 && sizeof(S) == 8) {  // one 32-byte store (sm_100 256-bit STG) when aligned
+        if ((reinterpret_cast<uintptr_t>(chain) & 31u) == 0) {
+          asm volatile("st.global.v4.f64 [%0], {%1, %2, %3, %4};" ::"l"(chain + K * 4), "d"(dm[0]), "d"(dm[1]),
+                       "d"(dm[2]), "d"(dm[3])
+                       : "memory");
+        } else {  // the API's 16-byte alignment
+          reinterpret_cast<double2*>(chain + K * 4)[0] = make_double2(dm[0], dm[1]);
+          reinterpret_cast<double2*>(chain + K * 4)[1] = make_double2(dm[2], dm[3]);
+        }
+      } else if constexpr (D == 3) {
+        reinterpret_cast<float4*>(chain)[K] = make_float4(dm[0], dm[1], dm[2], dm[3]);
+      } else {
+#pragma unroll
+        for (int a = 0; a <= D; ++a) chain[K * (D + 1) + a] = dm[a];
+      }
+    }
+  }
+}
+
+// Cells c, c + stride, ... < cend of one thread, software-pipelined: the cell record is loaded
+// two cells ahead and the next cell's vertex coordinates and u one cell ahead, so the dependent
+// record → coordinates gather chain overlaps the current cell's arithmetic instead of stalling.
+template <typename S, int D, bool SAME, bool IOTA, bool CF>
+__device__ __forceinline__ void interp_cells(const double* __restrict__ coords, const float* __restrict__ coordsf,
+                                             const int32_t* __restrict__ cells, const int32_t* __restrict__ vdofs,
+                                             const int32_t* __restrict__ wdofs, int64_t c, int64_t cend,
+                                             int64_t stride, const S* __restrict__ u, S* __restrict__ w,
+                                             S* __restrict__ chain, double p, bool minsurf, int nw) {
+  if (c >= cend) return;
+  auto idx = [&](int64_t cc, CellIdx<D>& cv, CellIdx<D>& dv) {
+    const int64_t q = cc < cend ? cc : c;  // clamped: a valid record, never used
+    cv = load_cidx<D>(cells, q);
+    dv = SAME ? cv : load_cidx<D>(vdofs, q);
+  };
+  CellIdx<D> cv1, dv1, cv2, dv2;
+  idx(c, cv1, dv1);
+  CellIn<S, D> cur;
+  gather_cell<S, D, SAME, CF>(coords, coordsf, cv1, dv1, u, cur);
+  idx(c + stride, cv2, dv2);
+  for (; c < cend; c += stride) {
+    CellIn<S, D> nxt;
+    gather_cell<S, D, SAME, CF>(coords, coordsf, cv2, dv2, u, nxt);  // next cell's gathers in flight
+    idx(c + 2 * stride, cv2, dv2);                                    // record two cells ahead
+    gradpow_cell<S, D, IOTA>(cur, c, wdofs, w, chain, p, minsurf, nw);
+    cur = nxt;
+  }
+}
+
+}  // namespace ip
+}  // namespace egfem
