@@ -38,8 +38,9 @@ def main():
                       "launch, lts__t_sector_hit_rate.pct); see profiles/README.md"}
     keys = ["interp", "apply", "jac_picard", "jac_newton", "fused"]
     rnd = sys.argv[4] if len(sys.argv) > 4 else "r2"
-    summ = {"cfg4-f64": f"profiles/{rnd}_cfg4_f64_ncu_full_v1.txt", "cfg4-f32": f"profiles/{rnd}_cfg4_f32_ncu_full_v1.txt",
-            "cfg5-f64": f"profiles/{rnd}_cfg5_f64_ncu_full_v1.txt"}
+    ver = sys.argv[6] if len(sys.argv) > 6 else "v3"  # the profiles/ summary version the entries cite
+    summ = {"cfg4-f64": f"profiles/{rnd}_cfg4_f64_ncu_full_{ver}.txt", "cfg4-f32": f"profiles/{rnd}_cfg4_f32_ncu_full_{ver}.txt",
+            "cfg5-f64": f"profiles/{rnd}_cfg5_f64_ncu_full_{ver}.txt"}
     for rep, wl in ((sys.argv[1], "cfg4-f64"), (sys.argv[2], "cfg4-f32")):
         rs = rows(rep)
         out[wl] = {k: entry(d, summ[wl]) for k, d in zip(keys, rs)}

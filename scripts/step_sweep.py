@@ -42,7 +42,7 @@ def main():
     name = sys.argv[1] if len(sys.argv) > 1 else "cfg4"
     dtype = 1 if (len(sys.argv) > 2 and sys.argv[2] == "f32") else 0
     K = int(sys.argv[3]) if len(sys.argv) > 3 else 30
-    variants = sys.argv[4:] or ["16,64,512"]
+    variants = [v for v in sys.argv[4:] if v != "-"] if len(sys.argv) > 4 else ["32,64,2048"]
     pr = I.make_problem(name)
     for v in ["two", "interp", "fused"] + variants:
         base = v in ("two", "interp", "fused")
