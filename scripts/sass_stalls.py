@@ -1,5 +1,6 @@
 """Summarise an `ncu --page source --csv --print-source sass` dump: stall samples by reason and by
-instruction opcode, and the top stalled instructions.  usage: sass_stalls.py dump.csv [top]"""
+instruction opcode, and the top stalled instructions (the first kernel of a multi-kernel dump).
+usage: sass_stalls.py dump.csv [top]"""
 import collections
 import csv
 import sys
@@ -15,6 +16,8 @@ by_op = collections.Counter()
 by_op_reason = collections.defaultdict(collections.Counter)
 insts = []
 for r in rows[2:]:
+    if r and r[0] == "Kernel Name":  # a multi-kernel dump: the first kernel only
+        break
     if len(r) < len(h):
         continue
     src = r[si].strip()
