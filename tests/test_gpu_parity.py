@@ -162,7 +162,8 @@ def test_cfg4_full_size_sampled_rows(eg, orc, dtype):
 
 
 @pytest.mark.parametrize("name,n", [("cfg4", 6), ("cfg4", 10), ("cfg3", 9), ("cfg2", 17), ("cfg1", 300),
-                                    ("biochem_p1", 20), ("minsurf2d", 12)])
+                                    ("biochem_p1", 20), ("minsurf2d", 12), ("minsurf3d", 8), ("plap3d_i2", 5),
+                                    ("quadratic_i4", 16)])
 def test_fp32_small(eg, orc, name, n):
     """fp32 handles (the fp64 build rounded once) on every single-vector kernel family: cell-major
     P0 (cfg3/cfg4), W = V dense blocks (cfg1/cfg2, RECIPROCAL Newton), MINSURF interp."""
@@ -716,3 +717,29 @@ def test_batched_groups_wide_batches(eg, orc, B, same):
     torch.cuda.synchronize()
     ref = o.apply_batched(pr.u, Wt.cpu().numpy().T)
     assert rel_l2(R.cpu().numpy().T, ref) <= FP64_TOL
+
+
+@pytest.mark.parametrize("name,n", [("plap3d_i2", 6), ("cfg4", 9), ("quadratic_i4", 20)])
+def test_row_subranges_bitwise(eg, name, n):
+    """egfem_apply_jacobian_rows over three row ranges (ragged, one of them empty) writes exactly the
+    whole-tensor call's values in those rows (the cell-major kernel on a row view; 3D I_2 rows of
+    384 nonzeros take the 32-lane configuration)."""
+    import torch
+    from gpu_helpers import needs_chain
+    pr = I.make_problem(name, n=n)
+    t = eg.egfem_tensor_build(pr.mesh, pr.V, pr.W, pr.form, device=0)
+    assert eg.egfem_kernel_name(t, 2, eg.JAC_NEWTON, pr.interp, pr.p).startswith("k_cell")
+    u = torch.tensor(pr.u, device="cuda")
+    w = torch.empty(t.n_f, dtype=torch.float64, device="cuda")
+    chain = torch.empty(t.n_f * (pr.mesh.dim + 1), dtype=torch.float64, device="cuda") if needs_chain(pr) else None
+    eg.egfem_interp(t, pr.interp, pr.p, u, w, chain)
+    r = torch.empty(t.n_u, dtype=torch.float64, device="cuda")
+    J = torch.empty(t.nnz_csr, dtype=torch.float64, device="cuda")
+    eg.egfem_apply_jacobian(t, eg.JAC_NEWTON, pr.interp, pr.p, u, w, chain, r, J)
+    r2 = torch.full_like(r, float("nan"))
+    J2 = torch.full_like(J, float("nan"))
+    cuts = [0, t.n_u // 3 + 1, t.n_u // 3 + 1, t.n_u - 7, t.n_u]
+    for lo, hi in zip(cuts[:-1], cuts[1:]):
+        eg.egfem_apply_jacobian_rows(t, eg.JAC_NEWTON, pr.interp, pr.p, u, w, chain, r2, J2, lo, hi)
+    torch.cuda.synchronize()
+    assert torch.equal(r, r2) and torch.equal(J, J2)
