@@ -53,6 +53,9 @@ struct CellArgs {
   const uint32_t* ck_k;    // per cell of a row: K
   const S* ck_val;         // per nonzero, cell-major: T_{i v_m K}
   const uint16_t* ck_b;    // per nonzero: fiber index in row (low byte) | canonical position (high)
+  const uint64_t* ck_m = nullptr;   // per cell of a row: the packed word (egfem_tensor::ck_m), PM kernels
+  const uint32_t* ck_kb = nullptr;  // per row: K of its first cell (PM)
+  int fb = 0, fw = 0, ks = 0;       // PM field widths: fiber bits, fiber + position bits, shift of K − kb
   const S* u;
   const S* w;
   const S* chain;          // (D_u w)_{K m}, N_f x (d+1)
@@ -136,7 +139,7 @@ __device__ __forceinline__ float xfma(float a, float b, float c) { return __fmaf
 // scratch.  With warp-level bulk staging the 32/G groups of a warp pool their stage regions
 // into one warp stage per buffer (the warp's rows are consecutive, so their slices are one
 // contiguous span per array) and the warp's two mbarriers sit in group 0's tail.
-template <typename S, int D1, int G, int CPL, bool JT, int SUN = 0>
+template <typename S, int D1, int G, int CPL, bool JT, int SUN = 0, bool NS = false>
 struct CellSmem {
   static constexpr int CC = G * CPL;  // cells per row (max)
   static constexpr int CE = CC * D1;  // nonzeros per row (max)
@@ -147,7 +150,7 @@ struct CellSmem {
   static constexpr int st_k = 0;
   static constexpr int st_v = (st_k + CC * 4 + 32 + 15) & ~15;
   static constexpr int st_b = st_v;
-  static constexpr int stage = (st_b + CE * 2 + 32 + 15) & ~15;
+  static constexpr int stage = NS ? 0 : (st_b + CE * 2 + 32 + 15) & ~15;
   static constexpr int o_t = 2 * stage;  // S[CE]: Jacobian terms at canonical positions
   // warp stage (bulk): WPG groups' slices back to back, each array with 32 B of slack
   static constexpr int WPG = 32 / G;
@@ -324,13 +327,17 @@ __host__ __device__ constexpr bool cells_su() {
 // COH: the chain records are read through L2 only (ld.global.cg), not the non-coherent
 // read-only path — the single-pass step kernel writes them during the same launch.
 // Rows row, row + NG, ... < lim of one group; wrow0 is the first row of the group's warp.
-template <typename S, int D1, int G, int CPL, int FREG, bool DO_R, int JAC, bool WB, bool C32, bool COH>
+// PM: the row's per-cell data comes from the packed 64-bit words (ck_m / ck_kb), loaded one row
+// ahead straight into registers — no shared-memory staging of K and (fiber, position) slices.
+template <typename S, int D1, int G, int CPL, int FREG, bool DO_R, int JAC, bool WB, bool C32, bool COH,
+          bool PM = false>
 __device__ __forceinline__ void cell_rows(const CellArgs<S>& A, int64_t row, const int64_t wrow0, const int64_t NG,
                                           const int64_t lim) {
   constexpr bool kN = JAC == kJacNewtonP0 || JAC == kJacNewtonPK;
   constexpr bool kPK = JAC == kJacNewtonPK;
   constexpr bool SU = cells_su<S, FREG, JAC>() && (DO_R || kN);
-  using L = CellSmem<S, D1, G, CPL, JAC != kJacNone, SU ? G * FREG : 0>;
+  static_assert(!(PM && WB), "packed row words replace the staged slices");
+  using L = CellSmem<S, D1, G, CPL, JAC != kJacNone, SU ? G * FREG : 0, PM>;
   constexpr bool kJ = JAC != kJacNone;
   constexpr bool kU = DO_R || kN;  // u (and B_iK) needed; the Picard matrix alone reads no u
   // Control flow is warp-uniform (a group past the last row runs on an empty one), so
@@ -397,6 +404,22 @@ __device__ __forceinline__ void cell_rows(const CellArgs<S>& A, int64_t row, con
       commit();
     }
   };
+  // PM: the lane's packed words of a row (streamed once: L1 bypass, L2 evict-first) and the row's
+  // first K; a lane past the row's cells holds 0 and never uses it
+  auto words = [&](const Meta& m, int64_t r, uint64_t* mw, uint32_t& kb) {
+    const int n = (int)(m.e1 - m.e0) / D1;
+#pragma unroll
+    for (int c = 0; c < CPL; ++c) {
+      const int q = lane + c * G;
+      uint64_t x = 0;
+      if (q < n)
+        asm("ld.global.nc.L1::no_allocate.L2::cache_hint.u64 %0, [%1], %2;"
+            : "=l"(x)
+            : "l"(A.ck_m + m.e0 / D1 + q), "l"(pol));
+      mw[c] = x;
+    }
+    kb = r < lim ? __ldg(A.ck_kb + r) : 0u;
+  };
   if constexpr (WB) {
     if ((threadIdx.x & 31) == 0) {
       bar_init(&bars[0]);
@@ -410,8 +433,11 @@ __device__ __forceinline__ void cell_rows(const CellArgs<S>& A, int64_t row, con
   Meta cur = meta(A, row, lim);
   Meta nxt = meta(A, row + NG, lim);
   Meta nn = meta(A, row + 2 * NG, lim);
-  int shk, shv, shb;
-  stage_in(0, cur, shk, shv, shb);
+  int shk = 0, shv = 0, shb = 0;
+  uint64_t mw_cur[PM ? CPL : 1], mw_nxt[PM ? CPL : 1];
+  uint32_t kb_cur = 0, kb_nxt = 0;
+  if constexpr (PM) words(cur, row, mw_cur, kb_cur);
+  else stage_in(0, cur, shk, shv, shb);
   S uj_cur[FREG], uj_nxt[FREG];
   int fb_cur[FREG], fb_nxt[FREG], fj_cur[FREG], fj_nxt[FREG];
   fibers(cur, fj_cur, fb_cur);
@@ -424,7 +450,8 @@ __device__ __forceinline__ void cell_rows(const CellArgs<S>& A, int64_t row, con
     const int nf = (int)(cur.f1 - cur.f0);
     // ---- prefetch: the next row's stream (async) and fiber data, metadata two rows ahead
     int nshk = 0, nshv = 0, nshb = 0;
-    if (WB || row + NG < lim) stage_in(st ^ 1, nxt, nshk, nshv, nshb);  // WB: 0-byte arrive past the end
+    if constexpr (PM) words(nxt, row + NG, mw_nxt, kb_nxt);
+    else if (WB || row + NG < lim) stage_in(st ^ 1, nxt, nshk, nshv, nshb);  // WB: 0-byte arrive past the end
     else commit();
     ucols(fj_nxt, uj_nxt);
     int fj_nn[FREG], fb_nn[FREG];
@@ -449,7 +476,7 @@ __device__ __forceinline__ void cell_rows(const CellArgs<S>& A, int64_t row, con
     if constexpr (WB) {
       bar_wait(&bars[st], (phase >> st) & 1u);
       phase ^= 1u << st;
-    } else {
+    } else if constexpr (!PM) {
       wait_prev();
     }
     __syncwarp();
@@ -475,8 +502,14 @@ __device__ __forceinline__ void cell_rows(const CellArgs<S>& A, int64_t row, con
     for (int c = 0; c < CPL; ++c) {
       const int q = lane + c * G;
       const bool ok = q < nc;
-      const uint32_t K = ok ? bk[q] : 0u;
-      if constexpr (!kPK) wk[c] = ok ? __ldg(A.w + K) : S(0);
+      uint32_t K;
+      if constexpr (PM) K = ok ? kb_cur + (uint32_t)(mw_cur[c] >> A.ks) : 0u;
+      else K = ok ? bk[q] : 0u;
+      // PM: no select on a loaded value here (in the PM instances it stalled the warp at once:
+      // fused 0.70 -> 0.64 ms on cfg4); a lane past the row's cells loads a valid cell's data and
+      // every use below is predicated on ok.  The staged instances keep the select (measured
+      // faster there: 0.67 vs 0.70 ms) — the two forms give the same sums.
+      if constexpr (!kPK) wk[c] = PM ? __ldg(A.w + K) : ok ? __ldg(A.w + K) : S(0);
       if constexpr (kN) {
         // the cell's D1 values (16-byte vector loads); a lane past the row's cells loads cell 0's
         // row and never uses it (no select on the loaded value)
@@ -489,7 +522,7 @@ __device__ __forceinline__ void cell_rows(const CellArgs<S>& A, int64_t row, con
           for (int m = 0; m < D1; ++m) dd[c][m] = __ldg(A.chain + (size_t)K * D1 + m);
         }
         if constexpr (kPK) {  // packed record [w_K, D_0 .. D_{d−1}]: D_d = −Σ_{m<d} D_m
-          wk[c] = ok ? dd[c][0] : S(0);
+          wk[c] = PM ? dd[c][0] : ok ? dd[c][0] : S(0);
           S sd = S(0);
 #pragma unroll
           for (int m = 0; m + 1 < D1; ++m) {
@@ -533,7 +566,14 @@ __device__ __forceinline__ void cell_rows(const CellArgs<S>& A, int64_t row, con
 #pragma unroll
           for (int m = 0; m < D1; ++m) tv[m] = tvg[c][m];
         }
-        if constexpr (D1 == 4) {
+        if constexpr (PM) {  // (fiber, position) fields of the packed word, re-packed as in ck_b
+          const uint32_t fmk = (1u << A.fb) - 1u, pmk = (1u << (A.fw - A.fb)) - 1u;
+#pragma unroll
+          for (int m = 0; m < D1; ++m) {
+            const uint32_t x = (uint32_t)(mw_cur[c] >> (m * A.fw));
+            bq[m] = (x & fmk) | (((x >> A.fb) & pmk) << kCkPosShift);
+          }
+        } else if constexpr (D1 == 4) {
           const uint2 x = *reinterpret_cast<const uint2*>(bb + q * D1);  // 8-byte aligned: e0 % 4 == 0
           bq[0] = x.x & 0xffffu;
           bq[1] = x.x >> 16;
@@ -569,7 +609,9 @@ __device__ __forceinline__ void cell_rows(const CellArgs<S>& A, int64_t row, con
           B = (m == 0) ? xmul(tv[m], um) : xfma(tv[m], um, B);
         }
       }
-      if constexpr (DO_R) acc = xfma(wk[c], B, acc);
+      if constexpr (DO_R) {
+        if (!PM || ok) acc = xfma(wk[c], B, acc);
+      }
       if constexpr (kJ) {
         if (ok) {
 #pragma unroll
@@ -620,6 +662,11 @@ __device__ __forceinline__ void cell_rows(const CellArgs<S>& A, int64_t row, con
     cur = nxt;
     nxt = nn;
     nn = n3;
+    if constexpr (PM) {
+#pragma unroll
+      for (int c = 0; c < CPL; ++c) mw_cur[c] = mw_nxt[c];
+      kb_cur = kb_nxt;
+    }
     shk = nshk;
     shv = nshv;
     shb = nshb;
@@ -635,7 +682,7 @@ __device__ __forceinline__ void cell_rows(const CellArgs<S>& A, int64_t row, con
   }
 }
 
-template <typename S, int D1, int G, int CPL, int FREG, bool DO_R, int JAC, bool WB, bool C32 = false>
+template <typename S, int D1, int G, int CPL, int FREG, bool DO_R, int JAC, bool WB, bool C32 = false, bool PM = false>
 __global__ void __launch_bounds__(cell_threads<S, JAC>(),
                                   (JAC == kJacNone || G >= 16) ? 3 * 256 / cell_threads<S, JAC>() : 2 * 256 / cell_threads<S, JAC>())
     k_cell(const CellArgs<S> A) {
@@ -644,7 +691,7 @@ __global__ void __launch_bounds__(cell_threads<S, JAC>(),
   const int64_t row = (int64_t)blockIdx.x * GPB + threadIdx.x / G;
   const int64_t wrow0 = (int64_t)blockIdx.x * GPB + (threadIdx.x >> 5) * (32 / G);
   if (wrow0 >= A.n_u) return;
-  cell_rows<S, D1, G, CPL, FREG, DO_R, JAC, WB, C32, false>(A, row, wrow0, NG, A.n_u);
+  cell_rows<S, D1, G, CPL, FREG, DO_R, JAC, WB, C32, false, PM>(A, row, wrow0, NG, A.n_u);
 }
 
 // Offline: the cell-major copy of a P0-W tensor's rows (one thread per row).
@@ -675,6 +722,31 @@ __global__ void k_make_cells(int64_t n_u, const int64_t* __restrict__ row_fib, c
     }
 }
 
+// Offline: the packed row words (egfem_tensor::ck_m) from the cell-major copy, one thread per row.
+// mode 0: the largest K − (row's first K) into *maxd; mode 1: write the words.
+__global__ void k_make_words(int64_t n_u, const int64_t* __restrict__ row_nz, const uint32_t* __restrict__ ck_k,
+                             const uint16_t* __restrict__ ck_b, int D1, int fb, int ks, int mode,
+                             unsigned long long* maxd, uint64_t* ck_m, uint32_t* ck_kb) {
+  const int64_t i = (int64_t)blockIdx.x * blockDim.x + threadIdx.x;
+  if (i >= n_u) return;
+  const int64_t c0 = row_nz[i] / D1, c1 = row_nz[i + 1] / D1;
+  const uint32_t kb = c1 > c0 ? ck_k[c0] : 0u;
+  if (mode == 0) {
+    if (c1 > c0) atomicMax(maxd, (unsigned long long)(ck_k[c1 - 1] - kb));
+    return;
+  }
+  ck_kb[i] = kb;
+  const int fw = ks / D1;
+  for (int64_t c = c0; c < c1; ++c) {
+    uint64_t x = (uint64_t)(ck_k[c] - kb) << ks;
+    for (int m = 0; m < D1; ++m) {
+      const uint32_t b = ck_b[c * D1 + m];
+      x |= (uint64_t)((b & kCkFibMask) | ((b >> kCkPosShift) << fb)) << (m * fw);
+    }
+    ck_m[c] = x;
+  }
+}
+
 int g_sm_count[64] = {0};
 
 // Row-stream staging: TMA bulk copies of each warp's consecutive rows (WB) when a warp holds
@@ -693,19 +765,34 @@ bool cells_warp_bulk(int G, int vbytes) {
   return v == 2 ? (G <= 4 && vbytes == 4) : (v == 1);
 }
 
+// The packed 64-bit row words (PM kernels) when the tensor has them; EGFEM_CELLS_WORDS=0 keeps the
+// staged (K, fiber|pos) slices (A/B experiments; both give bitwise the same results).
+bool cells_packed_words() {
+  static int v = -1;
+  if (v < 0) v = getenv("EGFEM_CELLS_WORDS") ? (atoi(getenv("EGFEM_CELLS_WORDS")) != 0) : 1;
+  return v;
+}
+
 template <typename S, int D1, int G, int CPL, int FREG, bool DO_R, int JAC>
 egfem_status run_cells(const egfem_tensor* t, const CellArgs<S>& A, cudaStream_t s) {
   constexpr bool SU = cells_su<S, FREG, JAC>() && (DO_R || JAC == kJacNewtonP0 || JAC == kJacNewtonPK);
   using L = CellSmem<S, D1, G, CPL, JAC != kJacNone, SU ? G * FREG : 0>;
+  using LP = CellSmem<S, D1, G, CPL, JAC != kJacNone, SU ? G * FREG : 0, true>;
   const bool wb = cells_warp_bulk(G, (int)sizeof(S));
-  auto fn = wb ? k_cell<S, D1, G, CPL, FREG, DO_R, JAC, true> : k_cell<S, D1, G, CPL, FREG, DO_R, JAC, false>;
+  const bool pm = !wb && A.ck_m && cells_packed_words();
+  auto fn = wb ? k_cell<S, D1, G, CPL, FREG, DO_R, JAC, true>
+               : pm ? k_cell<S, D1, G, CPL, FREG, DO_R, JAC, false, false, true> : k_cell<S, D1, G, CPL, FREG, DO_R, JAC, false>;
   if constexpr ((JAC == kJacNewtonP0 || JAC == kJacNewtonPK) && D1 == 4 && sizeof(S) == 8) {
     if (A.chain32)
-      fn = wb ? k_cell<S, D1, G, CPL, FREG, DO_R, JAC, true, true> : k_cell<S, D1, G, CPL, FREG, DO_R, JAC, false, true>;
+      fn = wb ? k_cell<S, D1, G, CPL, FREG, DO_R, JAC, true, true>
+              : pm ? k_cell<S, D1, G, CPL, FREG, DO_R, JAC, false, true, true> : k_cell<S, D1, G, CPL, FREG, DO_R, JAC, false, true>;
   }
   constexpr int CT = cell_threads<S, JAC>();
-  const int smem = wb ? L::wbytes * (CT / 32) : L::bytes * (CT / G);
+  const int smem = wb ? L::wbytes * (CT / 32) : pm ? LP::bytes * (CT / G) : L::bytes * (CT / G);
   if (smem > 48 * 1024) EGFEM_CUDA_TRY(cudaFuncSetAttribute(fn, cudaFuncAttributeMaxDynamicSharedMemorySize, smem));
+  static int carve = -2;  // EGFEM_CELLS_CARVE=<percent>: preferred shared-memory carveout (experiments)
+  if (carve == -2) carve = getenv("EGFEM_CELLS_CARVE") ? atoi(getenv("EGFEM_CELLS_CARVE")) : -1;
+  if (carve >= 0) EGFEM_CUDA_TRY(cudaFuncSetAttribute(fn, cudaFuncAttributePreferredSharedMemoryCarveout, carve));
   const int dev = t->device & 63;
   if (!g_sm_count[dev])
     EGFEM_CUDA_TRY(cudaDeviceGetAttribute(&g_sm_count[dev], cudaDevAttrMultiProcessorCount, t->device));
@@ -771,6 +858,11 @@ egfem_status cells_dispatch(const egfem_tensor* t, bool do_r, int jac, bool pack
   A.ck_k = t->ck_k;
   A.ck_val = static_cast<const S*>(t->ck_val);
   A.ck_b = t->ck_b;
+  A.ck_m = t->ck_m;
+  A.ck_kb = t->ck_kb;
+  A.fb = t->ck_fb;
+  A.fw = t->ck_fb + t->ck_pb;
+  A.ks = t->ck_ks;
   A.u = static_cast<const S*>(u);
   A.w = static_cast<const S*>(w);
   A.chain = static_cast<const S*>(chain);
@@ -936,6 +1028,14 @@ bool cells_path_ok(const egfem_tensor* t, int jac) {
   return pick_cells(t, &c);
 }
 
+// how k_cell reads a row's per-cell data for this tensor (the variant run_cells picks)
+const char* cells_variant(const egfem_tensor* t) {
+  CellCfg c{};
+  if (!pick_cells(t, &c)) return "no configuration";
+  if (cells_warp_bulk(c.G, t->dtype == EGFEM_F64 ? 8 : 4)) return "warp TMA-staged slices";
+  return (t->ck_m && cells_packed_words()) ? "packed 64-bit row words" : "cp.async-staged slices";
+}
+
 egfem_status launch_cells(const egfem_tensor* t, bool do_r, int jac, bool packed, const void* u, const void* w,
                           const void* chain, void* r, void* csr_vals, cudaStream_t s) {
   if (t->n_u <= 0) return EGFEM_OK;
@@ -980,7 +1080,39 @@ egfem_status make_p0_cells(egfem_tensor* t) {
     t->ck_k = nullptr;
     t->ck_val = nullptr;
     t->ck_b = nullptr;
+    return EGFEM_OK;
   }
+  // packed row words: fiber and position fields as narrow as this tensor's rows allow, K as an
+  // offset from the row's first cell in the remaining bits (skipped when it does not fit)
+  auto bits = [](int n) {
+    int b = 1;
+    while ((1 << b) < n) ++b;
+    return b;
+  };
+  const int fb = bits(t->max_row_fib), pb = bits(t->max_row_nnz), ks = d1 * (fb + pb);
+  if (ks >= 64) return EGFEM_OK;
+  unsigned long long* dmax = nullptr;
+  EGFEM_CUDA_TRY(cudaMalloc(&dmax, sizeof(unsigned long long)));
+  EGFEM_CUDA_TRY(cudaMemset(dmax, 0, sizeof(unsigned long long)));
+  k_make_words<<<nb, 128>>>(t->n_u, t->row_nz, t->ck_k, t->ck_b, d1, fb, ks, 0, dmax, nullptr, nullptr);
+  count_launch();
+  unsigned long long hmax = 0;
+  ce = cudaMemcpy(&hmax, dmax, sizeof(hmax), cudaMemcpyDeviceToHost);
+  cudaFree(dmax);
+  EGFEM_CUDA_TRY(ce);
+  const bool fits = 64 - ks >= 32 || hmax < (1ull << (64 - ks));
+  if (getenv("EGFEM_DEBUG"))
+    fprintf(stderr, "[egfem] packed row words: fiber %d + position %d bits x %d, K offset max %llu in %d bits: %s\n", fb,
+            pb, d1, hmax, 64 - ks, fits ? "built" : "skipped");
+  if (!fits) return EGFEM_OK;
+  EGFEM_CUDA_TRY(dmalloc_padded((void**)&t->ck_m, 8 * (t->nnz / d1 + 1)));
+  EGFEM_CUDA_TRY(dmalloc_padded((void**)&t->ck_kb, 4 * (t->n_u + 1)));
+  k_make_words<<<nb, 128>>>(t->n_u, t->row_nz, t->ck_k, t->ck_b, d1, fb, ks, 1, nullptr, t->ck_m, t->ck_kb);
+  count_launch();
+  EGFEM_CUDA_TRY(cudaGetLastError());
+  t->ck_fb = fb;
+  t->ck_pb = pb;
+  t->ck_ks = ks;
   return EGFEM_OK;
 }
 

@@ -82,6 +82,12 @@ struct egfem_tensor {
   uint32_t* ck_k = nullptr;     // nnz/(d+1): K of each row cell
   void* ck_val = nullptr;       // nnz, dtype: T_{i v_m K}
   uint16_t* ck_b = nullptr;     // nnz: fiber index within the row | canonical position << 6
+  // the same per-cell data packed into one 64-bit word per row cell when it fits (make_p0_cells):
+  // bits [m·FW, m·FW + FB) fiber of nonzero m, [m·FW + FB, (m+1)·FW) its canonical position
+  // (FW = FB + PB), bits [ck_ks, 64) K − ck_kb[row]; the kernel reads it straight into registers
+  uint64_t* ck_m = nullptr;     // nnz/(d+1)
+  uint32_t* ck_kb = nullptr;    // n_u: K of each row's first cell (cells ascend: the minimum)
+  int ck_fb = 0, ck_pb = 0, ck_ks = 0;
   // W = V only (batched action): per row the dense |N|x|N| block over its CSR stencil N(i)
   int64_t* blk_off = nullptr;   // n_u+1: block offsets (row stride |N| rounded up to even)
   void* blk = nullptr;          // dtype: M_i[a][b] = T_{i, N_a, N_b}
@@ -141,6 +147,7 @@ egfem_status launch_rows(const egfem_tensor* t, bool do_r, int jac, egfem_interp
 bool rows_path_ok(const egfem_tensor* t, int jac);
 egfem_status make_wv_aux(egfem_tensor* t);
 bool cells_path_ok(const egfem_tensor* t, int jac);
+const char* cells_variant(const egfem_tensor* t);
 egfem_status launch_cells(const egfem_tensor* t, bool do_r, int jac, bool packed, const void* u, const void* w,
                           const void* chain, void* r, void* csr_vals, cudaStream_t s);
 egfem_status make_p0_cells(egfem_tensor* t);

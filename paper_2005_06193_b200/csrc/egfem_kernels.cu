@@ -786,7 +786,8 @@ std::string dispatch_name(const egfem_tensor* t, int entry, int jac) {
   static const char* force = getenv("EGFEM_PATH");
   const bool tile = force && force[0] == 't';
   const bool rows_only = force && force[0] == 'r';
-  if (!tile && !rows_only && cells_path_ok(t, jac)) return "k_cell (cell-major P0, egfem_cells.cu)";
+  if (!tile && !rows_only && cells_path_ok(t, jac))
+    return std::string("k_cell (cell-major P0, egfem_cells.cu; ") + cells_variant(t) + ")";
   if (!tile && !rows_only && dense1_path_ok(t, jac)) return "k_dense1 (dense single-vector W = V, egfem_dense.cu)";
   if (!tile && rows_path_ok(t, jac)) return "k_seg (row groups on the CSF, egfem_rows.cu)";
   return "k_tile (TMA row tiles, egfem_kernels.cu)";
@@ -841,6 +842,11 @@ egfem_status launch_tile_rows(const egfem_tensor* t, int64_t lo, int64_t hi, boo
   v.ck_k = t->ck_k;
   v.ck_val = t->ck_val;
   v.ck_b = t->ck_b;
+  v.ck_m = t->ck_m;
+  v.ck_kb = t->ck_kb ? t->ck_kb + lo : nullptr;
+  v.ck_fb = t->ck_fb;
+  v.ck_pb = t->ck_pb;
+  v.ck_ks = t->ck_ks;
   v.row_begin = t->row_begin + lo;
   v.col_begin = t->col_begin;
   void* rl = r ? (char*)r + (t->dtype == EGFEM_F64 ? 8 : 4) * lo : nullptr;

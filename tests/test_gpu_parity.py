@@ -537,7 +537,8 @@ def test_split_step_library_bitwise(eg, name, nranks):
         assert np.array_equal(J.cpu().numpy(), ref["J"][grp[wdw.row_begin]:grp[wdw.row_end]])
 
 
-@pytest.mark.parametrize("env", [{"EGFEM_PATH": "tile"}, {"EGFEM_PATH": "rows", "EGFEM_BATCHED": "csf"}])
+@pytest.mark.parametrize("env", [{"EGFEM_PATH": "tile"}, {"EGFEM_PATH": "rows", "EGFEM_BATCHED": "csf"},
+                                 {"EGFEM_CELLS_WORDS": "0"}])
 def test_kernel_paths(eg, env):
     """The non-default kernels (TMA tile kernel, canonical-CSF row kernel for P0 W, CSF batched
     kernel) match the oracle: they are the fallbacks for long rows / wide stencils."""
@@ -549,6 +550,29 @@ def test_kernel_paths(eg, env):
                          capture_output=True, text=True, timeout=600)
     assert res.returncode == 0, res.stdout + res.stderr
     assert "path ok" in res.stdout
+
+
+def test_packed_words_bitwise():
+    """The cell-major kernels reading the packed 64-bit row words (default) and the staged
+    (K, fiber|position) slices (EGFEM_CELLS_WORDS=0) compute the same sums in the same order:
+    apply, Picard, Newton and fused outputs are bitwise equal at full cfg3 / cfg4 size, fp64 and
+    fp32 (the staged kernels are oracle-checked)."""
+    import os
+    import subprocess
+    import sys
+    here = os.path.dirname(os.path.abspath(__file__))
+    out = []
+    for env in ({}, {"EGFEM_CELLS_WORDS": "0"}):
+        res = subprocess.run([sys.executable, os.path.join(here, "words_check.py")], env=dict(os.environ, **env),
+                             capture_output=True, text=True, timeout=900)
+        assert res.returncode == 0, res.stdout + res.stderr
+        out.append([ln.split() for ln in res.stdout.splitlines() if ln.startswith("hash")])
+    assert len(out[0]) == 4 and len(out[1]) == 4
+    for a, b in zip(*out):
+        assert a[1:3] == b[1:3] and a[-1] == b[-1], (a, b)
+    # the default run took the packed words on the 3D fp64 tensor (the headline), the other the slices
+    assert any("packed 64-bit row words" in " ".join(a) for a in out[0] if a[1] == "cfg4")
+    assert all("packed" not in " ".join(b) for b in out[1])
 
 
 @pytest.mark.parametrize("name", ["gfem2d", "biochem_p1"])
