@@ -195,7 +195,9 @@ egfem_status egfem_tensor_export(const egfem_tensor* t, int64_t* t_row_ptr, int3
  *                              exact because w depends on u through ∇u_h and Σ_m ∇λ_m = 0),
  *                              so the Newton kernel reads a cell's w and D_u w with one gather.  p > 1 required for GRADPOW_P0; p is k of RECIPROCAL (any value; p + u = 0
  * gives ±inf); p ignored otherwise.  At ∇u_h|_K = 0 and p < 4 the GRADPOW derivative is
- * taken as 0 (reading C11). */
+ * taken as 0 (reading C11).  For GRADPOW_P0 / MINSURF_P0 with chain, w may be NULL: w_k is
+ * then written only into the packed record chain[k*(d+1)] (one copy instead of two; the Newton
+ * calls below read it from there). */
 egfem_status egfem_interp(const egfem_tensor* t, egfem_interp_kind kind, double p, const void* u,
                           void* w, void* chain, egfem_stream_t stream);
 
@@ -224,7 +226,10 @@ egfem_status egfem_apply_batched(const egfem_tensor* t, int32_t batch, egfem_lay
  *   NEWTON cell-wise W  : J = T·w + (T·₂u)·D_u w, D_u w from `chain` (egfem_interp):
  *                         W = P0 or QUAD with GRADPOW_P0, MINSURF_P0, RECIPROCAL, (QUAD) SQUARE
  * u: [N_u] (NEWTON), w: [N_f], chain: [N_f*(d+1)] (P0-W NEWTON), csr_vals: [nnz_csr].
- * NEWTON with P1_TO_P2_SQUARE returns UNSUPPORTED. */
+ * NEWTON with P1_TO_P2_SQUARE returns UNSUPPORTED.  w may be NULL in a NEWTON call of a packed
+ * kind (GRADPOW_P0, MINSURF_P0, chain given) served by the cell-major kernels — they read w_K from
+ * the packed record (egfem_kernel_name reports k_cell); otherwise NULL w is INVALID_ARGUMENT.
+ * The same holds for egfem_apply_jacobian, egfem_apply_jacobian_rows and egfem_step. */
 egfem_status egfem_jacobian(const egfem_tensor* t, egfem_jac_mode mode, egfem_interp_kind kind, double p,
                             const void* u, const void* w, const void* chain, void* csr_vals,
                             egfem_stream_t stream);

@@ -305,7 +305,9 @@ static egfem_status interp_check(const egfem_tensor* t, egfem_interp_kind kind, 
   if (kind < EGFEM_INTERP_IDENTITY || kind > EGFEM_INTERP_RECIPROCAL)
     return fail(EGFEM_ERR_INVALID_ARGUMENT, "bad interp kind");
   egfem_status st;
-  if ((st = check_dev_ptr(t, u, "u", true)) || (st = check_dev_ptr(t, w, "w", true)) ||
+  // the packed kinds hold w_k in chain[k(d+1)] too: w may then be NULL (written once, in the record)
+  const bool w_opt = chain && packed_chain_kind(kind);
+  if ((st = check_dev_ptr(t, u, "u", true)) || (st = check_dev_ptr(t, w, "w", !w_opt)) ||
       (st = check_dev_ptr(t, chain, "chain", false)))
     return st;
   switch (kind) {
@@ -465,13 +467,23 @@ egfem_status egfem_group_compile(const int32_t* key, int32_t key_len, int32_t pa
   return st;
 }
 
+// w may be NULL in a Newton call of a packed kind (GRADPOW_P0, MINSURF_P0 with chain) that the
+// cell-major kernels serve: they read w_K from the packed record; any other call needs w.
+static egfem_status check_w_newton(const egfem_tensor* t, int code, egfem_interp_kind kind, const void* w,
+                                   const void* chain) {
+  if (w) return check_dev_ptr(t, w, "w", true);
+  if (code == 3 && chain && packed_chain_kind(kind) && cells_path_ok(t, code)) return EGFEM_OK;
+  return fail(EGFEM_ERR_INVALID_ARGUMENT, "w is NULL (allowed only for a packed-kind Newton call on the cell-major path)");
+}
+
 egfem_status egfem_jacobian(const egfem_tensor* t, egfem_jac_mode mode, egfem_interp_kind kind, double p,
                             const void* u, const void* w, const void* chain, void* csr_vals, egfem_stream_t stream) {
   if (!t) return fail(EGFEM_ERR_INVALID_ARGUMENT, "tensor is NULL");
   egfem_status st;
-  if ((st = check_dev_ptr(t, w, "w", true)) || (st = check_dev_ptr(t, csr_vals, "csr_vals", true))) return st;
+  if ((st = check_dev_ptr(t, csr_vals, "csr_vals", true))) return st;
   int code = 0;
   if ((st = jac_mode_code(t, mode, kind, p, u, chain, &code))) return st;
+  if ((st = check_w_newton(t, code, kind, w, chain))) return st;
   DeviceGuard g(t->device);
   return launch_tile(t, false, code, kind, p, u, w, chain, nullptr, csr_vals, (cudaStream_t)stream);
 }
@@ -481,11 +493,12 @@ egfem_status egfem_apply_jacobian(const egfem_tensor* t, egfem_jac_mode mode, eg
                                   egfem_stream_t stream) {
   if (!t) return fail(EGFEM_ERR_INVALID_ARGUMENT, "tensor is NULL");
   egfem_status st;
-  if ((st = check_dev_ptr(t, u, "u", true)) || (st = check_dev_ptr(t, w, "w", true)) ||
-      (st = check_dev_ptr(t, r, "r", true)) || (st = check_dev_ptr(t, csr_vals, "csr_vals", true)))
+  if ((st = check_dev_ptr(t, u, "u", true)) || (st = check_dev_ptr(t, r, "r", true)) ||
+      (st = check_dev_ptr(t, csr_vals, "csr_vals", true)))
     return st;
   int code = 0;
   if ((st = jac_mode_code(t, mode, kind, p, u, chain, &code))) return st;
+  if ((st = check_w_newton(t, code, kind, w, chain))) return st;
   DeviceGuard g(t->device);
   return launch_tile(t, true, code, kind, p, u, w, chain, r, csr_vals, (cudaStream_t)stream);
 }
@@ -497,6 +510,7 @@ egfem_status egfem_step(const egfem_tensor* t, egfem_interp_kind kind, double p,
   if ((st = check_dev_ptr(t, r, "r", true)) || (st = check_dev_ptr(t, csr_vals, "csr_vals", true))) return st;
   int code = 0;
   if ((st = jac_mode_code(t, EGFEM_JAC_NEWTON, kind, p, u, chain, &code))) return st;
+  if ((st = check_w_newton(t, code, kind, w, chain))) return st;
   DeviceGuard g(t->device);
   const cudaStream_t s = (cudaStream_t)stream;
   st = launch_step(t, kind, p, u, w, chain, r, csr_vals, s);
@@ -511,13 +525,14 @@ egfem_status egfem_apply_jacobian_rows(const egfem_tensor* t, egfem_jac_mode mod
                                        int64_t row_lo, int64_t row_hi, egfem_stream_t stream) {
   if (!t) return fail(EGFEM_ERR_INVALID_ARGUMENT, "tensor is NULL");
   egfem_status st;
-  if ((st = check_dev_ptr(t, u, "u", true)) || (st = check_dev_ptr(t, w, "w", true)) ||
-      (st = check_dev_ptr(t, r, "r", true)) || (st = check_dev_ptr(t, csr_vals, "csr_vals", true)))
+  if ((st = check_dev_ptr(t, u, "u", true)) || (st = check_dev_ptr(t, r, "r", true)) ||
+      (st = check_dev_ptr(t, csr_vals, "csr_vals", true)))
     return st;
   if (row_lo < 0 || row_hi < row_lo || row_hi > t->n_u)
     return fail(EGFEM_ERR_INVALID_ARGUMENT, "row range outside [0, n_u]");
   int code = 0;
   if ((st = jac_mode_code(t, mode, kind, p, u, chain, &code))) return st;
+  if ((st = check_w_newton(t, code, kind, w, chain))) return st;
   DeviceGuard g(t->device);
   return launch_tile_rows(t, row_lo, row_hi, true, code, kind, p, u, w, chain, r, csr_vals, (cudaStream_t)stream);
 }

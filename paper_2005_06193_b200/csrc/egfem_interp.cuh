@@ -163,7 +163,7 @@ __device__ __forceinline__ void gradpow_cell(const CellIn<S, D>& in, int64_t c, 
   if (IOTA) nw = 1;  // canonical P0 (the IOTA instance is only launched for it)
   for (int l = 0; l < nw; ++l) {
     const int64_t K = IOTA ? c : (int64_t)__ldg(wdofs + c * nw + l);
-    w[K] = (S)wk;
+    if (w) w[K] = (S)wk;  // NULL: w_K is kept in the packed record only (include/egfem.h egfem_interp)
     if (chain) {
       if constexpr (D == 3 && sizeof(S) == 8) {  // one 32-byte store (sm_100 256-bit STG) when aligned
         if ((reinterpret_cast<uintptr_t>(chain) & 31u) == 0) {

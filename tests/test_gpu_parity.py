@@ -767,3 +767,59 @@ def test_row_subranges_bitwise(eg, name, n):
         eg.egfem_apply_jacobian_rows(t, eg.JAC_NEWTON, pr.interp, pr.p, u, w, chain, r2, J2, lo, hi)
     torch.cuda.synchronize()
     assert torch.equal(r, r2) and torch.equal(J, J2)
+
+
+@pytest.mark.parametrize("name,f32", [("cfg4", False), ("cfg4", True), ("cfg3", False), ("minsurf3d", False),
+                                      ("plap3d_i2", False)])
+def test_w_null_packed_record(eg, name, f32):
+    """The gradient kinds keep w_K in the packed Newton record (include/egfem.h egfem_interp), so
+    w may be NULL: egfem_interp then writes the record only (identical to the call with w, whose
+    w equals the record's first entries), and the Newton calls on the cell-major path read w_K
+    from the record — r and J bitwise equal to the calls with w.
+    Calls that need the w array reject NULL before launching anything."""
+    import torch
+    pr = I.make_problem(name, n=I.SMALL_N[name])
+    t = eg.egfem_tensor_build(pr.mesh, pr.V, pr.W, pr.form, dtype=eg.F32 if f32 else eg.F64, device=0)
+    td = t.torch_dtype
+    d1 = pr.mesh.dim + 1
+    u = torch.tensor(pr.u, dtype=td, device="cuda")
+    w = torch.empty(t.n_f, dtype=td, device="cuda")
+    ch0, ch1 = (torch.full((t.n_f * d1,), float("nan"), dtype=td, device="cuda") for _ in range(2))
+    eg.egfem_interp(t, pr.interp, pr.p, u, w, ch0)
+    eg.egfem_interp(t, pr.interp, pr.p, u, None, ch1)
+    torch.cuda.synchronize()
+    assert torch.equal(ch0, ch1)
+    assert torch.equal(ch1.view(-1, d1)[:, 0], w)
+    outs = []
+    for wx, ch in ((w, ch0), (None, ch1)):
+        r = torch.full((t.n_u,), float("nan"), dtype=td, device="cuda")
+        J = torch.full((t.nnz_csr,), float("nan"), dtype=td, device="cuda")
+        J2 = torch.full((t.nnz_csr,), float("nan"), dtype=td, device="cuda")
+        r3 = torch.full((t.n_u,), float("nan"), dtype=td, device="cuda")
+        J3 = torch.full((t.nnz_csr,), float("nan"), dtype=td, device="cuda")
+        eg.egfem_apply_jacobian(t, eg.JAC_NEWTON, pr.interp, pr.p, u, wx, ch, r, J)
+        eg.egfem_jacobian(t, eg.JAC_NEWTON, pr.interp, pr.p, u, wx, ch, J2)
+        eg.egfem_step(t, pr.interp, pr.p, u, wx, ch, r3, J3)
+        torch.cuda.synchronize()
+        outs.append([x.cpu().numpy() for x in (r, J, J2, r3, J3)])
+    for a, b in zip(*outs):
+        assert np.array_equal(a, b)
+    assert np.array_equal(outs[0][1], outs[0][2]) and np.array_equal(outs[0][0], outs[0][3])
+    # row sub-ranges (the multi-GPU split step's calls) with w = NULL
+    h = t.n_u // 2
+    r = torch.full((t.n_u,), float("nan"), dtype=td, device="cuda")
+    J = torch.full((t.nnz_csr,), float("nan"), dtype=td, device="cuda")
+    eg.egfem_apply_jacobian_rows(t, eg.JAC_NEWTON, pr.interp, pr.p, u, None, ch1, r, J, 0, h)
+    eg.egfem_apply_jacobian_rows(t, eg.JAC_NEWTON, pr.interp, pr.p, u, None, ch1, r, J, h, t.n_u)
+    torch.cuda.synchronize()
+    assert np.array_equal(r.cpu().numpy(), outs[0][0]) and np.array_equal(J.cpu().numpy(), outs[0][1])
+    # w is required where it is read: apply alone, Picard, Newton without the record
+    r = torch.empty(t.n_u, dtype=td, device="cuda")
+    J = torch.empty(t.nnz_csr, dtype=td, device="cuda")
+    for call in (lambda: eg.egfem_apply(t, u, None, r),
+                 lambda: eg.egfem_jacobian(t, eg.JAC_PICARD, pr.interp, pr.p, None, None, None, J),
+                 lambda: eg.egfem_interp(t, pr.interp, pr.p, u, None, None),
+                 lambda: eg.egfem_apply_jacobian(t, eg.JAC_NEWTON, pr.interp, pr.p, u, None, None, r, J)):
+        with pytest.raises(eg.EgfemError) as ex:
+            call()
+        assert ex.value.status in (1, 3)  # INVALID_ARGUMENT, UNSUPPORTED
