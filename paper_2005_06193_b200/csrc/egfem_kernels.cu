@@ -719,7 +719,7 @@ egfem_status launch_interp(const egfem_tensor* t, egfem_interp_kind kind, double
     int per_sm = 0;                                                                                   \
     cudaOccupancyMaxActiveBlocksPerMultiprocessor(&per_sm, k_interp_gradpow<S, D, SA, IO, CF>, 128, 0); \
     const int g = (int)std::min<int64_t>(grid, (int64_t)std::max(per_sm, 1) * 148);                   \
-    S* wl = IO ? (S*)w + lo : (S*)w;                                                                  \
+    S* wl = (IO && w) ? (S*)w + lo : (S*)w; /* w may be NULL (packed kinds) */                        \
     S* cl2 = (IO && chain) ? (S*)chain + lo * (D + 1) : (S*)chain;                                    \
     k_interp_gradpow<S, D, SA, IO, CF><<<g, 128, 0, s>>>(D == 3 ? t->coords4 : t->coords, t->coordsf, cl, vd, \
                                                          wd, n, (const S*)u, wl, cl2, p,              \

@@ -44,4 +44,6 @@ res["picard"] = tm(lambda: eg.egfem_jacobian(t, eg.JAC_PICARD, pr.interp, pr.p, 
 res["newton"] = tm(lambda: eg.egfem_jacobian(t, eg.JAC_NEWTON, pr.interp, pr.p, u, w, chain, J))
 res["fused"] = tm(lambda: eg.egfem_apply_jacobian(t, eg.JAC_NEWTON, pr.interp, pr.p, u, w, chain, r, J))
 res["interp"] = tm(lambda: eg.egfem_interp(t, pr.interp, pr.p, u, w, chain))
+if gp:  # w kept in the packed record only (w = NULL), as the bench step runs it
+    res["interp_rec"] = tm(lambda: eg.egfem_interp(t, pr.interp, pr.p, u, None, chain))
 print(json.dumps(res), flush=True)
