@@ -936,7 +936,7 @@ __device__ __forceinline__ void st_release(uint32_t* p, uint32_t v) {
   asm volatile("st.release.gpu.global.u32 [%0], %1;" ::"l"(p), "r"(v) : "memory");
 }
 
-template <typename S, int D1, int G, int CPL, int FREG, bool C32, bool CF>
+template <typename S, int D1, int G, int CPL, int FREG, bool C32, bool CF, bool PM = false>
 __global__ void __launch_bounds__(cell_threads<S, kJacNewtonPK>(), 2 * 256 / cell_threads<S, kJacNewtonPK>())
     k_step(const CellArgs<S> A, const StepArgs<S> B) {
   constexpr int D = D1 - 1;
@@ -967,7 +967,7 @@ __global__ void __launch_bounds__(cell_threads<S, kJacNewtonPK>(), 2 * 256 / cel
       __syncwarp();
       const int64_t base = (int64_t)r * B.RI;
       const int64_t lim = min(base + (int64_t)B.RI, A.n_u);
-      cell_rows<S, D1, G, CPL, FREG, true, kJacNewtonPK, false, C32, true>(A, base + wl / G, base, WPG, lim);
+      cell_rows<S, D1, G, CPL, FREG, true, kJacNewtonPK, false, C32, true, PM>(A, base + wl / G, base, WPG, lim);
     }
   }
   __syncwarp();
@@ -1004,9 +1004,12 @@ __global__ void k_step_need(int64_t n_u, const int64_t* __restrict__ row_nz, con
 template <typename S, int D1, int G, int CPL, int FREG, bool C32>
 egfem_status run_step(const egfem_tensor* t, const CellArgs<S>& A, const StepArgs<S>& B, cudaStream_t s) {
   using L = CellSmem<S, D1, G, CPL, true, G * FREG>;
-  auto fn = B.coordsf ? k_step<S, D1, G, CPL, FREG, C32, true> : k_step<S, D1, G, CPL, FREG, C32, false>;
+  using LP = CellSmem<S, D1, G, CPL, true, G * FREG, true>;
+  const bool pm = A.ck_m && cells_packed_words();  // the row items read the packed row words too
+  auto fn = B.coordsf ? (pm ? k_step<S, D1, G, CPL, FREG, C32, true, true> : k_step<S, D1, G, CPL, FREG, C32, true>)
+                      : (pm ? k_step<S, D1, G, CPL, FREG, C32, false, true> : k_step<S, D1, G, CPL, FREG, C32, false>);
   constexpr int CT = cell_threads<S, kJacNewtonPK>();
-  const int smem = L::bytes * (CT / G);
+  const int smem = (pm ? LP::bytes : L::bytes) * (CT / G);
   if (smem > 48 * 1024) EGFEM_CUDA_TRY(cudaFuncSetAttribute(fn, cudaFuncAttributeMaxDynamicSharedMemorySize, smem));
   const int dev = t->device & 63;
   if (!g_sm_count[dev])
@@ -1239,6 +1242,11 @@ egfem_status step_dispatch(const egfem_tensor* t, egfem_interp_kind kind, double
   A.ck_k = t->ck_k;
   A.ck_val = static_cast<const S*>(t->ck_val);
   A.ck_b = t->ck_b;
+  A.ck_m = t->ck_m;
+  A.ck_kb = t->ck_kb;
+  A.fb = t->ck_fb;
+  A.fw = t->ck_fb + t->ck_pb;
+  A.ks = t->ck_ks;
   A.u = static_cast<const S*>(u);
   A.w = static_cast<const S*>(w);
   A.chain = static_cast<const S*>(chain);

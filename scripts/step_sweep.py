@@ -57,6 +57,7 @@ def main():
         chain = torch.empty(t.n_f * (pr.mesh.dim + 1), dtype=td, device="cuda")
         r = torch.empty(t.n_u, dtype=td, device="cuda")
         J = torch.empty(t.nnz_csr, dtype=td, device="cuda")
+        w = None  # the gradient kinds keep w_K in the packed record only, as bench.py runs the step
         if v == "two":
             def fn(s):
                 eg.egfem_interp(t, pr.interp, pr.p, u, w, chain, s)
