@@ -49,8 +49,17 @@ namespace egfem {
 // Kernel variants of a class: bit 0 = U and W are the same array (the u-slot values are the
 // W registers already loaded: no U loads), bit 1 = batch is a multiple of 32·P (no pair guards),
 // bit 2 = one pair per lane (batches below 64 or odd multiples of 32: a rank's shard of a
-// sharded batch) instead of the plan's P.
-constexpr int kVariants = 8;
+// sharded batch) instead of the plan's P, bit 3 = the symmetrized pattern (U == W only, below).
+//
+// Symmetrized pattern.  With U == W (the pairs (u, w = u) of the Burgers term (u·∇)u, PAPER.md
+// L396) the row action is a quadratic form, R_{i,p} = Σ_{j,k} T_ijk u_j u_k, so it equals
+//   R_{i,p} = Σ_j u_j Σ_{k ≥ j} S_ijk u_k,   S_ijk = T_ijk + T_ikj (k > j),  S_ijj = T_ijj,
+// which needs one FMA per (j ≤ k) pair instead of one per nonzero: cfg5's 26.1 M FMAs per pair
+// drop to ≈ 16 M.  The builder keeps, per class, the symmetrized pattern and S packed in its
+// FMA order (rounded once); the generated kernel is the same straight-line form.  The sums
+// run in a different order than the unsymmetrized kernel (graded by tolerance against the
+// oracle, like every kernel); EGFEM_GROUP_SYM=0 disables it.
+constexpr int kVariants = 16;
 
 struct GroupClass {
   int n = 0;       // group stencil width |N(leader)|
@@ -62,6 +71,9 @@ struct GroupClass {
   int32_t* rows = nullptr;  // ninst × g: member rows
   void* vals = nullptr;     // ninst × nv, dtype: T values in FMA program order
   std::vector<int32_t> key; // the pattern (Pattern::key), kept to generate variants on demand
+  std::vector<int32_t> skey;  // the symmetrized pattern (U == W), empty when disabled
+  int snv = 0;                // its value record stride
+  void* svals = nullptr;      // ninst × snv, dtype: S values in its FMA program order
   cudaKernel_t fn[kVariants] = {};
   int per_sm[kVariants] = {};     // resident CTAs per SM (registers), for the persistent grid
   size_t dyn_set[kVariants] = {};  // dynamic shared memory the kernel was opted in for
@@ -77,6 +89,7 @@ struct GroupPlan {
   int cap = 32;
   int carveout = -1;  // preferred shared-memory carveout in percent (-1: driver default)
   bool staged = false;    // full variants: W tiles by TMA bulk copies (kernel_source_staged; measured slower on cfg5)
+  bool sym = false;       // symmetrized classes built (the U == W launches take them)
   bool f64 = true;
   std::vector<GroupClass> classes;
   std::vector<cudaLibrary_t> libs;
@@ -599,6 +612,7 @@ void free_group_plan(GroupPlan* gp) {
     if (c.cols) cudaFree(c.cols);
     if (c.rows) cudaFree(c.rows);
     if (c.vals) cudaFree(c.vals);
+    if (c.svals) cudaFree(c.svals);
   }
   if (gp->fb_rows) cudaFree(gp->fb_rows);
   for (cudaLibrary_t l : gp->libs) cudaLibraryUnload(l);
@@ -723,6 +737,8 @@ egfem_status make_groups(egfem_tensor* t, const std::vector<int64_t>& hrf) {
   if (const char* e = getenv("EGFEM_GROUP_PERSIST")) gp->persistent = e[0] != '0';
   if (const char* e = getenv("EGFEM_GROUP_CAP")) gp->cap = std::max(1, atoi(e));
   if (const char* e = getenv("EGFEM_GROUP_CARVE")) gp->carveout = atoi(e);
+  gp->sym = true;
+  if (const char* e = getenv("EGFEM_GROUP_SYM")) gp->sym = e[0] != '0';
   gp->f64 = f64;
   for (size_t x = 0; x < chosen.size(); ++x) {
     GroupClass gc;
@@ -739,6 +755,7 @@ egfem_status make_groups(egfem_tensor* t, const std::vector<int64_t>& hrf) {
                 " groups]";
   }
   // per-class device arrays: columns, member rows, values in program order
+  int64_t fma_can = 0, fma_sym = 0;
   for (size_t x = 0; x < chosen.size(); ++x) {
     GroupClass& gc = gp->classes[x];
     const Pattern& pt = cls_pat[chosen[x]];
@@ -775,7 +792,90 @@ egfem_status make_groups(egfem_tensor* t, const std::vector<int64_t>& hrf) {
       return st;
     }
     gc.vals = dv;
+    if (!gp->sym) continue;
+    // the symmetrized pattern (U == W): per member the (a ≤ b) pairs of T's (a, b) ∪ (b, a) nonzeros
+    const int n = gc.n, g = gc.g;
+    Pattern sp;
+    sp.n = n;
+    for (int m = 0; m < g; ++m) {
+      std::vector<char> on((size_t)n * n, 0);
+      for (const auto& f : pt.members[m])
+        for (int b : f.second) on[(size_t)std::min(f.first, b) * n + std::max(f.first, b)] = 1;
+      std::vector<std::pair<int, std::vector<int>>> fibs;
+      for (int a = 0; a < n; ++a) {
+        std::vector<int> bs;
+        for (int b = a; b < n; ++b)
+          if (on[(size_t)a * n + b]) bs.push_back(b);
+        if (!bs.empty()) fibs.push_back({a, bs});
+      }
+      sp.members.push_back(fibs);
+    }
+    gc.skey = sp.key();
+    gc.snv = vals_stride(sp.nnz(), (int)vs);
+    auto fmas = [](const Pattern& x) {  // FMAs per pair and instance: one per nonzero, one per fiber
+      int c = x.nnz();
+      for (const auto& m : x.members) c += (int)m.size();
+      return (int64_t)c;
+    };
+    fma_can += gc.ninst * fmas(pt);
+    fma_sym += gc.ninst * fmas(sp);
+    std::vector<unsigned char> hs((size_t)gc.ninst * gc.snv * vs, 0);
+    std::vector<double> dense((size_t)g * n * n, 0.0);
+    std::vector<size_t> touched;
+    auto val = [&](size_t z) {
+      if (f64) {
+        double x;
+        std::memcpy(&x, &hv[z * vs], 8);
+        return x;
+      }
+      float x;
+      std::memcpy(&x, &hv[z * vs], 4);
+      return (double)x;
+    };
+    for (int64_t q = 0; q < gc.ninst; ++q) {
+      const auto& mem = members[inst[q]];
+      for (size_t z : touched) dense[z] = 0.0;
+      touched.clear();
+      for (int m = 0; m < g; ++m)
+        for (int fi = 0; fi < (int)pt.members[m].size(); ++fi) {
+          const int64_t f = hrf[mem[m]] + fi;
+          const int a = pt.members[m][fi].first;
+          const auto& bs = pt.members[m][fi].second;
+          for (uint32_t z = fnz[f]; z < fnz[f + 1]; ++z) {
+            const size_t at = ((size_t)m * n + a) * n + bs[z - fnz[f]];
+            dense[at] = val(z);
+            touched.push_back(at);
+          }
+        }
+      // S in the kernel's program order: a ascending, members in order, b ascending
+      int e = 0;
+      for (int a = 0; a < n; ++a)
+        for (int m = 0; m < g; ++m)
+          for (const auto& f : sp.members[m]) {
+            if (f.first != a) continue;
+            for (int b : f.second) {
+              const double x = a == b ? dense[((size_t)m * n + a) * n + a]
+                                      : dense[((size_t)m * n + a) * n + b] + dense[((size_t)m * n + b) * n + a];
+              unsigned char* dst = &hs[((size_t)q * gc.snv + e++) * vs];
+              if (f64) {
+                std::memcpy(dst, &x, 8);
+              } else {
+                const float xf = (float)x;
+                std::memcpy(dst, &xf, 4);
+              }
+            }
+          }
+    }
+    unsigned char* ds = nullptr;
+    if ((st = upload(&ds, hs))) {
+      free_group_plan(gp);
+      return st;
+    }
+    gc.svals = ds;
   }
+  if (gp->sym)
+    gp->info += " [U == W: symmetrized patterns, S_ijk = T_ijk + T_ikj for k > j: " + std::to_string(fma_sym) +
+                " instead of " + std::to_string(fma_can) + " FMAs per pair in the compiled classes]";
   // fallback rows (rare classes), grouped by stencil width, row order within a width
   std::vector<int32_t> fb;
   for (size_t c = 0; c < cls_pat.size(); ++c)
@@ -877,7 +977,7 @@ egfem_status ensure_variant(GroupPlan* gp, int v) {
   std::vector<egfem_status> sts(nc, EGFEM_OK);
   for (size_t c = 0; c < nc; ++c) {
     names[c] = "egfem_grp_" + std::to_string(c) + "_v" + std::to_string(v);
-    const Pattern pt = pattern_from_key(gp->classes[c].key);
+    const Pattern pt = pattern_from_key((v & 8) ? gp->classes[c].skey : gp->classes[c].key);
     const char* S = gp->f64 ? "double" : "float";
     srcs[c] = full && gp->staged ? kernel_source_staged(pt, names[c], S, P, same, gp->interleave)
                                  : kernel_source(pt, names[c], S, P, same, full, gp->interleave);
@@ -947,7 +1047,8 @@ egfem_status launch_groups(const egfem_tensor* t, int32_t batch, const void* U, 
   int P = gp->pairs_per_lane;
   if (P > 1 && batch < 32 * P) P = 1;
   const int nch = (batch + 32 * P - 1) / (32 * P);
-  const int v = (U == W ? 1 : 0) | (batch % (32 * P) == 0 ? 2 : 0) | (P == 1 && gp->pairs_per_lane != 1 ? 4 : 0);
+  const int v = (U == W ? 1 : 0) | (batch % (32 * P) == 0 ? 2 : 0) | (P == 1 && gp->pairs_per_lane != 1 ? 4 : 0) |
+                (U == W && gp->sym ? 8 : 0);
   egfem_status st = ensure_variant(gp, v);
   if (st) return st;
   const size_t nc = gp->classes.size();
@@ -997,7 +1098,8 @@ egfem_status launch_groups(const egfem_tensor* t, int32_t batch, const void* U, 
         std::max<int64_t>(1, std::min<int64_t>(runs, (int64_t)g_sms_grp[dev] * (gp->persistent ? gc.per_sm[v] : gp->cap)));
     long long ninst = gc.ninst;
     int B = batch, run = gp->run, pfl = pf;
-    void* args[] = {(void*)&gc.cols, (void*)&gc.rows, (void*)&gc.vals, &ninst, &B, &run, &pfl, (void*)&U, (void*)&W, &R};
+    void* vals = (v & 8) ? gc.svals : gc.vals;
+    void* args[] = {(void*)&gc.cols, (void*)&gc.rows, (void*)&vals, &ninst, &B, &run, &pfl, (void*)&U, (void*)&W, &R};
     const size_t dyn = staged ? (size_t)nw * gc.n * 32 * P * vsz0 : 0;
     if (!gc.carve_set[v]) {  // L1 over shared memory: consecutive instances of a run share stencil rows
       if (gp->carveout >= 0)

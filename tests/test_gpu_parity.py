@@ -649,7 +649,9 @@ def test_batched_groups_graph_and_shards(eg, orc, same):
     import torch
     pr = I.make_problem("cfg5", n=24, batch=96)
     t = eg.egfem_tensor_build(pr.mesh, pr.V, pr.W, pr.form, device=0)
-    assert "egfem_grp" in eg.egfem_kernel_name(t, 3)
+    name = eg.egfem_kernel_name(t, 3)
+    # U == W launches take the symmetrized patterns (R = Σ_{j≤k} S_ijk u_j u_k, egfem_group.cu)
+    assert "egfem_grp" in name and "symmetrized" in name
     o = orc.OracleTensor(pr.mesh, pr.V, pr.W, pr.form)
     U = torch.tensor(np.ascontiguousarray(pr.u.T), device="cuda")
     Wt = U if same else U * 0.5 + 0.25
