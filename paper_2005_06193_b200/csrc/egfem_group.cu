@@ -59,7 +59,10 @@ namespace egfem {
 // FMA order (rounded once); the generated kernel is the same straight-line form.  The sums
 // run in a different order than the unsymmetrized kernel (graded by tolerance against the
 // oracle, like every kernel); EGFEM_GROUP_SYM=0 disables it.
-constexpr int kVariants = 16;
+// Bit 4 = the symmetrized pattern at P = 4 pairs per lane (U == W, batch >= 128; P = 4 under a
+// 168-register cap measured best there: cfg5 0.49 ms at P = 2 / 120 registers, 0.433 at P = 2 /
+// 96, 0.428 at P = 4 / 168).
+constexpr int kVariants = 32;
 
 struct GroupClass {
   int n = 0;       // group stencil width |N(leader)|
@@ -90,6 +93,7 @@ struct GroupPlan {
   int carveout = -1;  // preferred shared-memory carveout in percent (-1: driver default)
   bool staged = false;    // full variants: W tiles by TMA bulk copies (kernel_source_staged; measured slower on cfg5)
   bool sym = false;       // symmetrized classes built (the U == W launches take them)
+  int sym_P = 4;          // their pairs per lane for batches >= 128 (EGFEM_GROUP_SYM_P: 2 keeps the plan's P)
   bool f64 = true;
   std::vector<GroupClass> classes;
   std::vector<cudaLibrary_t> libs;
@@ -210,7 +214,7 @@ void emit_body(std::string& o, const Pattern& pt, const char* S, int P, bool sam
 // by cp.async one instance ahead (double buffer), and the CTA's warps take its 32·P-pair chunks.
 // same: U == W (u_a is the register w_a); full: batch % (32·P) == 0 (no guards).
 std::string kernel_source(const Pattern& pt, const std::string& name, const char* S, int P, bool same, bool full,
-                          int IL) {
+                          int IL, int maxreg = -1) {
   const int n = pt.n, g = (int)pt.members.size();
   const int vs = std::strcmp(S, "double") == 0 ? 8 : 4;
   const int nv = vals_stride(pt.nnz(), vs), ncp = cols_stride(n);
@@ -226,7 +230,7 @@ std::string kernel_source(const Pattern& pt, const std::string& name, const char
   // (W and the member accumulators, P doubles each) is small; EGFEM_GROUP_MAXREG overrides
   // (0 = no cap).
   static const int env_reg = std::getenv("EGFEM_GROUP_MAXREG") ? std::atoi(std::getenv("EGFEM_GROUP_MAXREG")) : -1;
-  const int maxnreg = env_reg >= 0 ? env_reg : (2 * P * (n + g) <= 96 && P <= 2 ? 120 : 0);
+  const int maxnreg = env_reg >= 0 ? env_reg : maxreg >= 0 ? maxreg : (2 * P * (n + g) <= 96 && P <= 2 ? 120 : 0);
   if (maxnreg > 0)
     emit("extern \"C\" __global__ void __maxnreg__(%d) %s(const int* __restrict__ gcols, "
          "const int* __restrict__ grows, const %s* __restrict__ gvals, long long ninst, int B, int run, int pf, "
@@ -739,6 +743,7 @@ egfem_status make_groups(egfem_tensor* t, const std::vector<int64_t>& hrf) {
   if (const char* e = getenv("EGFEM_GROUP_CARVE")) gp->carveout = atoi(e);
   gp->sym = true;
   if (const char* e = getenv("EGFEM_GROUP_SYM")) gp->sym = e[0] != '0';
+  if (const char* e = getenv("EGFEM_GROUP_SYM_P")) gp->sym_P = atoi(e) == 4 ? 4 : 2;
   gp->f64 = f64;
   for (size_t x = 0; x < chosen.size(); ++x) {
     GroupClass gc;
@@ -971,7 +976,9 @@ egfem_status ensure_variant(GroupPlan* gp, int v) {
   for (const auto& gc : gp->classes) all &= gc.fn[v] != nullptr;
   if (all) return EGFEM_OK;
   const bool same = v & 1, full = (v >> 1) & 1;
-  const int P = (v & 4) ? 1 : gp->pairs_per_lane;
+  const int P = (v & 4) ? 1 : (v & 16) ? 4 : gp->pairs_per_lane;
+  // register caps of the symmetrized kernels (measured on cfg5, see kVariants)
+  const int maxreg = (v & 8) ? (P == 4 ? 168 : P == 2 ? 96 : -1) : -1;
   std::vector<std::string> names(nc), srcs(nc);
   std::vector<std::vector<char>> cubins(nc);
   std::vector<egfem_status> sts(nc, EGFEM_OK);
@@ -980,7 +987,7 @@ egfem_status ensure_variant(GroupPlan* gp, int v) {
     const Pattern pt = pattern_from_key((v & 8) ? gp->classes[c].skey : gp->classes[c].key);
     const char* S = gp->f64 ? "double" : "float";
     srcs[c] = full && gp->staged ? kernel_source_staged(pt, names[c], S, P, same, gp->interleave)
-                                 : kernel_source(pt, names[c], S, P, same, full, gp->interleave);
+                                 : kernel_source(pt, names[c], S, P, same, full, gp->interleave, maxreg);
   }
   std::vector<std::thread> th;
   std::atomic<size_t> next{0};
@@ -1044,11 +1051,14 @@ egfem_status launch_groups(const egfem_tensor* t, int32_t batch, const void* U, 
   // pairs per lane: the plan's P, or 1 for batches narrower than one 32·P chunk (e.g. a rank's
   // 32-pair shard of the 256 cfg5 pairs: 0.221 -> 0.172 ms); wider batches keep P (B = 96 at
   // P = 1 measured slower than B = 128 at P = 2)
+  const bool sym = U == W && gp->sym;
   int P = gp->pairs_per_lane;
-  if (P > 1 && batch < 32 * P) P = 1;
+  const bool p4 = sym && gp->sym_P == 4 && batch >= 128;
+  if (p4) P = 4;
+  else if (P > 1 && batch < 32 * P) P = 1;
   const int nch = (batch + 32 * P - 1) / (32 * P);
   const int v = (U == W ? 1 : 0) | (batch % (32 * P) == 0 ? 2 : 0) | (P == 1 && gp->pairs_per_lane != 1 ? 4 : 0) |
-                (U == W && gp->sym ? 8 : 0);
+                (sym ? 8 : 0) | (p4 ? 16 : 0);
   egfem_status st = ensure_variant(gp, v);
   if (st) return st;
   const size_t nc = gp->classes.size();
