@@ -209,7 +209,9 @@ egfem_status egfem_apply(const egfem_tensor* t, const void* u, const void* w, vo
 /* (2b) the same for `batch` independent (u, w) pairs reusing each T nonzero:
  * R_p = T:(U_p ⊗ W_p).  Layout NODE_MAJOR: U[j*batch+p], W[k*batch+p], R[i*batch+p];
  * PAIR_MAJOR: U[p*N_u+j], ... (batch >= 1).  U may alias W (pairs (u, w = u): the u-slot
- * values are then taken from the W registers).  W = V tensors with dense blocks run the
+ * values are then taken from the W registers, and the compiled row groups evaluate the quadratic
+ * form R_i = Σ_j u_j Σ_{k≥j} (T_ijk + T_ikj [k > j]) u_k from symmetrized patterns — the same sum
+ * regrouped, within rounding of the unaliased call; EGFEM_GROUP_SYM=0 keeps the plain patterns).  W = V tensors with dense blocks run the
  * compiled row-group kernels for NODE_MAJOR (egfem_group.cu): the kernel variant for
  * (U aliases W, batch % 128 == 0) is NVRTC-compiled on its first use (a one-time host cost
  * of ~1 s, cached process-wide), and the call forks its small pattern classes onto the
