@@ -352,7 +352,9 @@ def run_ours(args):
     torch.cuda.set_device(local)
     dev = torch.device("cuda", local)
     if world > 1:
-        dist.init_process_group("nccl", device_id=dev)
+        # a bounded collective timeout: a hung exchange aborts the ranks instead of the whole run
+        import datetime
+        dist.init_process_group("nccl", device_id=dev, timeout=datetime.timedelta(seconds=300))
     pr = I.make_problem(args.config, batch=args.batch)
     dtype = eg.F64 if args.dtype == "f64" else eg.F32
     td = torch.float64 if dtype == eg.F64 else torch.float32
