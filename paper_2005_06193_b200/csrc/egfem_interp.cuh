@@ -5,6 +5,10 @@
 #include <cuda_runtime.h>
 #include <stdint.h>
 
+#ifndef EGFEM_INTERP_LEAN
+#define EGFEM_INTERP_LEAN 1  // lean 3D gradient form (A/B switch; 0: ∇λ_a formed first)
+#endif
+
 namespace egfem {
 namespace ip {
 
@@ -89,6 +93,8 @@ __device__ __forceinline__ void gradpow_cell(const CellIn<S, D>& in, int64_t c, 
     g[1][1] = -e2x * inv;
     g[2][0] = -e1y * inv;
     g[2][1] = e1x * inv;
+  } else if constexpr (EGFEM_INTERP_LEAN) {
+    // (lean 3D form below, after the generic block)
   } else {
     double e[3][3];
 #pragma unroll
@@ -109,20 +115,42 @@ __device__ __forceinline__ void gradpow_cell(const CellIn<S, D>& in, int64_t c, 
       g[3][q] = c12[q] * inv;
     }
   }
-#pragma unroll
-  for (int q = 0; q < D; ++q) {
-    double s = 0.0;
-#pragma unroll
-    for (int a = 1; a <= D; ++a) s += g[a][q];
-    g[0][q] = -s;
-  }
   double gu[D];
+  // lean 3D: ∇λ_a = c_a / det (a = 1..3), Σ_a ∇λ_a = 0, so ∇u_h = (1/det) Σ_{a≥1} (u_a − u_0) c_a and
+  // the derivative record needs only gu·c_a
+  double cc[EGFEM_INTERP_LEAN && D == 3 ? 3 : 1][3], inv3 = 0.0;
+  if constexpr (EGFEM_INTERP_LEAN && D == 3) {
+    double e[3][3];
 #pragma unroll
-  for (int q = 0; q < D; ++q) {
-    double s = 0.0;
+    for (int a = 0; a < 3; ++a)
 #pragma unroll
-    for (int a = 0; a <= D; ++a) s += uv[a] * g[a][q];
-    gu[q] = s;
+      for (int q = 0; q < 3; ++q) e[a][q] = x[a + 1][q] - x[0][q];
+#pragma unroll
+    for (int q = 0; q < 3; ++q) {
+      const int q1 = (q + 1) % 3, q2 = (q + 2) % 3;
+      cc[0][q] = e[1][q1] * e[2][q2] - e[1][q2] * e[2][q1];
+      cc[1][q] = e[2][q1] * e[0][q2] - e[2][q2] * e[0][q1];
+      cc[2][q] = e[0][q1] * e[1][q2] - e[0][q2] * e[1][q1];
+    }
+    inv3 = 1.0 / (e[0][0] * cc[0][0] + e[0][1] * cc[0][1] + e[0][2] * cc[0][2]);
+    const double d1 = uv[1] - uv[0], d2 = uv[2] - uv[0], d3 = uv[3] - uv[0];
+#pragma unroll
+    for (int q = 0; q < 3; ++q) gu[q] = inv3 * (d1 * cc[0][q] + d2 * cc[1][q] + d3 * cc[2][q]);
+  } else {
+#pragma unroll
+    for (int q = 0; q < D; ++q) {
+      double s = 0.0;
+#pragma unroll
+      for (int a = 1; a <= D; ++a) s += g[a][q];
+      g[0][q] = -s;
+    }
+#pragma unroll
+    for (int q = 0; q < D; ++q) {
+      double s = 0.0;
+#pragma unroll
+      for (int a = 0; a <= D; ++a) s += uv[a] * g[a][q];
+      gu[q] = s;
+    }
   }
   double gg = 0.0;
 #pragma unroll
@@ -151,12 +179,22 @@ __device__ __forceinline__ void gradpow_cell(const CellIn<S, D>& in, int64_t c, 
   S dm[D + 1];
   if (chain) {
     dm[0] = (S)wk;
+    if constexpr (EGFEM_INTERP_LEAN && D == 3) {  // D_a = fac gu·∇λ_a, a = 1..3; D_0 = −(D_1 + D_2 + D_3)
+      const double f = fac * inv3;
+      double dv[3];
 #pragma unroll
-    for (int a = 0; a < D; ++a) {
-      double s = 0.0;
+      for (int a = 0; a < 3; ++a) dv[a] = f * (gu[0] * cc[a][0] + gu[1] * cc[a][1] + gu[2] * cc[a][2]);
+      dm[1] = (S)(-(dv[0] + dv[1] + dv[2]));
+      dm[2] = (S)dv[0];
+      dm[3] = (S)dv[1];
+    } else {
 #pragma unroll
-      for (int q = 0; q < D; ++q) s += gu[q] * g[a][q];
-      dm[a + 1] = (S)(fac * s);
+      for (int a = 0; a < D; ++a) {
+        double s = 0.0;
+#pragma unroll
+        for (int q = 0; q < D; ++q) s += gu[q] * g[a][q];
+        dm[a + 1] = (S)(fac * s);
+      }
     }
   }
   // the cell's W DOFs (P0: one; QUAD: N_q points, ∇u_h is constant on the cell)
