@@ -868,8 +868,9 @@ egfem_status egfem_partition(const egfem_tensor* G, int32_t nranks, int32_t rank
     if ((st = make_wv_aux(t))) return bail(st);
     if ((st = make_p0_cells(t))) return bail(st);
     if ((st = make_dense_blocks(t, lrf))) return bail(st);
-    // no compiled row groups on a partitioned handle: its columns are window indices, not rows
-    // (the batched action shards the batch, never the rows — DESIGN.md §8)
+    // compiled row groups of the local rows (their columns are window indices: make_groups maps a
+    // column to its local row by the window offset) — the row-partitioned batched action
+    if ((st = make_groups(t, lrf))) return bail(st);
   }
   if (row_begin) *row_begin = rb;
   if (row_end) *row_end = re;

@@ -655,13 +655,15 @@ egfem_status make_groups(egfem_tensor* t, const std::vector<int64_t>& hrf) {
     auto [b, nb] = sten(l);
     return std::includes(b, b + nb, a, a + na);
   };
-  // owner: the widest stencil containing N(i) (ties: lowest row); candidates lie in N(i)
+  // owner: the widest stencil containing N(i) (ties: lowest row); candidates lie in N(i).  A
+  // partitioned handle addresses columns in its window: column c is local row c − doff
+  const int64_t doff = t->row_begin - t->col_begin;
   std::vector<int32_t> owner(n_u);
   for (int64_t i = 0; i < n_u; ++i) {
     auto [a, na] = sten(i);
     int64_t best = i;
     for (int x = 0; x < na; ++x) {
-      const int64_t l = a[x];
+      const int64_t l = a[x] - doff;
       if (l == i || l < 0 || l >= n_u) continue;
       const int nl = (int)(hrf[l + 1] - hrf[l]);
       const int nbst = (int)(hrf[best + 1] - hrf[best]);

@@ -825,3 +825,30 @@ def test_w_null_packed_record(eg, name, f32):
         with pytest.raises(eg.EgfemError) as ex:
             call()
         assert ex.value.status in (1, 3)  # INVALID_ARGUMENT, UNSUPPORTED
+
+
+def test_batched_row_partition(eg, orc):
+    """The row-partitioned batched action (the SURVEY §8(e) alternative to batch sharding): each
+    rank's local tensor (its rows, window columns) builds its own compiled row groups and, on its
+    U window, reproduces its rows of the full action (rows are independent) within
+    FP64_TOL, aliased (symmetrized patterns) and not."""
+    import torch
+    pr = I.make_problem("cfg5", n=24, batch=64)
+    tg = eg.egfem_tensor_build(pr.mesh, pr.V, pr.W, pr.form, device=0)
+    o = orc.OracleTensor(pr.mesh, pr.V, pr.W, pr.form)
+    U = torch.tensor(np.ascontiguousarray(pr.u.T), device="cuda")
+    Wt = (0.5 * U - 0.125).contiguous()
+    ref_same = o.apply_batched(pr.u, pr.u).T
+    ref_diff = o.apply_batched(pr.u, Wt.cpu().numpy().T).T
+    for N in (2, 3):
+        for rank in range(N):
+            loc, win = eg.egfem_partition(tg, N, rank)
+            assert "egfem_grp" in eg.egfem_kernel_name(loc, 3)
+            rb, re_, cb, ce = win["row_begin"], win["row_end"], win["col_begin"], win["col_end"]
+            Ul = U[cb:ce].contiguous()
+            Wl = Wt[cb:ce].contiguous()
+            for Wx, ref in ((Ul, ref_same), (Wl, ref_diff)):
+                Rl = torch.empty((re_ - rb, 64), dtype=U.dtype, device="cuda")
+                eg.egfem_apply_batched(loc, 64, eg.LAYOUT_NODE_MAJOR, Ul, Wx, Rl)
+                torch.cuda.synchronize()
+                assert rel_l2(Rl.cpu().numpy(), ref[rb:re_]) <= FP64_TOL, (N, rank)
