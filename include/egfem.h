@@ -297,7 +297,10 @@ egfem_status egfem_bilinear_jacobian(const egfem_tensor* t, const void* b_vals, 
  * makes the referenced columns one range; a non-contiguous range is still
  * correct, only larger).  Local W (P0) covers cells [w_begin, w_end) referenced by
  * the owned rows.  Outputs (host scalars, any may be NULL): row_begin/row_end
- * (owned global rows), col_begin/col_end (local u window), w_begin/w_end. */
+ * (owned global rows), col_begin/col_end (local u window), w_begin/w_end.  The local tensor
+ * carries its own derived layouts (cell-major copy and packed row words, W = V transposes,
+ * dense blocks and compiled row groups), so egfem_apply_batched on it — U / W the node-major
+ * [col_begin, col_end) window, R its rows — is the row-partitioned batched action. */
 egfem_status egfem_partition(const egfem_tensor* global, int32_t nranks, int32_t rank, int device,
                              egfem_tensor** local, int64_t* row_begin, int64_t* row_end,
                              int64_t* col_begin, int64_t* col_end, int64_t* w_begin, int64_t* w_end);
