@@ -398,6 +398,11 @@ def run_ours(args):
     w_rec = (plan is None and chain is not None and pr.interp in (I.INTERP_GRADPOW_P0, I.INTERP_MINSURF_P0)
              and "k_cell" in eg.egfem_kernel_name(t, 2, eg.JAC_NEWTON, pr.interp, pr.p))
     ws = None if w_rec else w
+    # IDENTITY (W = V): w = u by definition, so the single-GPU step passes u as w — the interp is an
+    # in-place copy and the fused Newton runs the symmetrized blocks (k_dense1 JAC 3)
+    w_alias = plan is None and pr.interp == I.INTERP_IDENTITY and pr.W.family not in (I.P0, I.QUAD)
+    if w_alias:
+        ws = u
 
     if plan is not None:
         from paper_2005_06193_b200 import dist as edist
@@ -500,7 +505,7 @@ def run_ours(args):
     value = units / (ms * 1e-3)
     gpu_out = None
     if world == 1:  # the last timed step's outputs, for the parity check of the cpu_baseline leg
-        wv = chain.view(-1, pr.mesh.dim + 1)[:, 0] if w_rec else w  # w_K from the packed record
+        wv = chain.view(-1, pr.mesh.dim + 1)[:, 0] if w_rec else (u if w_alias else w)  # w_K from the packed record
         gpu_out = {"w": wv.double().cpu().numpy(), "r": r.double().cpu().numpy(), "J": J.double().cpu().numpy()}
 
     # separate apply / Jacobian launches (explanatory, outside the headline region)
@@ -526,7 +531,7 @@ def run_ours(args):
         t_interp = avg_ms(lambda: eg.egfem_interp(t, pr.interp, pr.p, u, w, chain, stream))
         t_fused = avg_ms(lambda: eg.egfem_apply_jacobian(t, eg.JAC_NEWTON, pr.interp, pr.p, u, w, chain, r, J,
                                                          stream))
-    if w_rec:  # the separate apply / Picard launches below read the w array: fill it once
+    if w_rec or w_alias:  # the separate apply / Picard launches below read the w array: fill it once
         eg.egfem_interp(t, pr.interp, pr.p, u, w, chain, stream)
     t_apply = avg_ms(lambda: eg.egfem_apply(t, u, w, r, stream))
     t_jac = avg_ms(lambda: eg.egfem_jacobian(t, eg.JAC_NEWTON, pr.interp, pr.p, u, w, chain, J, stream))
@@ -547,8 +552,9 @@ def run_ours(args):
         if plan is not None:
             edist.split_step(eg, t, plan, (ir0, ir1, iw0, iw1), pr.interp, pr.p, ux, w, chain, rx, Jx, stream)
             return
-        eg.egfem_interp(t, pr.interp, pr.p, ux, ws, chain, stream)
-        eg.egfem_apply_jacobian(t, eg.JAC_NEWTON, pr.interp, pr.p, ux, ws, chain, rx, Jx, stream)
+        wx = ux if w_alias else ws
+        eg.egfem_interp(t, pr.interp, pr.p, ux, wx, chain, stream)
+        eg.egfem_apply_jacobian(t, eg.JAC_NEWTON, pr.interp, pr.p, ux, wx, chain, rx, Jx, stream)
 
     def e2e_run(with_j):
         ev_in, ev_c, ev_out = ([torch.cuda.Event() for _ in range(K)] for _ in range(3))
@@ -633,9 +639,12 @@ def run_ours(args):
         "vs_baseline": None, "dtype": args.dtype, "data": "synthetic (seeded, BASELINE.json recipe)",
         "config": {"workload": workload, "description": pr.description, "nnz": nnz_total,
                    "nnz_csr": t.nnz_csr if world == 1 else None, "n_u": pr.n_u, "n_f": pr.n_f,
-                   "step": "interp(GRADPOW_P0 + D_u w) + fused apply/Newton-Jacobian" +
+                   "step": ("interp(%s%s) + fused apply/Newton-Jacobian" % (
+                       ["IDENTITY", "SQUARE", "GRADPOW_P0", "P1_TO_P2_SQUARE", "MINSURF_P0", "RECIPROCAL"][pr.interp],
+                       " + D_u w" if chain is not None else "")) +
                            (" + NCCL u-halo overlapped with the interior rows" if world > 1 else "") +
-                           ("; w_K kept in the packed Newton record only (w = NULL)" if w_rec else ""),
+                           ("; w_K kept in the packed Newton record only (w = NULL)" if w_rec else "") +
+                           ("; w = u (IDENTITY): fused Newton on the symmetrized blocks" if w_alias else ""),
                    "l2": (f"working set {ws_bytes / 1e9:.2f} GB < 4 x L2 ({l2_bytes >> 20} MB): 512 MB write "
                           "between timed steps, step time = sum of per-step intervals") if flush else
                          f"working set {ws_bytes / 1e9:.2f} GB >= 4 x L2 ({l2_bytes >> 20} MB); no flush",

@@ -931,7 +931,7 @@ egfem_status export_arrays(const egfem_tensor* t, int64_t* t_row_ptr, int32_t* t
 }
 
 void free_tensor(egfem_tensor* t) {
-  void* ptrs[] = {t->row_fib, t->row_nz, t->fib_j, t->fib_nz, t->nz_k, t->nz_val, t->nz_aux, t->nz_kpos, t->fib_kr, t->ck_k, t->ck_val, t->ck_b, t->ck_m, t->ck_kb, t->blk_off, t->blk, t->dense_rows,
+  void* ptrs[] = {t->row_fib, t->row_nz, t->fib_j, t->fib_nz, t->nz_k, t->nz_val, t->nz_aux, t->nz_kpos, t->fib_kr, t->ck_k, t->ck_val, t->ck_b, t->ck_m, t->ck_kb, t->blk_off, t->blk, t->blk_sym, t->dense_rows,
                   t->tile_row, t->tile_fib, t->tile_nz, t->coords, t->coords4, t->coordsf, t->cells, t->vdofs, t->wdofs, t->wcell, t->wpts};
   for (void* p : ptrs)
     if (p) cudaFree(p);

@@ -259,15 +259,20 @@ struct Dense1Args {
   int dmode;
   double pk;
   int64_t lo, hi;
+  const S* blks;  // JAC 3: the symmetrized blocks M + Mᵀ
 };
 
 __device__ __forceinline__ double dmul1(double a, double b) { return __dmul_rn(a, b); }
 __device__ __forceinline__ float dmul1(float a, float b) { return __fmul_rn(a, b); }
 
+// JAC 3: the IDENTITY Newton with u == w (the Burgers residual is the quadratic form
+// r_i = Σ_{j,k} T_ijk u_j u_k): J_ij = Σ_k T_ijk u_k + Σ_k T_ikj u_k = Σ_b (M + Mᵀ)[a][b] u_b is one
+// block-row product per stencil point (no reduce-scatter for T·₂u) and r_i = ½ Σ_a u_a J_ia.
 template <typename S, int G, bool DO_R, int JAC>
 __global__ void __launch_bounds__(256) k_dense1(const Dense1Args<S> A) {
   constexpr bool kN = JAC == 2;  // W = V Newton
-  constexpr bool kU = DO_R || kN;
+  constexpr bool kS = JAC == 3;  // W = V IDENTITY Newton, u == w, symmetrized blocks
+  constexpr bool kU = DO_R || kN || kS;
   constexpr unsigned FM = 0xffffffffu;
   constexpr int RPW = 32 / G;  // rows per warp
   const int lane = threadIdx.x % G;
@@ -302,7 +307,7 @@ __global__ void __launch_bounds__(256) k_dense1(const Dense1Args<S> A) {
     const int n = cur.n;
     const int64_t f0 = cur.f0;
     const int np = n + (n & 1);
-    const S* M = A.blk + cur.off;
+    const S* M = (kS ? A.blks : A.blk) + cur.off;
     const bool has = lane < n;
     const S wl = __ldg(A.w + jc);  // j = 0 for lanes past the stencil: a valid, unused value
     const S ul = kU ? __ldg(A.u + jc) : S(0);
@@ -346,7 +351,7 @@ __global__ void __launch_bounds__(256) k_dense1(const Dense1Args<S> A) {
       S acc = has ? dmul1(ul, X) : S(0);
 #pragma unroll
       for (int o = G / 2; o > 0; o >>= 1) acc = acc + __shfl_xor_sync(FM, acc, o, G);
-      if (live && lane == 0) A.r[row] = acc;
+      if (live && lane == 0) A.r[row] = kS ? dmul1(S(0.5), acc) : acc;
     }
     if constexpr (JAC != 0) {
       if (has) {
@@ -387,6 +392,7 @@ egfem_status run_dense1(const egfem_tensor* t, const Dense1Args<S>& A, cudaStrea
 template <typename S, int NMAX>
 egfem_status dense1_mode(const egfem_tensor* t, const Dense1Args<S>& A, bool do_r, int jac, cudaStream_t s) {
   if (do_r) {
+    if (jac == 3) return run_dense1<S, NMAX, true, 3>(t, A, s);
     if (jac == 0) return run_dense1<S, NMAX, true, 0>(t, A, s);
     if (jac == 1) return run_dense1<S, NMAX, true, 1>(t, A, s);
     return run_dense1<S, NMAX, true, 2>(t, A, s);
@@ -401,7 +407,12 @@ egfem_status dense1_dispatch(const egfem_tensor* t, int64_t lo, int64_t hi, bool
                              cudaStream_t s) {
   Dense1Args<S> A{t->row_fib, t->fib_j, t->blk_off, static_cast<const S*>(t->blk), static_cast<const S*>(u),
                   static_cast<const S*>(w), static_cast<S*>(r), static_cast<S*>(csr),
-                  kind == EGFEM_INTERP_SQUARE ? 1 : (kind == EGFEM_INTERP_RECIPROCAL ? 2 : 0), p, lo, hi};
+                  kind == EGFEM_INTERP_SQUARE ? 1 : (kind == EGFEM_INTERP_RECIPROCAL ? 2 : 0), p, lo, hi,
+                  static_cast<const S*>(t->blk_sym)};
+  // the fused IDENTITY Newton with u and w the same array: the symmetrized blocks (k_dense1 JAC 3)
+  static int sym_env = -1;
+  if (sym_env < 0) sym_env = getenv("EGFEM_DENSE_SYM") ? (atoi(getenv("EGFEM_DENSE_SYM")) != 0) : 1;
+  if (do_r && jac == 2 && kind == EGFEM_INTERP_IDENTITY && u == w && t->blk_sym && sym_env) jac = 3;
   const int dev = t->device & 63;
   if (!g_sms_dense1[dev])
     EGFEM_CUDA_TRY(cudaDeviceGetAttribute(&g_sms_dense1[dev], cudaDevAttrMultiProcessorCount, t->device));
@@ -438,6 +449,22 @@ __global__ void k_make_dense(int64_t n_u, const int64_t* __restrict__ row_fib, c
       }
       M[(f - f0) * np + lo] = nz_val[e];
     }
+}
+
+// Offline: M + Mᵀ of each row's block (W = V; the IDENTITY Newton of k_dense1 JAC 3).
+template <typename S>
+__global__ void k_make_dense_sym(int64_t n_u, const int64_t* __restrict__ row_fib, const int64_t* __restrict__ blk_off,
+                                 const S* __restrict__ blk, S* out) {
+  const int64_t i = (int64_t)blockIdx.x * blockDim.x + threadIdx.x;
+  if (i >= n_u) return;
+  const int n = (int)(row_fib[i + 1] - row_fib[i]);
+  const int np = n + (n & 1);
+  const S* M = blk + blk_off[i];
+  S* O = out + blk_off[i];
+  for (int a = 0; a < n; ++a) {
+    for (int b = 0; b < n; ++b) O[a * np + b] = M[a * np + b] + M[b * np + a];
+    if (np > n) O[a * np + n] = S(0);
+  }
 }
 
 int g_sms_dense[64] = {0};
@@ -596,6 +623,16 @@ egfem_status make_dense_blocks(egfem_tensor* t, const std::vector<int64_t>& hrf)
   }
   EGFEM_CUDA_TRY(cudaMalloc(&t->dense_rows, sizeof(int32_t) * t->n_u));
   EGFEM_CUDA_TRY(cudaMemcpy(t->dense_rows, order.data(), sizeof(int32_t) * t->n_u, cudaMemcpyHostToDevice));
+  // the symmetrized blocks for the single-vector IDENTITY Newton with u == w (stencils <= 16)
+  if (t->max_row_fib <= kDense1MaxN) {
+    EGFEM_CUDA_TRY(dmalloc_padded(&t->blk_sym, vs * std::max<int64_t>(off[t->n_u], 1)));
+    if (t->dtype == EGFEM_F64)
+      k_make_dense_sym<double><<<nb, 128>>>(t->n_u, t->row_fib, t->blk_off, (const double*)t->blk, (double*)t->blk_sym);
+    else
+      k_make_dense_sym<float><<<nb, 128>>>(t->n_u, t->row_fib, t->blk_off, (const float*)t->blk, (float*)t->blk_sym);
+    count_launch();
+    EGFEM_CUDA_TRY(cudaGetLastError());
+  }
   return EGFEM_OK;
 }
 

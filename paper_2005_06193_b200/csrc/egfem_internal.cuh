@@ -91,6 +91,7 @@ struct egfem_tensor {
   // W = V only (batched action): per row the dense |N|x|N| block over its CSR stencil N(i)
   int64_t* blk_off = nullptr;   // n_u+1: block offsets (row stride |N| rounded up to even)
   void* blk = nullptr;          // dtype: M_i[a][b] = T_{i, N_a, N_b}
+  void* blk_sym = nullptr;      // dtype: (M_i + M_iᵀ)[a][b] (the IDENTITY Newton with u == w, k_dense1)
   int32_t* dense_rows = nullptr;  // n_u: rows grouped by stencil width |N(i)| (row order within a width)
   std::vector<std::array<int64_t, 4>> dense_classes;  // host: (width, first entry in dense_rows, count, first block value)
   egfem::GroupPlan* grp = nullptr;  // W = V batched action: row groups with compiled-in patterns (egfem_group.cu)

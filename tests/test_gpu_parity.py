@@ -852,3 +852,29 @@ def test_batched_row_partition(eg, orc):
                 eg.egfem_apply_batched(loc, 64, eg.LAYOUT_NODE_MAJOR, Ul, Wx, Rl)
                 torch.cuda.synchronize()
                 assert rel_l2(Rl.cpu().numpy(), ref[rb:re_]) <= FP64_TOL, (N, rank)
+
+
+@pytest.mark.parametrize("name,f32", [("cfg1", False), ("cfg2", False), ("cfg2", True)])
+def test_identity_newton_symmetric_blocks(eg, orc, name, f32):
+    """The fused IDENTITY Newton with u and w the same array runs the symmetrized dense blocks:
+    J_ij = Σ_b (M + Mᵀ)[a][b] u_b (= T·w + T·₂u at w = u) and r_i = ½ Σ_a u_a J_ia
+    (= Σ_jk T_ijk u_j u_k, L183) — the same values as the call with a separate w, within the
+    tolerance against the oracle."""
+    import torch
+    pr = I.make_problem(name, n=I.SMALL_N[name])
+    t = eg.egfem_tensor_build(pr.mesh, pr.V, pr.W, pr.form, dtype=eg.F32 if f32 else eg.F64, device=0)
+    o = orc.OracleTensor(pr.mesh, pr.V, pr.W, pr.form)
+    ref = oracle_pass(o, pr, pr.u)
+    td = t.torch_dtype
+    u = torch.tensor(pr.u, dtype=td, device="cuda")
+    w = u.clone()
+    tol = FP32_TOL if f32 else FP64_TOL
+    outs = []
+    for wx in (u, w):  # aliased: symmetrized blocks; separate: the plain blocks + reduce-scatter
+        r = torch.empty(t.n_u, dtype=td, device="cuda")
+        J = torch.empty(t.nnz_csr, dtype=td, device="cuda")
+        eg.egfem_apply_jacobian(t, eg.JAC_NEWTON, eg.INTERP_IDENTITY, 0.0, u, wx, None, r, J)
+        torch.cuda.synchronize()
+        outs.append((r.double().cpu().numpy(), J.double().cpu().numpy()))
+        assert rel_l2(outs[-1][0], ref["r"]) <= tol and rel_l2(outs[-1][1], ref["J"]) <= tol
+    assert rel_l2(outs[0][0], outs[1][0]) <= tol and rel_l2(outs[0][1], outs[1][1]) <= tol
