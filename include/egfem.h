@@ -22,6 +22,9 @@
  *   - u, w, r, chain, csr_vals, U, W, R are caller-owned DEVICE pointers on the
  *     handle's device, of the handle's dtype, 16-byte aligned, contiguous.
  *     Lengths are implied by egfem_tensor_info (N_u, N_f, nnz_csr).
+ *     Each handle remembers the last 16 device pointers that passed the device check
+ *     (cudaPointerGetAttributes); a remembered pointer is not queried again, so a
+ *     buffer freed with cudaFree after use on a handle must not be passed to it again.
  *   - Compute calls are asynchronous on the given cudaStream_t (0 = legacy default).
  *     Kernel faults surface at the next call or at the caller's stream sync.
  *   - The handle is immutable after build (its only lazily created state — the compiled

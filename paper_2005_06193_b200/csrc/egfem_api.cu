@@ -42,14 +42,22 @@ bool aligned16(const void* p) { return (reinterpret_cast<uintptr_t>(p) & 15u) ==
 egfem_status check_dev_ptr(const egfem_tensor* t, const void* p, const char* name, bool required) {
   if (!p) return required ? fail(EGFEM_ERR_INVALID_ARGUMENT, std::string(name) + " is NULL") : EGFEM_OK;
   if (!aligned16(p)) return fail(EGFEM_ERR_INVALID_ARGUMENT, std::string(name) + " is not 16-byte aligned");
+  const uintptr_t key = reinterpret_cast<uintptr_t>(p);
+  {
+    std::lock_guard<std::mutex> lk(t->ptr_mu);
+    for (uintptr_t q : t->ptr_ok)
+      if (q == key) return EGFEM_OK;
+  }
   cudaPointerAttributes a;
   if (cudaPointerGetAttributes(&a, p) != cudaSuccess) {
     cudaGetLastError();
     return fail(EGFEM_ERR_INVALID_ARGUMENT, std::string(name) + " is not a CUDA pointer");
   }
-  if (a.type == cudaMemoryTypeManaged) return EGFEM_OK;
-  if (a.type != cudaMemoryTypeDevice || a.device != t->device)
+  if (a.type != cudaMemoryTypeManaged && (a.type != cudaMemoryTypeDevice || a.device != t->device))
     return fail(EGFEM_ERR_INVALID_ARGUMENT, std::string(name) + " is not device memory on the handle's device");
+  std::lock_guard<std::mutex> lk(t->ptr_mu);
+  t->ptr_ok[t->ptr_ok_next] = key;
+  t->ptr_ok_next = (t->ptr_ok_next + 1) % 16;
   return EGFEM_OK;
 }
 

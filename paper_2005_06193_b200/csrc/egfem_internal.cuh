@@ -18,6 +18,7 @@
 #include <stdint.h>
 
 #include <array>
+#include <mutex>
 #include <string>
 #include <vector>
 
@@ -118,6 +119,12 @@ struct egfem_tensor {
   int64_t row_begin = 0, col_begin = 0;
   // local tensors: rows / interp items that read only owned u (egfem_interior); -1 = all
   int64_t int_row_lo = -1, int_row_hi = -1, int_w_lo = -1, int_w_hi = -1;
+
+  // caller pointers already validated on this handle (check_dev_ptr): a hit skips the driver's
+  // cudaPointerGetAttributes, so a step's repeated calls on the same buffers cost no driver query
+  mutable std::mutex ptr_mu;
+  mutable uintptr_t ptr_ok[16] = {};
+  mutable int ptr_ok_next = 0;
 };
 
 namespace egfem {

@@ -395,6 +395,20 @@ def test_validation_errors(eg):
     with pytest.raises(eg.EgfemError) as e:
         eg.egfem_apply(t, u[1:], w, r)  # misaligned
     assert e.value.status == 1
+    # the C ABI itself (no binding checks): device pointers validated once are remembered per
+    # handle, host pointers are still rejected after many accepted calls
+    import ctypes
+    L = eg.lib()
+    pu, pw, pr_ = (ctypes.c_void_p(x.data_ptr()) for x in (u, w, r))
+    for _ in range(40):
+        assert L.egfem_apply(t.h, pu, pw, pr_, None) == 0
+    hw = torch.zeros(t.n_f, dtype=torch.float64).pin_memory()
+    for _ in range(3):
+        assert L.egfem_apply(t.h, pu, ctypes.c_void_p(hw.data_ptr()), pr_, None) == 1
+    r2 = torch.full_like(r, 7.0)
+    assert L.egfem_apply(t.h, pu, pw, ctypes.c_void_p(r2.data_ptr()), None) == 0
+    torch.cuda.synchronize()
+    assert torch.equal(r2, r)
     bad = I.Mesh(2, pr.mesh.coords, pr.mesh.cells.copy())
     bad.cells[3, 1] = 10 ** 6
     with pytest.raises(eg.EgfemError) as e:
