@@ -395,7 +395,7 @@ def run_ours(args):
     # the gradient kinds keep w_K in the packed Newton record (include/egfem.h egfem_interp): on the
     # cell-major path the single-GPU step writes that one copy and the fused kernel reads w_K from
     # it, so the step passes w = NULL (a separate w array is a second copy nothing in the step reads)
-    w_rec = (plan is None and chain is not None and pr.interp in (I.INTERP_GRADPOW_P0, I.INTERP_MINSURF_P0)
+    w_rec = (chain is not None and pr.interp in (I.INTERP_GRADPOW_P0, I.INTERP_MINSURF_P0)
              and "k_cell" in eg.egfem_kernel_name(t, 2, eg.JAC_NEWTON, pr.interp, pr.p))
     ws = None if w_rec else w
     # IDENTITY (W = V): w = u by definition, so the single-GPU step passes u as w — the interp is an
@@ -412,7 +412,7 @@ def run_ours(args):
     def dist_step(ux, rx, e=None):
         """N>1: post the u-halo exchange, run the interior phase, wait for the halo (the
         compute stream waits on the communicator's), run the boundary phase."""
-        edist.split_step(eg, t, plan, (ir0, ir1, iw0, iw1), pr.interp, pr.p, ux, w, chain, rx, J, stream, e)
+        edist.split_step(eg, t, plan, (ir0, ir1, iw0, iw1), pr.interp, pr.p, ux, ws, chain, rx, J, stream, e)
 
     K, Wm = args.steps, args.warmup
     ev = [[torch.cuda.Event(enable_timing=True) for _ in range(4)] for _ in range(K)]
@@ -528,8 +528,8 @@ def run_ours(args):
         dist_ms = {"interp": (float(np.median(ti)), float(np.min(ti))),
                    "apply_jacobian_fused": (float(np.median(tf)), float(np.min(tf)))}
     else:  # N>1 splits them into phases: whole-range launches, outside the timed region
-        t_interp = avg_ms(lambda: eg.egfem_interp(t, pr.interp, pr.p, u, w, chain, stream))
-        t_fused = avg_ms(lambda: eg.egfem_apply_jacobian(t, eg.JAC_NEWTON, pr.interp, pr.p, u, w, chain, r, J,
+        t_interp = avg_ms(lambda: eg.egfem_interp(t, pr.interp, pr.p, u, ws, chain, stream))
+        t_fused = avg_ms(lambda: eg.egfem_apply_jacobian(t, eg.JAC_NEWTON, pr.interp, pr.p, u, ws, chain, r, J,
                                                          stream))
     if w_rec or w_alias:  # the separate apply / Picard launches below read the w array: fill it once
         eg.egfem_interp(t, pr.interp, pr.p, u, w, chain, stream)
@@ -550,7 +550,7 @@ def run_ours(args):
 
     def step_on(ux, rx, Jx):
         if plan is not None:
-            edist.split_step(eg, t, plan, (ir0, ir1, iw0, iw1), pr.interp, pr.p, ux, w, chain, rx, Jx, stream)
+            edist.split_step(eg, t, plan, (ir0, ir1, iw0, iw1), pr.interp, pr.p, ux, ws, chain, rx, Jx, stream)
             return
         wx = ux if w_alias else ws
         eg.egfem_interp(t, pr.interp, pr.p, ux, wx, chain, stream)

@@ -524,10 +524,12 @@ def test_overlap_split_reads_no_halo(eg, name, nranks):
     assert eg.egfem_interior(t) == (0, t.n_u, 0, n_items)
 
 
-@pytest.mark.parametrize("name,nranks", [("cfg4", 3), ("cfg2", 2), ("biochem_p0", 2)])
-def test_split_step_library_bitwise(eg, name, nranks):
+@pytest.mark.parametrize("name,nranks,w_null", [("cfg4", 3, False), ("cfg4", 3, True), ("cfg2", 2, False),
+                                                ("biochem_p0", 2, False)])
+def test_split_step_library_bitwise(eg, name, nranks, w_null):
     """dist.split_step — the N>1 bench step through the library — on each rank's local tensor
-    with its window already filled (a plan without exchanges) reproduces the single-GPU r and J."""
+    with its window already filled (a plan without exchanges) reproduces the single-GPU r and J.
+    w_null: the bench's N > 1 step for the packed gradient kinds (w_K only in the Newton record)."""
     import torch
 
     from paper_2005_06193_b200 import dist as edist
@@ -545,6 +547,9 @@ def test_split_step_library_bitwise(eg, name, nranks):
             if pr.W.family in (I.P0, I.QUAD) and pr.interp != I.INTERP_IDENTITY else None
         r = torch.empty(loc.n_u, dtype=torch.float64, device="cuda")
         J = torch.empty(loc.nnz_csr, dtype=torch.float64, device="cuda")
+        if w_null:
+            assert "k_cell" in eg.egfem_kernel_name(loc, 2, eg.JAC_NEWTON, pr.interp, pr.p)
+            wl = None
         edist.split_step(eg, loc, plan, eg.egfem_interior(loc), pr.interp, pr.p, ul, wl, chain, r, J)
         torch.cuda.synchronize()
         assert np.array_equal(r.cpu().numpy(), ref["r"][wdw.row_begin:wdw.row_end])
