@@ -357,7 +357,8 @@ egfem_status egfem_halo_unpack(const egfem_tensor* local, const int32_t* d_idx, 
 
 /* Name of the kernel family `entry` dispatches to for this handle (0 = egfem_apply,
  * 1 = egfem_jacobian, 2 = egfem_apply_jacobian with (mode, kind, p), 3 = egfem_apply_batched
- * NODE_MAJOR, 4 = egfem_step with (kind, p), a 32-byte aligned chain assumed), written
+ * NODE_MAJOR, 4 = egfem_step with (kind, p), a 32-byte aligned chain assumed, 5 = egfem_interp
+ * with kind: "k_interp_gradpow_geo" when the handle holds geometry classes), written
  * NUL-terminated into the host buffer buf[len] (truncated if short).
  * Used by bench.py to name the kernel its roofline line measures.  No launch.
  * INVALID_ARGUMENT on NULL t/buf, len = 0 or a bad entry; the Jacobian checks of

@@ -384,7 +384,7 @@ def egfem_halo_unpack(t: Tensor, idx, recv_buf, u_local, stream=None):
 
 def egfem_kernel_name(t: Tensor, entry, mode=JAC_NEWTON, kind=INTERP_IDENTITY, p=0.0) -> str:
     """Kernel family an entry point runs for this handle (0 apply, 1 jacobian, 2 apply_jacobian,
-    3 apply_batched node-major, 4 step); bench.py names its roofline kernel with it."""
+    3 apply_batched node-major, 4 step, 5 interp); bench.py names its roofline kernel with it."""
     buf = ctypes.create_string_buffer(2048)
     _check("egfem_kernel_name", _lib.egfem_kernel_name(t.h, int(entry), mode, kind, float(p), buf, 2048))
     return buf.value.decode()

@@ -455,9 +455,17 @@ egfem_status egfem_kernel_name(const egfem_tensor* t, int32_t entry, egfem_jac_m
   if (entry == 1 || entry == 2)
     if ((st = jac_mode_code(t, mode, kind, p, nullptr, nullptr, &code, false))) return st;
   if (entry == 4 && (st = jac_mode_code(t, EGFEM_JAC_NEWTON, kind, p, nullptr, nullptr, &code, false))) return st;
-  if (entry < 0 || entry > 4) return fail(EGFEM_ERR_INVALID_ARGUMENT, "entry must be 0..4");
+  if (entry < 0 || entry > 5) return fail(EGFEM_ERR_INVALID_ARGUMENT, "entry must be 0..5");
   std::string name;
-  if (entry == 4)  // egfem_step (a 32-byte aligned chain assumed)
+  if (entry == 5) {  // egfem_interp with kind
+    const bool grad = kind == EGFEM_INTERP_GRADPOW_P0 || kind == EGFEM_INTERP_MINSURF_P0;
+    if (grad && geo_interp_ok(t))
+      name = "k_interp_gradpow_geo (" + std::to_string(t->n_geo) + " geometry classes, egfem_kernels.cu)";
+    else if (grad)
+      name = "k_interp_gradpow (egfem_kernels.cu)";
+    else
+      name = "k_interp_* (egfem_kernels.cu)";
+  } else if (entry == 4)  // egfem_step (a 32-byte aligned chain assumed)
     name = step_path_ok(t, kind, nullptr) ? "k_step (single-pass interp + apply + Newton Jacobian, egfem_cells.cu)"
                                           : "k_interp_* + " + dispatch_name(t, 2, code);
   else

@@ -14,9 +14,12 @@
 
 #include <algorithm>
 #include <cmath>
+#include <cstdlib>
+#include <cstring>
 #include <vector>
 
 #include "egfem_internal.cuh"
+#include "egfem_interp.cuh"
 
 namespace egfem {
 namespace {
@@ -169,6 +172,20 @@ __global__ void k_element_triples(const ElemParams P) {
       }
     }
   }
+}
+
+// (cc, inv3) of each geometry class from its edge vectors, by the interp's own cof3 (bitwise the
+// per-cell evaluation): e is 9 x nk (class-major), gtab 10 x nk (value-major)
+__global__ void k_geo_table(const double* e, int nk, double* gtab) {
+  const int k = blockIdx.x * blockDim.x + threadIdx.x;
+  if (k >= nk) return;
+  double ee[3][3], cc[3][3], inv3;
+  for (int a = 0; a < 3; ++a)
+    for (int q = 0; q < 3; ++q) ee[a][q] = e[k * 9 + a * 3 + q];
+  ip::cof3(ee, cc, inv3);
+  for (int a = 0; a < 3; ++a)
+    for (int q = 0; q < 3; ++q) gtab[(a * 3 + q) * nk + k] = cc[a][q];
+  gtab[9 * nk + k] = inv3;
 }
 
 __global__ void k_iota(uint32_t* a, int64_t n) {
@@ -490,6 +507,56 @@ egfem_status upload_mesh(egfem_tensor* t, const egfem_mesh* mesh, const egfem_sp
     count_launch();
     EGFEM_CUDA_TRY(cudaGetLastError());
   }
+  return make_geo_classes(t, mesh);
+}
+
+// Geometry classes for the 3D interp of the gradient kinds (canonical P1 V / P0 W): a cell's
+// interp reads only u at its vertices and the (cc, inv3) of its class when every cell's edge
+// vectors x_{a+1} − x_0 (exact double differences, as the kernel forms them) are bitwise one of at
+// most kMaxGeoClasses tuples — meshes made of translated copies of a few cells (the structured
+// meshes of the paper's experiments).  Otherwise (or EGFEM_GEOM_CLASSES=0) no table: the
+// interp gathers the coordinates.
+egfem_status make_geo_classes(egfem_tensor* t, const egfem_mesh* mesh) {
+  if (t->dim != 3 || t->dtype != EGFEM_F32 || !t->vdofs_is_cells || !t->wdofs_is_iota || !t->w_p0 || t->nwc != 1)
+    return EGFEM_OK;  // (fp32 only: the interp kernel that reads the table, egfem_kernels.cu)
+  const char* env = std::getenv("EGFEM_GEOM_CLASSES");
+  if (env && env[0] == '0') return EGFEM_OK;
+  const int64_t nc = mesh->n_cells;
+  std::vector<double> reps;  // 9 per class
+  std::vector<uint8_t> cls((size_t)nc);
+  int last = 0;
+  for (int64_t c = 0; c < nc; ++c) {
+    const int32_t* v = mesh->cells + c * 4;
+    double e[9];
+    for (int a = 0; a < 3; ++a)
+      for (int q = 0; q < 3; ++q) e[a * 3 + q] = mesh->coords[(int64_t)v[a + 1] * 3 + q] - mesh->coords[(int64_t)v[0] * 3 + q];
+    const int nk = (int)(reps.size() / 9);
+    int k = -1;
+    for (int i = 0; i < nk && k < 0; ++i) {
+      const int cand = (last + i) % nk;  // the previous cell's class first
+      if (std::memcmp(e, &reps[(size_t)cand * 9], sizeof(e)) == 0) k = cand;
+    }
+    if (k < 0) {
+      if (nk == kMaxGeoClasses) return EGFEM_OK;  // not a few-class mesh: the gathering interp
+      reps.insert(reps.end(), e, e + 9);
+      k = nk;
+    }
+    cls[(size_t)c] = (uint8_t)k;
+    last = k;
+  }
+  const int nk = (int)(reps.size() / 9);
+  double* de = nullptr;
+  EGFEM_CUDA_TRY(cudaMalloc(&de, sizeof(double) * reps.size()));
+  EGFEM_CUDA_TRY(cudaMemcpy(de, reps.data(), sizeof(double) * reps.size(), cudaMemcpyHostToDevice));
+  EGFEM_CUDA_TRY(cudaMalloc(&t->gtab, sizeof(double) * 10 * nk));
+  k_geo_table<<<1, 64>>>(de, nk, t->gtab);
+  count_launch();
+  EGFEM_CUDA_TRY(cudaGetLastError());
+  EGFEM_CUDA_TRY(cudaDeviceSynchronize());
+  cudaFree(de);
+  EGFEM_CUDA_TRY(cudaMalloc(&t->gcls, std::max<int64_t>(nc, 16)));
+  EGFEM_CUDA_TRY(cudaMemcpy(t->gcls, cls.data(), nc, cudaMemcpyHostToDevice));
+  t->n_geo = nk;
   return EGFEM_OK;
 }
 
@@ -932,7 +999,7 @@ egfem_status export_arrays(const egfem_tensor* t, int64_t* t_row_ptr, int32_t* t
 
 void free_tensor(egfem_tensor* t) {
   void* ptrs[] = {t->row_fib, t->row_nz, t->fib_j, t->fib_nz, t->nz_k, t->nz_val, t->nz_aux, t->nz_kpos, t->fib_kr, t->ck_k, t->ck_val, t->ck_b, t->ck_m, t->ck_kb, t->blk_off, t->blk, t->blk_sym, t->dense_rows,
-                  t->tile_row, t->tile_fib, t->tile_nz, t->coords, t->coords4, t->coordsf, t->cells, t->vdofs, t->wdofs, t->wcell, t->wpts};
+                  t->tile_row, t->tile_fib, t->tile_nz, t->coords, t->coords4, t->coordsf, t->cells, t->vdofs, t->wdofs, t->wcell, t->wpts, t->gcls, t->gtab};
   for (void* p : ptrs)
     if (p) cudaFree(p);
   free_group_plan(t->grp);

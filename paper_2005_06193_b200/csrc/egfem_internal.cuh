@@ -37,6 +37,7 @@ constexpr uint32_t kKMask = (1u << kKShift) - 1u;   // k of a P0-W tensor
 constexpr uint32_t kKMaskAny = 0x7FFFFFFFu;          // k of any other tensor
 constexpr uint32_t kHead = 0x80000000u;              // bit 31: first nonzero of a fiber
 constexpr int kMaxQuad = 16;
+constexpr int kMaxGeoClasses = 32;  // geometry classes of the 3D interp (egfem_tensor::gcls)
 constexpr int kRowsMaxNnz = 512;   // rows up to this length take the row-group path (k_seg)
 // cell-major copy: ck_b packs the fiber index within the row (6 bits) and the canonical position
 // within the row (10 bits)
@@ -114,6 +115,11 @@ struct egfem_tensor {
   int32_t* vdofs = nullptr;     // n_cells*nV  V dof ids (u indices)
   int32_t* wdofs = nullptr;     // n_cells*nW  W dof ids
   int32_t* wcell = nullptr;     // n_f: cell owning P0 dof k (P0 W only)
+  // geometry classes (3D, canonical P1 V / P0 W, at most kMaxGeoClasses): cells whose edge vectors
+  // x_{a+1} − x_0 are bitwise equal share one entry (egfem_build.cu make_geo_classes)
+  uint8_t* gcls = nullptr;      // n_cells: class of each cell
+  double* gtab = nullptr;       // 10 x n_geo: cc[a][q] (v = 3a + q) and 1/det (v = 9) of each class
+  int n_geo = 0;
 
   // partition bookkeeping (global handles: 0 / identity)
   int64_t row_begin = 0, col_begin = 0;
@@ -132,6 +138,11 @@ namespace egfem {
 // builder / export (egfem_build.cu)
 egfem_status build_from_triples(egfem_tensor* t, int64_t m, uint64_t* d_key_ij, uint32_t* d_k, double* d_val);
 egfem_status upload_mesh(egfem_tensor* t, const egfem_mesh* mesh, const egfem_space* V, const egfem_space* W);
+egfem_status make_geo_classes(egfem_tensor* t, const egfem_mesh* mesh);
+// the interp of the gradient kinds reads geometry classes (fp32 handles with a class table)
+inline bool geo_interp_ok(const egfem_tensor* t) {
+  return t->dim == 3 && t->dtype == EGFEM_F32 && t->gcls && t->vdofs_is_cells && t->wdofs_is_iota && t->nwc == 1;
+}
 egfem_status emit_element_triples(egfem_tensor* t, egfem_form form, const egfem_quad* quad, int64_t* m_out,
                                   uint64_t** key, uint32_t** k, double** val);
 egfem_status export_arrays(const egfem_tensor* t, int64_t* t_row_ptr, int32_t* t_j, int32_t* t_k, void* t_val,

@@ -75,10 +75,27 @@ __device__ __forceinline__ void gather_cell(const double* __restrict__ coords, c
   }
 }
 
-template <typename S, int D, bool IOTA>
+// 3D cell geometry from the edge vectors e_a = x_{a+1} − x_0: the cofactor vectors c_a (∇λ_{a+1} =
+// c_a / det) and 1/det, with every rounding explicit — the geometry-class table (kernel k_geo_table)
+// evaluates the same function on a class's edge vectors and must match the per-cell path bit for bit
+__device__ __forceinline__ void cof3(const double (&e)[3][3], double (&cc)[3][3], double& inv3) {
+#pragma unroll
+  for (int q = 0; q < 3; ++q) {
+    const int q1 = (q + 1) % 3, q2 = (q + 2) % 3;
+    cc[0][q] = __fma_rn(e[1][q1], e[2][q2], -__dmul_rn(e[1][q2], e[2][q1]));
+    cc[1][q] = __fma_rn(e[2][q1], e[0][q2], -__dmul_rn(e[2][q2], e[0][q1]));
+    cc[2][q] = __fma_rn(e[0][q1], e[1][q2], -__dmul_rn(e[0][q2], e[1][q1]));
+  }
+  inv3 = 1.0 / __fma_rn(e[0][2], cc[0][2], __fma_rn(e[0][1], cc[0][1], __dmul_rn(e[0][0], cc[0][0])));
+}
+
+// GEO: the cell's geometry (cc, inv3 as 10 values, `geo[a * 3 + q]`, `geo[9]`) comes from its
+// geometry class instead of its vertex coordinates (3D lean form only; in.x is not read)
+template <typename S, int D, bool IOTA, bool GEO = false>
 __device__ __forceinline__ void gradpow_cell(const CellIn<S, D>& in, int64_t c, const int32_t* __restrict__ wdofs,
                                              S* __restrict__ w, S* __restrict__ chain, double p, bool minsurf,
-                                             int nw) {
+                                             int nw, const double* geo = nullptr) {
+  static_assert(!GEO || (D == 3 && EGFEM_INTERP_LEAN), "geometry classes: 3D lean form");
   const auto& x = in.x;
   const auto& uv = in.uv;
   // barycentric gradients of vertices 1..D from the edge vectors e_a = x_a − x_0
@@ -120,22 +137,24 @@ __device__ __forceinline__ void gradpow_cell(const CellIn<S, D>& in, int64_t c, 
   // the derivative record needs only gu·c_a
   double cc[EGFEM_INTERP_LEAN && D == 3 ? 3 : 1][3], inv3 = 0.0;
   if constexpr (EGFEM_INTERP_LEAN && D == 3) {
-    double e[3][3];
+    if constexpr (GEO) {
 #pragma unroll
-    for (int a = 0; a < 3; ++a)
+      for (int a = 0; a < 3; ++a)
 #pragma unroll
-      for (int q = 0; q < 3; ++q) e[a][q] = x[a + 1][q] - x[0][q];
+        for (int q = 0; q < 3; ++q) cc[a][q] = geo[a * 3 + q];
+      inv3 = geo[9];
+    } else {
+      double e[3][3];
 #pragma unroll
-    for (int q = 0; q < 3; ++q) {
-      const int q1 = (q + 1) % 3, q2 = (q + 2) % 3;
-      cc[0][q] = e[1][q1] * e[2][q2] - e[1][q2] * e[2][q1];
-      cc[1][q] = e[2][q1] * e[0][q2] - e[2][q2] * e[0][q1];
-      cc[2][q] = e[0][q1] * e[1][q2] - e[0][q2] * e[1][q1];
+      for (int a = 0; a < 3; ++a)
+#pragma unroll
+        for (int q = 0; q < 3; ++q) e[a][q] = x[a + 1][q] - x[0][q];
+      cof3(e, cc, inv3);
     }
-    inv3 = 1.0 / (e[0][0] * cc[0][0] + e[0][1] * cc[0][1] + e[0][2] * cc[0][2]);
     const double d1 = uv[1] - uv[0], d2 = uv[2] - uv[0], d3 = uv[3] - uv[0];
 #pragma unroll
-    for (int q = 0; q < 3; ++q) gu[q] = inv3 * (d1 * cc[0][q] + d2 * cc[1][q] + d3 * cc[2][q]);
+    for (int q = 0; q < 3; ++q)
+      gu[q] = __dmul_rn(inv3, __fma_rn(d3, cc[2][q], __fma_rn(d2, cc[1][q], __dmul_rn(d1, cc[0][q]))));
   } else {
 #pragma unroll
     for (int q = 0; q < D; ++q) {
@@ -154,7 +173,7 @@ __device__ __forceinline__ void gradpow_cell(const CellIn<S, D>& in, int64_t c, 
   }
   double gg = 0.0;
 #pragma unroll
-  for (int q = 0; q < D; ++q) gg += gu[q] * gu[q];
+  for (int q = 0; q < D; ++q) gg = __fma_rn(gu[q], gu[q], gg);
   double wk, fac;
   if (minsurf) {  // a = (1 + ‖g‖²)^{−1/2}, ∂a/∂u_m = −(1 + ‖g‖²)^{−3/2} g·∇λ_m
     wk = 1.0 / sqrt(1.0 + gg);
@@ -183,7 +202,8 @@ __device__ __forceinline__ void gradpow_cell(const CellIn<S, D>& in, int64_t c, 
       const double f = fac * inv3;
       double dv[3];
 #pragma unroll
-      for (int a = 0; a < 3; ++a) dv[a] = f * (gu[0] * cc[a][0] + gu[1] * cc[a][1] + gu[2] * cc[a][2]);
+      for (int a = 0; a < 3; ++a)
+        dv[a] = __dmul_rn(f, __fma_rn(gu[2], cc[a][2], __fma_rn(gu[1], cc[a][1], __dmul_rn(gu[0], cc[a][0]))));
       dm[1] = (S)(-(dv[0] + dv[1] + dv[2]));
       dm[2] = (S)dv[0];
       dm[3] = (S)dv[1];
@@ -248,6 +268,43 @@ __device__ __forceinline__ void interp_cells(const double* __restrict__ coords, 
     idx(c + 2 * stride, cv2, dv2);                                    // record two cells ahead
     gradpow_cell<S, D, IOTA>(cur, c, wdofs, w, chain, p, minsurf, nw);
     cur = nxt;
+  }
+}
+
+// Geometry classes (3D, canonical P1 V / P0 W): cells whose edge vectors are bitwise equal share
+// one (cc, inv3) entry of the class table `sg` (shared memory, entry k at sg[v * nk + k], v < 10),
+// so a cell needs its class byte and u at its vertices only — no coordinate gathers and no
+// cofactor arithmetic (SG: the table staged in shared memory, else read through L1 from global).
+// Same pipeline as interp_cells: the cell record two cells ahead, the u
+// gathers and the class byte one cell ahead.
+template <typename S, bool SG>
+__device__ __forceinline__ void interp_cells_geo(const uint8_t* __restrict__ gcls, const double* sg, int nk,
+                                                 const int32_t* __restrict__ cells, int64_t c, int64_t cend,
+                                                 int64_t stride, const S* __restrict__ u, S* __restrict__ w,
+                                                 S* __restrict__ chain, double p, bool minsurf) {
+  if (c >= cend) return;
+  auto idx = [&](int64_t cc) { return load_cidx<3>(cells, cc < cend ? cc : c); };
+  auto gather = [&](const CellIdx<3>& cv, int64_t cc, CellIn<S, 3>& in, int& k) {
+#pragma unroll
+    for (int a = 0; a <= 3; ++a) in.uv[a] = (double)__ldg(u + cv.v[a]);
+    k = __ldg(gcls + (cc < cend ? cc : c));
+  };
+  CellIdx<3> cv2 = idx(c);
+  CellIn<S, 3> cur;
+  int kc;
+  gather(cv2, c, cur, kc);
+  cv2 = idx(c + stride);
+  for (; c < cend; c += stride) {
+    CellIn<S, 3> nxt;
+    int kn;
+    gather(cv2, c + stride, nxt, kn);
+    cv2 = idx(c + 2 * stride);
+    double geo[10];
+#pragma unroll
+    for (int v = 0; v < 10; ++v) geo[v] = SG ? sg[v * nk + kc] : __ldg(sg + v * nk + kc);
+    gradpow_cell<S, 3, true, true>(cur, c, nullptr, w, chain, p, minsurf, 1, geo);
+    cur = nxt;
+    kc = kn;
   }
 }
 
