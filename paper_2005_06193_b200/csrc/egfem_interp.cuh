@@ -5,6 +5,9 @@
 #include <cuda_runtime.h>
 #include <stdint.h>
 
+#ifndef EGFEM_INTERP_EF
+#define EGFEM_INTERP_EF 0  // A/B: 1 = cell records loaded and Newton records stored L2 evict-first, 2 = stores only
+#endif
 #ifndef EGFEM_INTERP_LEAN
 #define EGFEM_INTERP_LEAN 1  // lean 3D gradient form (A/B switch; 0: ∇λ_a formed first)
 #endif
@@ -24,7 +27,18 @@ struct CellIdx {
 template <int D>
 __device__ __forceinline__ CellIdx<D> load_cidx(const int32_t* __restrict__ t, int64_t c) {
   CellIdx<D> r;
-  if constexpr (D == 3) {
+  if constexpr (D == 3 && EGFEM_INTERP_EF == 1) {
+    uint64_t pol;
+    asm("createpolicy.fractional.L2::evict_first.b64 %0, 1.0;" : "=l"(pol));
+    int4 q;
+    asm("ld.global.nc.L1::no_allocate.L2::cache_hint.v4.s32 {%0, %1, %2, %3}, [%4], %5;"
+        : "=r"(q.x), "=r"(q.y), "=r"(q.z), "=r"(q.w)
+        : "l"(reinterpret_cast<const int4*>(t) + c), "l"(pol));
+    r.v[0] = q.x;
+    r.v[1] = q.y;
+    r.v[2] = q.z;
+    r.v[3] = q.w;
+  } else if constexpr (D == 3) {
     const int4 q = __ldg(reinterpret_cast<const int4*>(t) + c);
     r.v[0] = q.x;
     r.v[1] = q.y;
@@ -225,9 +239,14 @@ __device__ __forceinline__ void gradpow_cell(const CellIn<S, D>& in, int64_t c, 
     if (chain) {
       if constexpr (D == 3 && sizeof(S) == 8) {  // one 32-byte store (sm_100 256-bit STG) when aligned
         if ((reinterpret_cast<uintptr_t>(chain) & 31u) == 0) {
-          asm volatile("st.global.v4.f64 [%0], {%1, %2, %3, %4};" ::"l"(chain + K * 4), "d"(dm[0]), "d"(dm[1]),
-                       "d"(dm[2]), "d"(dm[3])
-                       : "memory");
+          if constexpr (EGFEM_INTERP_EF != 0)
+            asm volatile("st.global.cs.v4.f64 [%0], {%1, %2, %3, %4};" ::"l"(chain + K * 4), "d"(dm[0]),
+                         "d"(dm[1]), "d"(dm[2]), "d"(dm[3])
+                         : "memory");
+          else
+            asm volatile("st.global.v4.f64 [%0], {%1, %2, %3, %4};" ::"l"(chain + K * 4), "d"(dm[0]), "d"(dm[1]),
+                         "d"(dm[2]), "d"(dm[3])
+                         : "memory");
         } else {  // the API's 16-byte alignment
           reinterpret_cast<double2*>(chain + K * 4)[0] = make_double2(dm[0], dm[1]);
           reinterpret_cast<double2*>(chain + K * 4)[1] = make_double2(dm[2], dm[3]);
