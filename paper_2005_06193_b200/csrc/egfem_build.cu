@@ -517,8 +517,7 @@ egfem_status upload_mesh(egfem_tensor* t, const egfem_mesh* mesh, const egfem_sp
 // meshes of the paper's experiments).  Otherwise (or EGFEM_GEOM_CLASSES=0) no table: the
 // interp gathers the coordinates.
 egfem_status make_geo_classes(egfem_tensor* t, const egfem_mesh* mesh) {
-  if (t->dim != 3 || t->dtype != EGFEM_F32 || !t->vdofs_is_cells || !t->wdofs_is_iota || !t->w_p0 || t->nwc != 1)
-    return EGFEM_OK;  // (fp32 only: the interp kernel that reads the table, egfem_kernels.cu)
+  if (t->dim != 3 || !t->vdofs_is_cells || !t->wdofs_is_iota || !t->w_p0 || t->nwc != 1) return EGFEM_OK;
   const char* env = std::getenv("EGFEM_GEOM_CLASSES");
   if (env && env[0] == '0') return EGFEM_OK;
   const int64_t nc = mesh->n_cells;

@@ -139,9 +139,9 @@ namespace egfem {
 egfem_status build_from_triples(egfem_tensor* t, int64_t m, uint64_t* d_key_ij, uint32_t* d_k, double* d_val);
 egfem_status upload_mesh(egfem_tensor* t, const egfem_mesh* mesh, const egfem_space* V, const egfem_space* W);
 egfem_status make_geo_classes(egfem_tensor* t, const egfem_mesh* mesh);
-// the interp of the gradient kinds reads geometry classes (fp32 handles with a class table)
+// the interp of the gradient kinds reads geometry classes (handles with a class table)
 inline bool geo_interp_ok(const egfem_tensor* t) {
-  return t->dim == 3 && t->dtype == EGFEM_F32 && t->gcls && t->vdofs_is_cells && t->wdofs_is_iota && t->nwc == 1;
+  return t->dim == 3 && t->gcls && t->vdofs_is_cells && t->wdofs_is_iota && t->nwc == 1;
 }
 egfem_status emit_element_triples(egfem_tensor* t, egfem_form form, const egfem_quad* quad, int64_t* m_out,
                                   uint64_t** key, uint32_t** k, double** val);

@@ -57,23 +57,39 @@ __global__ void __launch_bounds__(128) k_interp_gradpow(const double* __restrict
 
 // Geometry-class variant (3D, canonical P1 V / P0 W; egfem_interp.cuh interp_cells_geo): the class
 // table (cc, inv3 of each class, 10 x nk values, entry-major by value) is staged once per CTA.
-// Dispatched for fp32 only: there the interp is FP64-bound (its geometry is fp64) and the class
-// table removes the cofactor arithmetic — cfg4 0.127 -> 0.097 ms; the fp64 interp measured 0.137 ->
-// 0.142 ms with it (table in shared memory or read through L1 alike), so fp64 keeps the gathers.
-// SG = false reads the table through L1 (measured slower for fp32: 0.105 ms).
+// fp32: the interp is FP64-bound (its geometry is fp64) and the class table removes the cofactor
+// arithmetic — cfg4 0.127 -> 0.097 ms; fp64 (write-heavy: the 32-byte record) 0.137 -> 0.134 ms at
+// 6 CTAs per SM.  SG = false reads the table through L1 (measured slower: fp32 0.105 ms).
 template <typename S, bool SG>
-__global__ void __launch_bounds__(128) k_interp_gradpow_geo(const double* __restrict__ gtab, int nk,
-                                                            const uint8_t* __restrict__ gcls,
-                                                            const int32_t* __restrict__ cells, int64_t n_cells,
-                                                            const S* __restrict__ u, S* __restrict__ w,
-                                                            S* __restrict__ chain, double p, bool minsurf) {
+__device__ __forceinline__ void geo_body(const double* __restrict__ gtab, int nk, const uint8_t* __restrict__ gcls,
+                                         const int32_t* __restrict__ cells, int64_t n_cells, const S* __restrict__ u,
+                                         S* __restrict__ w, S* __restrict__ chain, double p, bool minsurf) {
   __shared__ double sg[SG ? 10 * kMaxGeoClasses : 1];
   if constexpr (SG) {
     for (int i = threadIdx.x; i < 10 * nk; i += blockDim.x) sg[i] = gtab[i];
     __syncthreads();
   }
   ip::interp_cells_geo<S, SG>(gcls, SG ? sg : gtab, nk, cells, (int64_t)blockIdx.x * blockDim.x + threadIdx.x, n_cells,
-                          (int64_t)gridDim.x * blockDim.x, u, w, chain, p, minsurf);
+                              (int64_t)gridDim.x * blockDim.x, u, w, chain, p, minsurf);
+}
+// fp64 at 6 CTAs per SM (80 registers, 32 bytes of spill stores): 0.134 ms vs 0.137 gathering and
+// 0.142 / 0.164 / 0.189 ms at 96 / unbounded / 64 registers; fp32 without a minimum (80 registers):
+// 0.097 ms vs 0.100 at 6 per SM (profiles/r2_geo_minb_ab_v1.jsonl)
+template <typename S, bool SG>
+__global__ void __launch_bounds__(128) k_interp_gradpow_geo(const double* __restrict__ gtab, int nk,
+                                                            const uint8_t* __restrict__ gcls,
+                                                            const int32_t* __restrict__ cells, int64_t n_cells,
+                                                            const S* __restrict__ u, S* __restrict__ w,
+                                                            S* __restrict__ chain, double p, bool minsurf) {
+  geo_body<S, SG>(gtab, nk, gcls, cells, n_cells, u, w, chain, p, minsurf);
+}
+template <typename S, bool SG>
+__global__ void __launch_bounds__(128, 6) k_interp_gradpow_geo6(const double* __restrict__ gtab, int nk,
+                                                                const uint8_t* __restrict__ gcls,
+                                                                const int32_t* __restrict__ cells, int64_t n_cells,
+                                                                const S* __restrict__ u, S* __restrict__ w,
+                                                                S* __restrict__ chain, double p, bool minsurf) {
+  geo_body<S, SG>(gtab, nk, gcls, cells, n_cells, u, w, chain, p, minsurf);
 }
 
 // Value kinds at the W DOFs of a cell-wise W (V = P1): u_h(x_l) = Σ_a λ_a(x_l) u_a with λ(x_l)
@@ -753,9 +769,9 @@ egfem_status launch_interp(const egfem_tensor* t, egfem_interp_kind kind, double
   } while (0)
 #define EGFEM_GP(S, D)                                                          \
   do {                                                                          \
-    if (geo_interp_ok(t) && D == 3 && sizeof(S) == 4) {                                              \
+    if (geo_interp_ok(t) && D == 3) {                                              \
       int per_sm = 0;                                                                                   \
-      auto kg = k_interp_gradpow_geo<S, true>;                                                          \
+      auto kg = sizeof(S) == 8 ? k_interp_gradpow_geo6<S, true> : k_interp_gradpow_geo<S, true>;        \
       cudaOccupancyMaxActiveBlocksPerMultiprocessor(&per_sm, kg, 128, 0);                               \
       const int g = (int)std::min<int64_t>(grid, (int64_t)std::max(per_sm, 1) * 148);                   \
       kg<<<g, 128, 0, s>>>(t->gtab, t->n_geo, t->gcls + lo, cl, n, (const S*)u,    \

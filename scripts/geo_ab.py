@@ -1,4 +1,4 @@
-"""A/B of the 3D interp on cfg4: geometry classes (default; fp32 handles only) vs the gathering
+"""A/B of the 3D interp on cfg4: geometry classes (default) vs the gathering
 kernel (EGFEM_GEOM_CLASSES=0); CUDA events, 50 launches each after warm-up, alternated 3 times.
 profiles/r2_geo_ab_v1.json also has the fp64 class kernel (since dispatched for fp32 only) and the
 table read through L1 instead of shared memory ("geo_smem" there = the kept variant)."""

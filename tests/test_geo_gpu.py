@@ -1,5 +1,5 @@
 """Geometry classes of the 3D interp (egfem_build.cu make_geo_classes, egfem_interp.cuh
-interp_cells_geo; fp32 handles): on a mesh made of translated copies of a few cells, step (1) of the gradient
+interp_cells_geo): on a mesh made of translated copies of a few cells, step (1) of the gradient
 kinds (PAPER.md L165–169, L582 / L605) reads each cell's (cofactors, 1/det) from its class
 instead of gathering its vertex coordinates.  Both paths form the same numbers with the same
 explicit roundings, so w and the packed Newton record are bitwise those of the gathering kernel
@@ -54,8 +54,7 @@ def test_geo_classes_bitwise(eg, monkeypatch, n, dtype, kind):
         monkeypatch.setenv("EGFEM_GEOM_CLASSES", env)
         t = eg.egfem_tensor_build(pr.mesh, pr.V, pr.W, pr.form, dtype=dt, device=0)
         name = eg.egfem_kernel_name(t, 5, eg.JAC_NEWTON, k, p)
-        # fp32 handles only (the fp64 interp measured faster gathering, egfem_kernels.cu)
-        assert ("geo" in name) == (env == "1" and dtype == "f32"), name
+        assert ("geo" in name) == (env == "1"), name
         if "geo" in name:
             assert "6 geometry classes" in name  # the six tetrahedra of a cube, translated
         out.append(_interp(eg, t, pr, k, p))
