@@ -41,6 +41,13 @@ import egfem_inputs as I  # noqa: E402
 # GPU box's host: 1.9e7 nnz/s for cfg4's interp + apply + Newton, 3.7e8 nnz·pairs/s batched)
 ORACLE_SAMPLE_NNZ = 80_000_000
 ORACLE_SAMPLE_NNZ_BATCHED = 3_000_000_000  # nnz·pairs for cfg5
+REFERENCE_STEPS_FULL = 24  # --impl reference: the per-step sample shrinks beyond this many steps (≈100 s of CPU work in all)
+
+
+def reference_budget(budget, steps):
+    """Per-step oracle sample of the reference arm: the cpu_baseline leg's sample up to
+    REFERENCE_STEPS_FULL steps, scaled down after that so --steps K stays within a few minutes."""
+    return budget if steps <= REFERENCE_STEPS_FULL else max(1, budget * REFERENCE_STEPS_FULL // steps)
 
 
 def _peaks():
@@ -869,7 +876,7 @@ def run_reference(args):
     hc = host_cpu()
     if args.config == "cfg5":
         B = pr.batch
-        R, _ = oracle_sample(pr, ORACLE_SAMPLE_NNZ_BATCHED // B)
+        R, _ = oracle_sample(pr, reference_budget(ORACLE_SAMPLE_NNZ_BATCHED, args.steps) // B)
         o = oracle.OracleTensor(pr.mesh, pr.V, pr.W, pr.form, rows=(0, R))
         U = np.ascontiguousarray(pr.u[:B])
         o.apply_batched(U[:1], U[:1])
@@ -882,7 +889,7 @@ def run_reference(args):
         metric = "tensor nonzero-pairs/s (batched action) and achieved HBM GB/s"
         sample = f"cfg5 rows [0,{R}) = {o.nnz} nnz x {B} pairs per step (batched action)"
     else:
-        R, items = oracle_sample(pr, ORACLE_SAMPLE_NNZ)
+        R, items = oracle_sample(pr, reference_budget(ORACLE_SAMPLE_NNZ, args.steps))
         o = oracle.OracleTensor(pr.mesh, pr.V, pr.W, pr.form, rows=(0, R))
         w = o.interp(pr.interp, pr.p, pr.u, items=items)
         o.apply(pr.u, w)
