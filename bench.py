@@ -41,7 +41,7 @@ import egfem_inputs as I  # noqa: E402
 # GPU box's host: 1.9e7 nnz/s for cfg4's interp + apply + Newton, 3.7e8 nnz·pairs/s batched)
 ORACLE_SAMPLE_NNZ = 80_000_000
 ORACLE_SAMPLE_NNZ_BATCHED = 3_000_000_000  # nnz·pairs for cfg5
-REFERENCE_STEPS_FULL = 24  # --impl reference: the per-step sample shrinks beyond this many steps (≈100 s of CPU work in all)
+REFERENCE_STEPS_FULL = 50  # --impl reference: the per-step sample shrinks beyond this many steps (≈3.5 min of CPU work in all)
 
 
 def reference_budget(budget, steps):
