@@ -5,6 +5,9 @@
 #include <cuda_runtime.h>
 #include <stdint.h>
 
+#ifndef EGFEM_INTERP_PFD
+#define EGFEM_INTERP_PFD 0  // A/B: L2 prefetch of the cell records this many grid strides ahead (0 = off)
+#endif
 #ifndef EGFEM_INTERP_EF
 #define EGFEM_INTERP_EF 0  // A/B: 1 = cell records loaded and Newton records stored L2 evict-first, 2 = stores only
 #endif
@@ -318,6 +321,10 @@ __device__ __forceinline__ void interp_cells_geo(const uint8_t* __restrict__ gcl
     int kn;
     gather(cv2, c + stride, nxt, kn);
     cv2 = idx(c + 2 * stride);
+    if constexpr (EGFEM_INTERP_PFD > 0) {
+      const int64_t cp = c + (int64_t)EGFEM_INTERP_PFD * stride;
+      if (cp < cend) asm volatile("prefetch.global.L2 [%0];" ::"l"(reinterpret_cast<const int4*>(cells) + cp));
+    }
     double geo[10];
 #pragma unroll
     for (int v = 0; v < 10; ++v) geo[v] = SG ? sg[v * nk + kc] : __ldg(sg + v * nk + kc);
