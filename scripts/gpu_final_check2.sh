@@ -1,0 +1,8 @@
+#!/bin/bash
+# Final tree: smoke, pytest -m gpu, default bench line, then the ncu launch list of the same command.
+cd $GRAFT_REPO_ROOT
+O=gpurun_out/r2v13; mkdir -p $O
+timeout 300 python __graft_entry__.py smoke > $O/smoke.log 2>&1; echo "smoke rc=$?" >> $O/smoke.log
+timeout 1500 python -m pytest tests -m gpu -q --timeout 900 > $O/pytest_gpu.log 2>&1; echo "pytest rc=$?" >> $O/pytest_gpu.log
+timeout 900 python bench.py > $O/bench.json 2> $O/bench.err; echo "bench rc=$?" >> $O/bench.err
+timeout 900 ncu --metrics gpu__time_duration.sum --clock-control none -c 400 --csv --log-file $O/launches_cfg4.csv python bench.py --steps 3 --warmup 3 --no-cpu-baseline > $O/ncu_launch.log 2>&1; echo "ncu launch rc=$?" >> $O/ncu_launch.log

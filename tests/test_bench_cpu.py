@@ -102,3 +102,17 @@ def test_oracle_sample_rows_and_items():
     V = np.asarray(pr.V.cell_dofs)
     need = np.nonzero((V < R).any(axis=1))[0]
     assert c0 == need.min() and c1 == need.max() + 1
+
+
+def test_reference_budget_bounds_total_work():
+    """--impl reference: the per-step oracle sample is the cpu_baseline leg's up to
+    REFERENCE_STEPS_FULL steps (the driver's K = 20 and the default K = 50 time the same rows),
+    and shrinks as 1 / K beyond that so the total CPU work stays bounded."""
+    import bench
+    full = bench.ORACLE_SAMPLE_NNZ
+    assert bench.reference_budget(full, 20) == full
+    assert bench.reference_budget(full, bench.REFERENCE_STEPS_FULL) == full
+    for K in (100, 400, 10_000):
+        b = bench.reference_budget(full, K)
+        assert 0 < b < full and b * K <= full * bench.REFERENCE_STEPS_FULL
+    assert bench.reference_budget(1, 10_000) == 1
