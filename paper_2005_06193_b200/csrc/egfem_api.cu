@@ -1,5 +1,6 @@
 // C ABI of libegfem.so: validation, handle lifetime, dispatch, multi-GPU
 // partitioning.  See include/egfem.h for the contract of every entry point.
+#include <nvtx3/nvToolsExt.h>
 #include <algorithm>
 #include <cmath>
 #include <atomic>
@@ -111,6 +112,15 @@ egfem_status validate_space(const egfem_mesh* m, const egfem_space* S, const cha
 
 }  // namespace
 
+// NVTX range around an API call (SURVEY §5 tracing): header-only nvtx3, a no-op pointer check
+// when no tool is attached; host-side only, so it is legal inside stream capture.
+struct NvtxRange {
+  explicit NvtxRange(const char* name) { nvtxRangePushA(name); }
+  ~NvtxRange() { nvtxRangePop(); }
+  NvtxRange(const NvtxRange&) = delete;
+  NvtxRange& operator=(const NvtxRange&) = delete;
+};
+
 void set_error(const std::string& msg) { g_last_error = msg; }
 void count_launch(int n) { g_launches.fetch_add((uint64_t)n, std::memory_order_relaxed); }
 
@@ -178,6 +188,7 @@ egfem_status egfem_tensor_build(const egfem_mesh* mesh, const egfem_space* V, co
     cudaGetLastError();
     return fail(EGFEM_ERR_INVALID_ARGUMENT, "no such CUDA device");
   }
+  NvtxRange nv("egfem_tensor_build");
   DeviceGuard g(device);
   if (!g.ok) return fail(EGFEM_ERR_CUDA, "cudaSetDevice failed");
   egfem_tensor* t = new egfem_tensor();
@@ -236,6 +247,7 @@ egfem_status egfem_tensor_from_coo(int64_t n_u, int64_t n_f, int64_t nnz, const 
     cudaGetLastError();
     return fail(EGFEM_ERR_INVALID_ARGUMENT, "no such CUDA device");
   }
+  NvtxRange nv("egfem_tensor_from_coo");
   DeviceGuard g(device);
   egfem_tensor* t = new egfem_tensor();
   t->device = device;
@@ -273,6 +285,7 @@ egfem_status egfem_tensor_from_coo(int64_t n_u, int64_t n_f, int64_t nnz, const 
 
 egfem_status egfem_tensor_destroy(egfem_tensor* t) {
   if (!t) return EGFEM_OK;
+  NvtxRange nv("egfem_tensor_destroy");
   DeviceGuard g(t->device);
   free_tensor(t);
   delete t;
@@ -303,6 +316,7 @@ egfem_status egfem_tensor_export(const egfem_tensor* t, int64_t* t_row_ptr, int3
   if (!t) return fail(EGFEM_ERR_INVALID_ARGUMENT, "tensor is NULL");
   if (slot_ik && !t->w_is_v) return fail(EGFEM_ERR_UNSUPPORTED, "slot_ik needs W = V numbering");
   if (loc && !(t->has_mesh && t->w_p0)) return fail(EGFEM_ERR_UNSUPPORTED, "loc needs W = P0");
+  NvtxRange nv("egfem_tensor_export");
   DeviceGuard g(t->device);
   return export_arrays(t, t_row_ptr, t_j, t_k, t_val, csr_row_ptr, csr_col, slot_ij, slot_ik, loc);
 }
@@ -357,6 +371,7 @@ egfem_status egfem_interp(const egfem_tensor* t, egfem_interp_kind kind, double 
                           void* chain, egfem_stream_t stream) {
   egfem_status st = interp_check(t, kind, p, u, w, chain);
   if (st) return st;
+  NvtxRange nv("egfem_interp");
   DeviceGuard g(t->device);
   return launch_interp(t, kind, p, u, w, chain, 0, interp_items(t, kind), (cudaStream_t)stream);
 }
@@ -367,6 +382,7 @@ egfem_status egfem_interp_range(const egfem_tensor* t, egfem_interp_kind kind, d
   if (st) return st;
   if (lo < 0 || hi < lo || hi > interp_items(t, kind))
     return fail(EGFEM_ERR_INVALID_ARGUMENT, "interp range outside [0, n_items]");
+  NvtxRange nv("egfem_interp_range");
   DeviceGuard g(t->device);
   return launch_interp(t, kind, p, u, w, chain, lo, hi, (cudaStream_t)stream);
 }
@@ -377,6 +393,7 @@ egfem_status egfem_apply(const egfem_tensor* t, const void* u, const void* w, vo
   if ((st = check_dev_ptr(t, u, "u", true)) || (st = check_dev_ptr(t, w, "w", true)) ||
       (st = check_dev_ptr(t, r, "r", true)))
     return st;
+  NvtxRange nv("egfem_apply");
   DeviceGuard g(t->device);
   return launch_tile(t, true, 0, EGFEM_INTERP_IDENTITY, 0.0, u, w, nullptr, r, nullptr, (cudaStream_t)stream);
 }
@@ -393,6 +410,7 @@ egfem_status egfem_apply_batched(const egfem_tensor* t, int32_t batch, egfem_lay
   if ((st = check_dev_ptr(t, U, "U", true)) || (st = check_dev_ptr(t, W, "W", true)) ||
       (st = check_dev_ptr(t, R, "R", true)))
     return st;
+  NvtxRange nv("egfem_apply_batched");
   DeviceGuard g(t->device);
   return launch_batched(t, batch, layout, U, W, R, (cudaStream_t)stream);
 }
@@ -500,6 +518,7 @@ egfem_status egfem_jacobian(const egfem_tensor* t, egfem_jac_mode mode, egfem_in
   int code = 0;
   if ((st = jac_mode_code(t, mode, kind, p, u, chain, &code))) return st;
   if ((st = check_w_newton(t, code, kind, w, chain))) return st;
+  NvtxRange nv("egfem_jacobian");
   DeviceGuard g(t->device);
   return launch_tile(t, false, code, kind, p, u, w, chain, nullptr, csr_vals, (cudaStream_t)stream);
 }
@@ -515,6 +534,7 @@ egfem_status egfem_apply_jacobian(const egfem_tensor* t, egfem_jac_mode mode, eg
   int code = 0;
   if ((st = jac_mode_code(t, mode, kind, p, u, chain, &code))) return st;
   if ((st = check_w_newton(t, code, kind, w, chain))) return st;
+  NvtxRange nv("egfem_apply_jacobian");
   DeviceGuard g(t->device);
   return launch_tile(t, true, code, kind, p, u, w, chain, r, csr_vals, (cudaStream_t)stream);
 }
@@ -527,6 +547,7 @@ egfem_status egfem_step(const egfem_tensor* t, egfem_interp_kind kind, double p,
   int code = 0;
   if ((st = jac_mode_code(t, EGFEM_JAC_NEWTON, kind, p, u, chain, &code))) return st;
   if ((st = check_w_newton(t, code, kind, w, chain))) return st;
+  NvtxRange nv("egfem_step");
   DeviceGuard g(t->device);
   const cudaStream_t s = (cudaStream_t)stream;
   st = launch_step(t, kind, p, u, w, chain, r, csr_vals, s);
@@ -549,6 +570,7 @@ egfem_status egfem_apply_jacobian_rows(const egfem_tensor* t, egfem_jac_mode mod
   int code = 0;
   if ((st = jac_mode_code(t, mode, kind, p, u, chain, &code))) return st;
   if ((st = check_w_newton(t, code, kind, w, chain))) return st;
+  NvtxRange nv("egfem_apply_jacobian_rows");
   DeviceGuard g(t->device);
   return launch_tile_rows(t, row_lo, row_hi, true, code, kind, p, u, w, chain, r, csr_vals, (cudaStream_t)stream);
 }
@@ -601,6 +623,7 @@ egfem_status egfem_bilinear_build(const egfem_tensor* t, void* b_vals, egfem_str
     return fail(EGFEM_ERR_UNSUPPORTED, "bilinear form of a partitioned tensor: build it on the global tensor");
   if (t->has_mesh && (t->form == EGFEM_FORM_CONV_J || t->form == EGFEM_FORM_PLAP))
     return fail(EGFEM_ERR_UNSUPPORTED, "the u-slot of this form is differentiated: T·₂1 = 0 (Σ_j ∇φ_j = 0)");
+  NvtxRange nv("egfem_bilinear_build");
   DeviceGuard g(t->device);
   return launch_bilinear_build(t, b_vals, (cudaStream_t)stream);
 }
@@ -612,6 +635,7 @@ egfem_status egfem_csr_spmv(const egfem_tensor* t, const void* vals, const void*
       (st = check_dev_ptr(t, y, "y", true)))
     return st;
   if (x == y) return fail(EGFEM_ERR_INVALID_ARGUMENT, "x and y must not alias");
+  NvtxRange nv("egfem_csr_spmv");
   DeviceGuard g(t->device);
   return launch_spmv(t, vals, x, y, (cudaStream_t)stream);
 }
@@ -629,6 +653,7 @@ egfem_status egfem_bilinear_jacobian(const egfem_tensor* t, const void* b_vals, 
   if (kind == EGFEM_INTERP_SQUARE) mode = 1;
   if (kind == EGFEM_INTERP_RECIPROCAL) mode = 2;
   if (mode < 0) return fail(EGFEM_ERR_UNSUPPORTED, "bilinear Jacobian: IDENTITY, SQUARE or RECIPROCAL");
+  NvtxRange nv("egfem_bilinear_jacobian");
   DeviceGuard g(t->device);
   return launch_scale_cols(t, b_vals, mode, p, u, csr_vals, (cudaStream_t)stream);
 }
@@ -642,6 +667,7 @@ egfem_status egfem_halo_pack(const egfem_tensor* local, const int32_t* d_idx, in
   if ((st = check_dev_ptr(local, d_idx, "idx", true)) || (st = check_dev_ptr(local, u_local, "u_local", true)) ||
       (st = check_dev_ptr(local, send_buf, "send_buf", true)))
     return st;
+  NvtxRange nv("egfem_halo_pack");
   DeviceGuard g(local->device);
   return launch_halo(local, d_idx, n, u_local, send_buf, true, (cudaStream_t)stream);
 }
@@ -655,6 +681,7 @@ egfem_status egfem_halo_unpack(const egfem_tensor* local, const int32_t* d_idx, 
   if ((st = check_dev_ptr(local, d_idx, "idx", true)) || (st = check_dev_ptr(local, recv_buf, "recv_buf", true)) ||
       (st = check_dev_ptr(local, u_local, "u_local", true)))
     return st;
+  NvtxRange nv("egfem_halo_unpack");
   DeviceGuard g(local->device);
   return launch_halo(local, d_idx, n, recv_buf, u_local, false, (cudaStream_t)stream);
 }
@@ -687,6 +714,7 @@ egfem_status egfem_partition(const egfem_tensor* G, int32_t nranks, int32_t rank
   if (G->has_mesh && !G->w_p0 && !G->w_is_v)
     return fail(EGFEM_ERR_UNSUPPORTED, "row partition needs W = V or W = P0");
   if (G->wfam == EGFEM_QUAD) return fail(EGFEM_ERR_UNSUPPORTED, "row partition of QUAD W is not implemented");
+  NvtxRange nv("egfem_partition");
   DeviceGuard g(G->device);
   // host copies of the integer structure (offline)
   std::vector<int64_t> row_fib(G->n_u + 1);

@@ -8,5 +8,5 @@ TU=$2; base=$(basename $TU .cu)
 nvcc -O3 -std=c++17 -gencode arch=compute_100a,code=sm_100a -lineinfo -Xcompiler -fPIC $3 -I include \
   -c -o $L/variants/obj/$1_$base.o paper_2005_06193_b200/csrc/$TU
 objs=""; for o in $L/obj/*.o; do [ "$(basename $o)" = "$base.o" ] && objs="$objs $L/variants/obj/$1_$base.o" || objs="$objs $o"; done
-nvcc -shared -gencode arch=compute_100a,code=sm_100a -Xcompiler -fPIC -o $L/variants/$1.so $objs -lnvrtc
+nvcc -shared -gencode arch=compute_100a,code=sm_100a -Xcompiler -fPIC -o $L/variants/$1.so $objs -lnvrtc -ldl
 echo built $L/variants/$1.so

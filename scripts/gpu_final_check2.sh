@@ -1,7 +1,7 @@
 #!/bin/bash
 # Final tree: smoke, pytest -m gpu, default bench line, then the ncu launch list of the same command.
 cd $GRAFT_REPO_ROOT
-O=gpurun_out/r2v13; mkdir -p $O
+O=gpurun_out/r2v14; mkdir -p $O
 timeout 300 python __graft_entry__.py smoke > $O/smoke.log 2>&1; echo "smoke rc=$?" >> $O/smoke.log
 timeout 1500 python -m pytest tests -m gpu -q --timeout 900 > $O/pytest_gpu.log 2>&1; echo "pytest rc=$?" >> $O/pytest_gpu.log
 timeout 900 python bench.py > $O/bench.json 2> $O/bench.err; echo "bench rc=$?" >> $O/bench.err
