@@ -33,6 +33,8 @@
  *     on different streams.
  *   - No floating-point atomics: results are bitwise reproducible run to run.
  *   - csr_vals is fully overwritten, never accumulated into.
+ *   - Tracing: every compute call opens an NVTX range named after the function for the
+ *     duration of the host call (a no-op without an attached profiler).
  */
 #ifndef EGFEM_H
 #define EGFEM_H
